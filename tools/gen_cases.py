@@ -1,0 +1,235 @@
+"""Seeded synthetic grids of the BASELINE.json config sizes -> cases/*.m.
+
+No real case300 / case2383wp / case9241pegase file exists on the box and there
+is no network (SURVEY.md §7 hard part 5), so the configs run on synthetic
+meshed grids of the same bus / branch / generator counts:
+
+  synth300   300 bus /    411 branch /   69 gen   (IEEE case300-sized)
+  synth2383  2383 bus /  2896 branch /  327 gen   (case2383wp-sized)
+  synth9241  9241 bus / 16049 branch / 1445 gen   (case9241pegase-sized)
+
+Construction (deterministic for a seed): buses uniform in a square of unit
+density; Delaunay triangulation; its Euclidean MST plus the shortest remaining
+Delaunay edges up to the branch count; series x proportional to length with
+X/R in [4, 10]; 10% of branches are off-nominal transformers; 70% of buses
+carry load; generators are spread uniformly and each is dispatched to the load
+of the buses closest to it in hops, so transfers stay local and the base case
+is well conditioned (the survey's naive generator was not, App. A).  The base
+case is solved from flat start with the scipy newtonpf and its voltages are
+stored rounded (Vm 4 decimals, Va 3 decimals), like the published MATPOWER
+files, which gives the reference's warm-start V0 rule (grid.hpp:331-342) the
+same meaning it has for real cases.
+
+Usage: python tools/gen_cases.py  [--only synth300 ...]
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.csgraph as csg
+from scipy.spatial import Delaunay
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+
+from newtonpf_scipy import newtonpf  # noqa: E402
+
+CONFIGS = {
+    "synth300": dict(n_bus=300, n_branch=411, n_gen=69, seed=300),
+    "synth2383": dict(n_bus=2383, n_branch=2896, n_gen=327, seed=2383),
+    "synth9241": dict(n_bus=9241, n_branch=16049, n_gen=1445, seed=9241),
+    "synth30": dict(n_bus=30, n_branch=41, n_gen=6, seed=30),
+    "synth118": dict(n_bus=118, n_branch=186, n_gen=54, seed=118),
+}
+
+
+def _edges(pts, n_branch, rng):
+    tri = Delaunay(pts)
+    e = set()
+    for s in tri.simplices:
+        for a, b in ((s[0], s[1]), (s[1], s[2]), (s[0], s[2])):
+            e.add((min(a, b), max(a, b)))
+    e = np.array(sorted(e), np.int64)
+    L = np.linalg.norm(pts[e[:, 0]] - pts[e[:, 1]], axis=1)
+    n = pts.shape[0]
+    G = sp.coo_matrix((L, (e[:, 0], e[:, 1])), shape=(n, n)).tocsr()
+    T = csg.minimum_spanning_tree(G).tocoo()
+    mst = {(min(a, b), max(a, b)) for a, b in zip(T.row, T.col)}
+    chosen = sorted(mst)
+    order = np.argsort(L, kind="stable")
+    for i in order:
+        if len(chosen) >= n_branch:
+            break
+        key = (int(e[i, 0]), int(e[i, 1]))
+        if key not in mst:
+            chosen.append(key)
+    chosen = np.array(chosen[:n_branch], np.int64)
+    perm = rng.permutation(len(chosen))
+    return chosen[perm]
+
+
+def build(n_bus, n_branch, n_gen, seed, xpu=0.01, xfloor=0.001, xtr=0.01, bpu=0.005):
+    rng = np.random.default_rng(seed)
+    side = np.sqrt(n_bus)
+    pts = rng.uniform(0.0, side, (n_bus, 2))
+    br = _edges(pts, n_branch, rng)
+    nb = br.shape[0]
+    length = np.linalg.norm(pts[br[:, 0]] - pts[br[:, 1]], axis=1)
+    x = np.round(xpu * length * rng.uniform(0.8, 1.2, nb), 5) + 1e-4
+    r = np.round(x / rng.uniform(4.0, 10.0, nb), 5)
+    b = np.round(bpu * length * rng.uniform(0.5, 1.5, nb), 4)
+    x = np.maximum(x, xfloor)
+    is_tr = rng.uniform(size=nb) < 0.10
+    tap = np.where(is_tr, np.round(rng.uniform(0.97, 1.03, nb), 3), 0.0)
+    # transformers: realistic leakage reactance, no charging
+    x = np.where(is_tr, np.maximum(x, np.round(xtr * rng.uniform(1.0, 3.0, nb), 4)), x)
+    r = np.where(is_tr, np.round(x / 30.0, 5), r)
+    b = np.where(is_tr, 0.0, b)
+    # loads
+    loaded = rng.uniform(size=n_bus) < 0.7
+    pd = np.where(loaded, np.round(rng.lognormal(np.log(15.0), 0.6, n_bus), 2), 0.0)
+    qd = np.round(pd * rng.uniform(0.1, 0.4, n_bus), 2)
+    bs = np.where(rng.uniform(size=n_bus) < 0.05, np.round(rng.uniform(5, 20, n_bus), 1), 0.0)
+    # generators: slack nearest the centre, then greedy k-center on hop distance
+    # (random tie-breaks) so no load pocket is far from voltage support
+    centre = int(np.argmin(np.linalg.norm(pts - side / 2, axis=1)))
+    A = sp.coo_matrix((np.ones(2 * nb), (np.r_[br[:, 0], br[:, 1]], np.r_[br[:, 1], br[:, 0]])),
+                      shape=(n_bus, n_bus)).tocsr()
+    gl = [centre]
+    dmin = csg.shortest_path(A, unweighted=True, indices=[centre])[0]
+    jitter = rng.uniform(0.0, 0.5, n_bus)
+    while len(gl) < n_gen:
+        nxt = int(np.argmax(dmin + jitter))
+        gl.append(nxt)
+        dmin = np.minimum(dmin, csg.shortest_path(A, unweighted=True, indices=[nxt])[0])
+    gbus = np.r_[centre, np.sort(gl[1:])]
+    # hop-distance Voronoi regions for local dispatch
+    dist = csg.shortest_path(A, unweighted=True, indices=gbus)
+    owner = np.argmin(dist, axis=0)
+    pg_load = np.array([pd[owner == g].sum() for g in range(n_gen)])
+    vg = np.full(n_gen, 1.02)
+    kind = np.ones(n_bus, np.int64)
+    kind[gbus] = 2
+    kind[centre] = 3
+    return dict(pts=pts, br=br, r=r, x=x, b=b, tap=tap, pd=pd, qd=qd, bs=bs, gbus=gbus,
+                pg_load=pg_load, pg=np.round(pg_load, 2), vg=vg, kind=kind, owner=owner)
+
+
+def ybus_np(n, g):
+    br = g["br"]
+    ys = 1.0 / (g["r"] + 1j * g["x"])
+    ysh = 1j * g["b"] / 2
+    tap = np.where(g["tap"] == 0.0, 1.0, g["tap"])
+    f, t = br[:, 0], br[:, 1]
+    Yff = (ys + ysh) / tap**2
+    Ytt = ys + ysh
+    Yft = -ys / tap
+    Ytf = -ys / tap
+    rows = np.r_[f, t, f, t, np.arange(n)]
+    cols = np.r_[f, t, t, f, np.arange(n)]
+    vals = np.r_[Yff, Ytt, Yft, Ytf, 1j * g["bs"] / 100.0]
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+
+
+def _branch_losses(n, g, V):
+    br = g["br"]
+    ys = 1.0 / (g["r"] + 1j * g["x"])
+    ysh = 1j * g["b"] / 2
+    tap = np.where(g["tap"] == 0.0, 1.0, g["tap"])
+    f, t = br[:, 0], br[:, 1]
+    If = (ys + ysh) / tap**2 * V[f] - ys / tap * V[t]
+    It = -ys / tap * V[f] + (ys + ysh) * V[t]
+    return (V[f] * np.conj(If) + V[t] * np.conj(It)).real * 100.0  # MW
+
+
+def solve_base(n, g, scales=(0.25, 0.5, 0.75, 1.0), rounds=3):
+    """Load continuation with loss re-dispatch by region.
+
+    Each generator serves the load of its hop-distance region; a single slack
+    would otherwise have to push all network losses through a weakly meshed
+    grid (angle spreads of >1000 degrees on the 2383-bus grid).  At every load
+    step the branch losses are attributed half to each endpoint's region and
+    added to that region's generator, then the case is re-solved (warm start)."""
+    Y = ybus_np(n, g)
+    ref = int(np.where(g["kind"] == 3)[0][0])
+    pv = np.where(g["kind"] == 2)[0]
+    pq = np.where(g["kind"] == 1)[0]
+    V = np.ones(n, complex)
+    V[g["gbus"]] = g["vg"]
+    base = g["pg_load"]
+    loss_reg = np.zeros_like(base)
+    pd0, qd0 = g["pd"], g["qd"]
+    prev = scales[0]
+    for sc in scales:
+        loss_reg = loss_reg * (sc / prev) ** 2  # losses grow ~ quadratically with load
+        prev = sc
+        for _ in range(rounds):
+            pg = sc * base + loss_reg
+            gen_p = np.zeros(n)
+            np.add.at(gen_p, g["gbus"], pg)
+            S = (gen_p - sc * pd0 - 1j * sc * qd0) / 100.0
+            V, ok, it = newtonpf(Y, S, V, ref, pv, pq, tol=1e-8, max_it=30)
+            if not ok:
+                return V, ok, it
+            bl = _branch_losses(n, g, V)
+            loss_reg = (np.bincount(g["owner"][g["br"][:, 0]], 0.5 * bl, len(base))
+                        + np.bincount(g["owner"][g["br"][:, 1]], 0.5 * bl, len(base)))
+    # final solve of the stored dispatch, warm-started from the continuation
+    g["pg"] = np.round(base + loss_reg, 2)
+    gen_p = np.zeros(n)
+    np.add.at(gen_p, g["gbus"], g["pg"])
+    S = (gen_p - pd0 - 1j * qd0) / 100.0
+    V, ok, it = newtonpf(Y, S, V, ref, pv, pq, tol=1e-8, max_it=30)
+    return V, ok, it
+
+
+def to_matpower(name, n, g, V):
+    L = [f"function mpc = {name}",
+         f"% synthetic {n}-bus grid made by tools/gen_cases.py (seeded, deterministic)",
+         "mpc.version = '2';", "mpc.baseMVA = 100;", "", "%% bus data",
+         "%\tbus_i\ttype\tPd\tQd\tGs\tBs\tarea\tVm\tVa\tbaseKV\tzone\tVmax\tVmin", "mpc.bus = ["]
+    vm = np.round(np.abs(V), 4)
+    va = np.round(np.degrees(np.angle(V)), 3)
+    for i in range(n):
+        L.append(f"\t{i + 1}\t{g['kind'][i]}\t{g['pd'][i]:.2f}\t{g['qd'][i]:.2f}\t0\t{g['bs'][i]:.1f}"
+                 f"\t1\t{vm[i]:.4f}\t{va[i]:.3f}\t230\t1\t1.1\t0.9;")
+    L += ["];", "", "%% generator data",
+          "%\tbus\tPg\tQg\tQmax\tQmin\tVg\tmBase\tstatus\tPmax\tPmin", "mpc.gen = ["]
+    for k, bi in enumerate(g["gbus"]):
+        L.append(f"\t{bi + 1}\t{g['pg'][k]:.2f}\t0\t999\t-999\t{g['vg'][k]:.3f}\t100\t1\t999\t0;")
+    L += ["];", "", "%% branch data",
+          "%\tfbus\ttbus\tr\tx\tb\trateA\trateB\trateC\tratio\tangle\tstatus", "mpc.branch = ["]
+    for k, (f, t) in enumerate(g["br"]):
+        L.append(f"\t{f + 1}\t{t + 1}\t{g['r'][k]:.5f}\t{g['x'][k]:.5f}\t{g['b'][k]:.4f}\t0\t0\t0"
+                 f"\t{g['tap'][k]:g}\t0\t1;")
+    L += ["];", ""]
+    return "\n".join(L)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", nargs="*")
+    ap.add_argument("--out", default=os.path.join(ROOT, "cases"))
+    a = ap.parse_args()
+    for name, cfg in CONFIGS.items():
+        if a.only and name not in a.only:
+            continue
+        g = build(**cfg)
+        V, ok, it = solve_base(cfg["n_bus"], g)
+        spread = np.degrees(np.angle(V)).max() - np.degrees(np.angle(V)).min()
+        print(f"{name}: converged={ok} it={it} |V| [{np.abs(V).min():.3f},{np.abs(V).max():.3f}] "
+              f"angle spread {spread:.1f} deg")
+        if not ok:
+            raise SystemExit(f"{name}: base case did not converge")
+        with open(os.path.join(a.out, f"{name}.m"), "w") as fh:
+            fh.write(to_matpower(name, cfg["n_bus"], g, V))
+
+
+if __name__ == "__main__":
+    main()
