@@ -1,0 +1,145 @@
+/* gbnr.h -- C ABI of the B200-native batched Newton-Raphson power-flow solver.
+ *
+ * Drop-in boundary for the reference's hot path.  The
+ * reference has no FFI; its in-library boundary is
+ *     nr_solve_batch(case, symbolic, tapes, cfg) -> TaskResult[]
+ * fed by batch_runtime.initialize / run, with the inputs
+ * built by grid_model (grid.hpp:208-344) and laid out as BatchTape
+ * (batch_tape.hpp:6-9).  The paper's caller reaches the same solver from Python
+ * through Cython with numpy buffers.  This header replaces
+ * that boundary with plain pointers:
+ *
+ *   gbnr_plan_create   <- batch_runtime.initialize: Jacobian
+ *                         pattern, amd_order (amd.hpp:29),
+ *                         factorize_initial, build_level_schedule
+ *                         (SPEC.md:301-309), build_scatter_lookup (sparse.hpp:237)
+ *   gbnr_solve         <- nr_solve_batch + TaskResult (:382-385)
+ *   gbnr_build_ybus    <- build_ybus (grid.hpp:208-243)
+ *   gbnr_amd_order     <- amd_order (amd.hpp:29-157)
+ *   gbnr_plan_stats    <- cmd_inspect counters
+ *   gbnr_refactor      <- refactorize_batch, LU-only microbenchmark
+ *
+ * Conventions
+ *  - Batched arrays are element-major with the task index innermost
+ *    (value(elem, task) at elem * n_tasks + task), exactly BatchTape.
+ *    n_*sets in {1, n_tasks}: one shared set broadcast to all tasks, or one
+ *    per task (ProfileBatch.n_sets, grid.hpp:292, :301-302).
+ *  - Voltages are polar (|V| p.u., angle rad) as PolarVoltageBatch;
+ *    Sbus = p0 + j q0 is the specified injection in p.u. (grid.hpp:326-327).
+ *  - Unknown/equation order is MATPOWER's: [theta(pv;pq), |V|(pq)].
+ *  - Return codes map core.hpp:32-65: 0 ok, 1 parse, 2 structural, 3 config,
+ *    4 singular initial factorization, 5 CUDA.  No C++ exception crosses the
+ *    ABI.  Per-task numerical failure goes to status_out, never to the return
+ *    code (core.hpp:33-34).
+ *  - A plan is immutable after creation; calls on one plan serialize.  One plan
+ *    per device; multi-GPU = one host thread (or process) per device.
+ *  - There is no CPU fallback: a plan created with device >= 0 runs only on the
+ *    GPU; gbnr_solve on a host-only plan (device = -1) returns 3.
+ */
+#ifndef GBNR_H
+#define GBNR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GBNR_OK 0
+#define GBNR_EPARSE 1
+#define GBNR_ESTRUCT 2
+#define GBNR_ECONFIG 3
+#define GBNR_ESINGULAR 4
+#define GBNR_ECUDA 5
+
+/* per-task status (TaskResult.status) */
+#define GBNR_CONVERGED 0
+#define GBNR_DIVERGED 1
+#define GBNR_SINGULAR 2
+
+typedef struct gbnr_plan gbnr_plan;
+
+typedef struct gbnr_options {
+    double tol;            /* mismatch infinity-norm tolerance, p.u. (default 1e-8)   */
+    int32_t max_iter;      /* Newton iterations (default 10)                          */
+    double pivot_tol;      /* threshold partial pivoting (default 1e-3) */
+    double singular_tol;   /* refactor pivot flag, relative (default 1e-14)          */
+    int32_t device;        /* CUDA ordinal; -1 = host-only plan (symbolic only)      */
+    int32_t lu_warps;      /* warps per task tile in LU / FS-BS (0 = default)        */
+    int32_t profile;       /* 1 = record per-kernel CUDA-event timings              */
+    int32_t reserved[5];
+} gbnr_options;
+
+void gbnr_default_options(gbnr_options* opt);
+const char* gbnr_last_error(void);
+const char* gbnr_version(void);
+
+/* MATPOWER branch model Ybus (grid.hpp:195-243).  Branch endpoints are internal
+ * 0-based bus indices.  indptr [n_bus+1]; indices/diag/y_re/y_im need capacity
+ * n_bus + 2*n_branch; *nnz_out receives nnz. */
+int gbnr_build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* from, const int32_t* to,
+                    const double* r, const double* x, const double* b, const double* tap,
+                    const double* shift_deg, const uint8_t* in_service, const double* gs,
+                    const double* bs, double base_mva, int32_t* indptr, int32_t* indices,
+                    int32_t* diag, double* y_re, double* y_im, int32_t* nnz_out);
+
+/* Fill-reducing ordering on a square CCS pattern (amd.hpp:29-157); fwd[old] = new. */
+int gbnr_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd);
+
+/* One-time symbolic analysis + device setup.  (y_re, y_im) are the Ybus values
+ * of the representative task and (vm0, va0) its start voltages [n_bus]; they
+ * fix the pivot sequence of the initial factorization. */
+int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indices,
+                     const double* y_re, const double* y_im, int32_t ref, const int32_t* pv,
+                     int32_t n_pv, const int32_t* pq, int32_t n_pq, const double* vm0,
+                     const double* va0, const gbnr_options* opt, gbnr_plan** out);
+void gbnr_plan_destroy(gbnr_plan* plan);
+
+/* out[16]: nJ, nnzJ, nnzLU, nnzL, nnzU, D (VMAD element updates), flops_lu,
+ * levels_lu, levels_fs, levels_bs, offdiag_pivots, npvpq, n_fill, max_col,
+ * max_udeps, nnzY */
+int gbnr_plan_stats(const gbnr_plan* plan, int64_t* out);
+/* row_fwd/col_fwd [nJ] (J index -> LU index), col_ptr [nJ+1], row_ix [nnzLU],
+ * level [nJ]; any pointer may be NULL. */
+int gbnr_plan_export(const gbnr_plan* plan, int32_t* row_fwd, int32_t* col_fwd, int32_t* col_ptr,
+                     int32_t* row_ix, int32_t* level);
+
+/* Batched Newton-Raphson, host buffers in and out (H2D, solve, D2H).
+ *   y_re/y_im [nnzY][n_ysets] (n_ysets must be 1 in this version),
+ *   p0/q0 [n_bus][n_ssets], vm0/va0 [n_bus][n_vsets],
+ *   vm_out/va_out [n_bus][n_tasks], iterations/converged/status/max_mismatch [n_tasks].
+ * iterations follow MATPOWER: 0 if V0 already converged, else the number of
+ * linear solves; max_iter for diverged tasks. */
+int gbnr_solve(gbnr_plan* plan, int32_t n_tasks, const double* y_re, const double* y_im,
+               int32_t n_ysets, const double* p0, const double* q0, int32_t n_ssets,
+               const double* vm0, const double* va0, int32_t n_vsets, double* vm_out,
+               double* va_out, int32_t* iterations_out, uint8_t* converged_out,
+               int32_t* status_out, double* max_mismatch_out);
+
+/* Split form of gbnr_solve for device-resident measurement:
+ * gbnr_stage copies inputs to the device, gbnr_run solves on them (blocking
+ * until done), gbnr_fetch copies results back. */
+int gbnr_stage(gbnr_plan* plan, int32_t n_tasks, const double* p0, const double* q0,
+               int32_t n_ssets, const double* vm0, const double* va0, int32_t n_vsets);
+int gbnr_run(gbnr_plan* plan);
+int gbnr_fetch(gbnr_plan* plan, double* vm_out, double* va_out, int32_t* iterations_out,
+               uint8_t* converged_out, int32_t* status_out, double* max_mismatch_out);
+
+/* Per-kernel device time of the last gbnr_run/gbnr_solve when opt.profile=1.
+ * out[0..5] ms: npm, jacobian, lu, fsbs, vupdate, total; out[6..11] launches of
+ * the same kernels; out[12] Newton iterations executed; out[13] tasks. */
+int gbnr_last_timing(const gbnr_plan* plan, double* out);
+
+/* LU-only microbenchmark / parity: the Jacobian at the staged
+ * voltages (gbnr_stage) is scattered once into the A tape, then `reps` batched
+ * refactorizations A -> LU run back to back (out of place, so every rep does
+ * the full work); lu_out [nnzLU][n_tasks] (may be NULL), flags_out [n_tasks]
+ * (pivot flagged, may be NULL), ms_out = mean device ms per refactorization
+ * (CUDA events on the solver stream). */
+int gbnr_refactor(gbnr_plan* plan, int32_t reps, double* lu_out, uint8_t* flags_out,
+                  double* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

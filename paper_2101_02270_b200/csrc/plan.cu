@@ -1,0 +1,474 @@
+// plan.cu -- the gbnr_plan object and the extern "C" boundary (include/gbnr.h).
+//
+// A plan owns the frozen symbolic state (symbolic.cpp) replicated on its
+// device, the per-batch tapes, one CUDA stream and pinned scratch.  The Newton
+// loop is driven from the host: one launch per kernel per iteration, and one
+// 4-byte device->host read of the active-task count per iteration to stop as
+// soon as every task has finished (PAPER.md:193 checked convergence on the
+// CPU; here the check itself runs on the device, only the count comes back).
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/gbnr.h"
+#include "kernels.hpp"
+#include "symbolic.hpp"
+
+using gbnr::Error;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define CK(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw Error(GBNR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return GBNR_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return GBNR_ECONFIG;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GBNR_ECONFIG;
+    }
+}
+
+template <class T>
+T* dev_upload(std::vector<void*>& owned, const std::vector<T>& h) {
+    T* d = nullptr;
+    const size_t bytes = std::max<size_t>(h.size(), 1) * sizeof(T);
+    CK(cudaMalloc(&d, bytes));
+    owned.push_back(d);
+    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+
+enum Phase { kNpm = 0, kJac, kLu, kFsbs, kVupd, kPhases };
+
+}  // namespace
+
+struct gbnr_plan {
+    gbnr::Symbolic sym;
+    gbnr_options opt{};
+    gbnr::LaunchCfg cfg;
+    bool on_device = false;
+    cudaStream_t stream = nullptr;
+    std::vector<void*> owned;     // structure buffers
+    double* d_scratch = nullptr;  // [n] staging for broadcast sets
+    std::vector<void*> batch;     // per-batch tapes
+    int32_t cap_tiles = 0;        // allocated tile capacity
+    bool shared_s = true;         // p0/q0 broadcast mode of the staged batch
+    bool staged = false;
+    gbnr::DevView v{};
+    int32_t* h_count = nullptr;   // pinned
+    double timing[16] = {0};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    ~gbnr_plan() {
+        if (!on_device) return;
+        cudaSetDevice(opt.device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (void* p : batch) cudaFree(p);
+        for (void* p : owned) cudaFree(p);
+        if (h_count) cudaFreeHost(h_count);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void upload_structure() {
+        CK(cudaSetDevice(opt.device));
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&h_count, sizeof(int32_t) * 64));
+        CK(cudaEventCreate(&ev0));
+        CK(cudaEventCreate(&ev1));
+        gbnr::configure_kernels(cfg);
+        const gbnr::Symbolic& s = sym;
+        CK(cudaMalloc(&d_scratch, size_t(s.n) * sizeof(double)));
+        owned.push_back(d_scratch);
+        v.n = s.n;
+        v.nJ = s.nJ;
+        v.nnzY = s.nnzY;
+        v.n_rows = static_cast<int32_t>(s.rows.size());
+        v.nnzLU = static_cast<int32_t>(s.nnzLU);
+        v.nA = static_cast<int32_t>(s.nnzJ);
+        v.yp = dev_upload(owned, s.yp);
+        v.yi = dev_upload(owned, s.yi);
+        v.rows = dev_upload(owned, s.rows);
+        v.brow_p = dev_upload(owned, s.brow_p);
+        v.brow_q = dev_upload(owned, s.brow_q);
+        v.zcol_t = dev_upload(owned, s.zcol_t);
+        v.zcol_v = dev_upload(owned, s.zcol_v);
+        v.lk = dev_upload(owned, s.lk);
+        v.aidx = dev_upload(owned, s.aidx);
+        v.col = dev_upload(owned, s.col);
+        v.dep = dev_upload(owned, s.dep);
+        v.upd = dev_upload(owned, s.upd_dst);
+        v.lu_sched = dev_upload(owned, s.lu_sched);
+        v.lrow = dev_upload(owned, s.lrow);
+        v.urow = dev_upload(owned, s.urow);
+        v.lent = dev_upload(owned, s.lent);
+        v.uent = dev_upload(owned, s.uent);
+        v.fs_sched = dev_upload(owned, s.fs_sched);
+        v.bs_sched = dev_upload(owned, s.bs_sched);
+        v.tol = opt.tol;
+        v.singular_tol = opt.singular_tol;
+        v.max_iter = opt.max_iter;
+    }
+
+    void set_ybus(const double* re, const double* im) {
+        std::vector<double> a(re, re + sym.nnzY), b(im, im + sym.nnzY);
+        v.yre = dev_upload(owned, a);
+        v.yim = dev_upload(owned, b);
+    }
+
+    void ensure_capacity(int32_t n_tiles) {
+        if (n_tiles <= cap_tiles) return;
+        CK(cudaStreamSynchronize(stream));
+        for (void* p : batch) cudaFree(p);
+        batch.clear();
+        const size_t bpad = size_t(n_tiles) * gbnr::kTile;
+        auto alloc = [&](size_t bytes) {
+            void* p = nullptr;
+            CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+            batch.push_back(p);
+            return p;
+        };
+        const size_t nb = size_t(sym.n) * bpad * sizeof(double);
+        v.vm = static_cast<double*>(alloc(nb));
+        v.va = static_cast<double*>(alloc(nb));
+        v.c = static_cast<double*>(alloc(nb));
+        v.s = static_cast<double*>(alloc(nb));
+        v.p0 = static_cast<double*>(alloc(nb));
+        v.q0 = static_cast<double*>(alloc(nb));
+        v.A = static_cast<double*>(alloc(size_t(n_tiles) * v.nA * gbnr::kTile * sizeof(double)));
+        v.LU = static_cast<double*>(alloc(size_t(n_tiles) * v.nnzLU * gbnr::kTile * sizeof(double)));
+        v.b = static_cast<double*>(alloc(size_t(n_tiles) * v.nJ * gbnr::kTile * sizeof(double)));
+        v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
+        v.iters = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
+        v.active = static_cast<uint8_t*>(alloc(bpad));
+        v.flag = static_cast<uint8_t*>(alloc(bpad));
+        v.maxmis = static_cast<double*>(alloc(bpad * sizeof(double)));
+        v.tile_active = static_cast<int32_t*>(alloc(size_t(n_tiles) * sizeof(int32_t)));
+        v.active_count = static_cast<int32_t*>(alloc(64 * sizeof(int32_t)));
+        cap_tiles = n_tiles;
+    }
+
+    // Element-major host [n][sets] -> device [n][bpad] (broadcast when sets == 1).
+    void put_tape(double* dst, const double* src, int32_t sets, int32_t n_tasks) {
+        const size_t bpad = size_t(v.n_tiles) * gbnr::kTile;
+        if (sets == n_tasks && n_tasks > 1) {
+            CK(cudaMemcpy2DAsync(dst, bpad * sizeof(double), src, size_t(n_tasks) * sizeof(double),
+                                 size_t(n_tasks) * sizeof(double), sym.n, cudaMemcpyHostToDevice,
+                                 stream));
+        } else {
+            CK(cudaMemcpyAsync(d_scratch, src, size_t(sym.n) * sizeof(double), cudaMemcpyHostToDevice,
+                               stream));
+            gbnr::launch_broadcast(dst, d_scratch, sym.n, int32_t(bpad), stream);
+            CK(cudaGetLastError());
+        }
+    }
+
+    void stage(int32_t n_tasks, const double* p0, const double* q0, int32_t n_ssets,
+               const double* vm0, const double* va0, int32_t n_vsets) {
+        if (!on_device) throw Error(GBNR_ECONFIG, "host-only plan (device = -1) cannot solve");
+        if (n_tasks <= 0) throw Error(GBNR_ECONFIG, "n_tasks must be positive");
+        if ((n_ssets != 1 && n_ssets != n_tasks) || (n_vsets != 1 && n_vsets != n_tasks))
+            throw Error(GBNR_ECONFIG, "set counts must be 1 or n_tasks");
+        CK(cudaSetDevice(opt.device));
+        const int32_t n_tiles = (n_tasks + gbnr::kTile - 1) / gbnr::kTile;
+        ensure_capacity(n_tiles);
+        v.n_tiles = n_tiles;
+        v.bpad = n_tiles * gbnr::kTile;
+        v.n_tasks = n_tasks;
+        put_tape(v.vm, vm0, n_vsets, n_tasks);
+        put_tape(v.va, va0, n_vsets, n_tasks);
+        shared_s = n_ssets == 1 && n_tasks > 1;
+        if (shared_s) {
+            CK(cudaMemcpyAsync(const_cast<double*>(v.p0), p0, size_t(sym.n) * sizeof(double),
+                               cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(const_cast<double*>(v.q0), q0, size_t(sym.n) * sizeof(double),
+                               cudaMemcpyHostToDevice, stream));
+            v.s_ld = 1;
+            v.s_inc = 0;
+        } else {
+            put_tape(const_cast<double*>(v.p0), p0, n_ssets, n_tasks);
+            put_tape(const_cast<double*>(v.q0), q0, n_ssets, n_tasks);
+            v.s_ld = v.bpad;
+            v.s_inc = 1;
+        }
+        staged = true;
+    }
+
+    void timed(int phase, const std::function<void()>& launch) {
+        if (!opt.profile) {
+            launch();
+            return;
+        }
+        CK(cudaEventRecord(ev0, stream));
+        launch();
+        CK(cudaEventRecord(ev1, stream));
+        CK(cudaEventSynchronize(ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        timing[phase] += ms;
+        timing[6 + phase] += 1.0;
+    }
+
+    void run() {
+        if (!staged) throw Error(GBNR_ECONFIG, "gbnr_run before gbnr_stage");
+        CK(cudaSetDevice(opt.device));
+        std::memset(timing, 0, sizeof timing);
+        cudaEvent_t t0, t1;
+        CK(cudaEventCreate(&t0));
+        CK(cudaEventCreate(&t1));
+        CK(cudaEventRecord(t0, stream));
+        CK(cudaMemsetAsync(v.active_count, 0, 64 * sizeof(int32_t), stream));
+        gbnr::launch_init(v, stream);
+        CK(cudaGetLastError());
+        timed(kNpm, [&] { gbnr::launch_npm(v, cfg, 0, stream); });
+        int it_done = 0;
+        for (int it = 1; it <= opt.max_iter; ++it) {
+            CK(cudaMemcpyAsync(h_count, v.active_count + (it - 1), sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            if (*h_count == 0) break;
+            timed(kJac, [&] { gbnr::launch_jacobian(v, cfg, stream); });
+            timed(kLu, [&] { gbnr::launch_lu(v, cfg, stream); });
+            timed(kFsbs, [&] { gbnr::launch_fsbs(v, cfg, it, stream); });
+            timed(kVupd, [&] { gbnr::launch_vupdate(v, stream); });
+            timed(kNpm, [&] { gbnr::launch_npm(v, cfg, it, stream); });
+            CK(cudaGetLastError());
+            it_done = it;
+        }
+        CK(cudaEventRecord(t1, stream));
+        CK(cudaStreamSynchronize(stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, t0, t1));
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        timing[5] = ms;
+        timing[12] = it_done;
+        timing[13] = v.n_tasks;
+    }
+
+    void fetch(double* vm, double* va, int32_t* iters, uint8_t* conv, int32_t* status,
+               double* maxmis) {
+        CK(cudaSetDevice(opt.device));
+        const int32_t nt = v.n_tasks;
+        const size_t bpad = size_t(v.bpad);
+        if (vm)
+            CK(cudaMemcpy2DAsync(vm, size_t(nt) * 8, v.vm, bpad * 8, size_t(nt) * 8, sym.n,
+                                 cudaMemcpyDeviceToHost, stream));
+        if (va)
+            CK(cudaMemcpy2DAsync(va, size_t(nt) * 8, v.va, bpad * 8, size_t(nt) * 8, sym.n,
+                                 cudaMemcpyDeviceToHost, stream));
+        std::vector<int32_t> st(nt);
+        CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        if (iters) CK(cudaMemcpyAsync(iters, v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        if (maxmis) CK(cudaMemcpyAsync(maxmis, v.maxmis, size_t(nt) * 8, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (status) std::memcpy(status, st.data(), size_t(nt) * 4);
+        if (conv)
+            for (int32_t t = 0; t < nt; ++t) conv[t] = st[t] == GBNR_CONVERGED;
+    }
+
+    void refactor(int32_t reps, double* lu_out, uint8_t* flags_out, double* ms_out) {
+        if (!staged) throw Error(GBNR_ECONFIG, "gbnr_refactor before gbnr_stage");
+        CK(cudaSetDevice(opt.device));
+        gbnr::launch_init(v, stream);
+        gbnr::launch_jacobian(v, cfg, stream);
+        CK(cudaGetLastError());
+        gbnr::launch_lu(v, cfg, stream);  // warm-up
+        CK(cudaEventRecord(ev0, stream));
+        for (int32_t r = 0; r < reps; ++r) gbnr::launch_lu(v, cfg, stream);
+        CK(cudaEventRecord(ev1, stream));
+        CK(cudaGetLastError());
+        CK(cudaEventSynchronize(ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        if (ms_out) *ms_out = reps > 0 ? ms / reps : 0.0;
+        const int32_t nt = v.n_tasks;
+        if (flags_out)
+            CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
+        if (lu_out) {
+            const size_t z = size_t(v.nnzLU);
+            std::vector<double> h(size_t(v.n_tiles) * z * gbnr::kTile);
+            CK(cudaMemcpy(h.data(), v.LU, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int32_t t = 0; t < nt; ++t) {
+                const size_t tile = t / gbnr::kTile, lane = t % gbnr::kTile;
+                const double* src = h.data() + tile * z * gbnr::kTile + lane;
+                for (size_t s = 0; s < z; ++s) lu_out[s * nt + t] = src[s * gbnr::kTile];
+            }
+        }
+    }
+};
+
+extern "C" {
+
+void gbnr_default_options(gbnr_options* o) {
+    std::memset(o, 0, sizeof *o);
+    o->tol = 1e-8;
+    o->max_iter = 10;
+    o->pivot_tol = 1e-3;
+    o->singular_tol = 1e-14;
+    o->device = 0;
+    o->lu_warps = 8;
+    o->profile = 0;
+}
+
+const char* gbnr_last_error(void) { return g_err.c_str(); }
+
+const char* gbnr_version(void) { return "gbnr 0.1 sm_100a"; }
+
+int gbnr_build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* from, const int32_t* to,
+                    const double* r, const double* x, const double* b, const double* tap,
+                    const double* shift_deg, const uint8_t* in_service, const double* gs,
+                    const double* bs, double base_mva, int32_t* indptr, int32_t* indices,
+                    int32_t* diag, double* y_re, double* y_im, int32_t* nnz_out) {
+    return guarded([&] {
+        const gbnr::YbusCsr y = gbnr::build_ybus(n_bus, n_branch, from, to, r, x, b, tap, shift_deg,
+                                                 in_service, gs, bs, base_mva);
+        std::memcpy(indptr, y.indptr.data(), y.indptr.size() * 4);
+        std::memcpy(indices, y.indices.data(), y.indices.size() * 4);
+        std::memcpy(diag, y.diag.data(), y.diag.size() * 4);
+        std::memcpy(y_re, y.re.data(), y.re.size() * 8);
+        std::memcpy(y_im, y.im.data(), y.im.size() * 8);
+        *nnz_out = static_cast<int32_t>(y.indices.size());
+    });
+}
+
+int gbnr_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd) {
+    return guarded([&] {
+        const std::vector<int32_t> f = gbnr::amd_order(n, col_ptr, row_ix);
+        std::memcpy(fwd, f.data(), size_t(n) * 4);
+    });
+}
+
+int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indices,
+                     const double* y_re, const double* y_im, int32_t ref, const int32_t* pv,
+                     int32_t n_pv, const int32_t* pq, int32_t n_pq, const double* vm0,
+                     const double* va0, const gbnr_options* opt, gbnr_plan** out) {
+    *out = nullptr;
+    gbnr_plan* p = new (std::nothrow) gbnr_plan();
+    if (!p) {
+        g_err = "host out of memory";
+        return GBNR_ECONFIG;
+    }
+    const int rc = guarded([&] {
+        if (opt)
+            p->opt = *opt;
+        else
+            gbnr_default_options(&p->opt);
+        if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 60)
+            throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 60");
+        const int w = p->opt.lu_warps ? p->opt.lu_warps : 8;
+        if (w != 4 && w != 8 && w != 16) throw Error(GBNR_ECONFIG, "lu_warps must be 4, 8 or 16");
+        p->cfg.lu_warps = w;
+        p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
+                       p->opt.pivot_tol);
+        if (p->opt.device >= 0) {
+            int ndev = 0;
+            CK(cudaGetDeviceCount(&ndev));
+            if (p->opt.device >= ndev) throw Error(GBNR_ECUDA, "CUDA device ordinal out of range");
+            p->on_device = true;
+            p->upload_structure();
+            p->set_ybus(y_re, y_im);
+        }
+    });
+    if (rc != GBNR_OK) {
+        delete p;
+        return rc;
+    }
+    *out = p;
+    return GBNR_OK;
+}
+
+void gbnr_plan_destroy(gbnr_plan* plan) { delete plan; }
+
+int gbnr_plan_stats(const gbnr_plan* p, int64_t* o) {
+    return guarded([&] {
+        const gbnr::Symbolic& s = p->sym;
+        const int64_t vals[16] = {s.nJ,         s.nnzJ,      s.nnzLU,     s.nnzL,
+                                  s.nnzU,       s.D,         2 * s.D + s.nnzL, s.levels_lu,
+                                  s.levels_fs,  s.levels_bs, s.offdiag_piv, s.npvpq,
+                                  s.nnzLU - s.nnzJ, s.max_col, s.max_udeps, s.nnzY};
+        std::memcpy(o, vals, sizeof vals);
+    });
+}
+
+int gbnr_plan_export(const gbnr_plan* p, int32_t* row_fwd, int32_t* col_fwd, int32_t* col_ptr,
+                     int32_t* row_ix, int32_t* level) {
+    return guarded([&] {
+        const gbnr::Symbolic& s = p->sym;
+        if (row_fwd) std::memcpy(row_fwd, s.row_fwd.data(), size_t(s.nJ) * 4);
+        if (col_fwd) std::memcpy(col_fwd, s.col_fwd.data(), size_t(s.nJ) * 4);
+        if (col_ptr) std::memcpy(col_ptr, s.cp.data(), size_t(s.nJ + 1) * 4);
+        if (row_ix) std::memcpy(row_ix, s.ri.data(), size_t(s.nnzLU) * 4);
+        if (level) std::memcpy(level, s.level.data(), size_t(s.nJ) * 4);
+    });
+}
+
+int gbnr_stage(gbnr_plan* p, int32_t n_tasks, const double* p0, const double* q0, int32_t n_ssets,
+               const double* vm0, const double* va0, int32_t n_vsets) {
+    return guarded([&] { p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets); });
+}
+
+int gbnr_run(gbnr_plan* p) {
+    return guarded([&] { p->run(); });
+}
+
+int gbnr_fetch(gbnr_plan* p, double* vm_out, double* va_out, int32_t* iterations_out,
+               uint8_t* converged_out, int32_t* status_out, double* max_mismatch_out) {
+    return guarded([&] {
+        if (!p->staged) throw Error(GBNR_ECONFIG, "gbnr_fetch before gbnr_stage");
+        p->fetch(vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out);
+    });
+}
+
+int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* y_im,
+               int32_t n_ysets, const double* p0, const double* q0, int32_t n_ssets,
+               const double* vm0, const double* va0, int32_t n_vsets, double* vm_out,
+               double* va_out, int32_t* iterations_out, uint8_t* converged_out,
+               int32_t* status_out, double* max_mismatch_out) {
+    return guarded([&] {
+        if (n_ysets != 1)
+            throw Error(GBNR_ECONFIG, "per-task Ybus value sets (N-1 mode) are not supported yet");
+        if (y_re && y_im) {
+            // a different shared value set than the plan's: refresh it on the device
+            CK(cudaSetDevice(p->opt.device));
+            CK(cudaMemcpyAsync(const_cast<double*>(p->v.yre), y_re, size_t(p->sym.nnzY) * 8,
+                               cudaMemcpyHostToDevice, p->stream));
+            CK(cudaMemcpyAsync(const_cast<double*>(p->v.yim), y_im, size_t(p->sym.nnzY) * 8,
+                               cudaMemcpyHostToDevice, p->stream));
+        }
+        p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
+        p->run();
+        p->fetch(vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out);
+    });
+}
+
+int gbnr_last_timing(const gbnr_plan* p, double* out) {
+    return guarded([&] { std::memcpy(out, p->timing, sizeof p->timing); });
+}
+
+int gbnr_refactor(gbnr_plan* p, int32_t reps, double* lu_out, uint8_t* flags_out, double* ms_out) {
+    return guarded([&] { p->refactor(reps, lu_out, flags_out, ms_out); });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""GPU parity: the CUDA path (through the C ABI) against the C oracle.
+
+Bar: iteration counts, convergence flags and statuses identical; voltages
+bit-identical (the arithmetic contract of DESIGN.md §4 makes the two
+implementations perform the same IEEE operations) -- the north star's 1e-8 p.u.
+tolerance is asserted as well so a contract break shows up as a bound, not
+just an inequality.
+"""
+import numpy as np
+import pytest
+
+import pyoracle as po
+import util
+from paper_2101_02270_b200.case import load_case
+from paper_2101_02270_b200.scenarios import montecarlo
+from paper_2101_02270_b200 import solver as S
+
+pytestmark = pytest.mark.gpu
+TOL_V = 1e-8  # p.u. / rad, BASELINE.json north_star
+
+
+def _setup(name):
+    gc = load_case(util.case_path(name))
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    vm0, va0 = gc.v_start()
+    plan = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, device=0)
+    oplan = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
+    return gc, plan, oplan, vm0, va0
+
+
+def _compare(r, o, exact=True):
+    np.testing.assert_array_equal(r.status, o["status"])
+    np.testing.assert_array_equal(r.iterations, o["iterations"])
+    np.testing.assert_array_equal(r.converged, o["converged"])
+    ok = r.status == 0
+    assert np.abs(r.vm[:, ok] - o["vm"][:, ok]).max(initial=0) <= TOL_V
+    assert np.abs(r.va[:, ok] - o["va"][:, ok]).max(initial=0) <= TOL_V
+    if exact:
+        np.testing.assert_array_equal(r.vm[:, ok], o["vm"][:, ok])
+        np.testing.assert_array_equal(r.va[:, ok], o["va"][:, ok])
+        np.testing.assert_array_equal(r.max_mismatch[ok], o["max_mismatch"][ok])
+
+
+@pytest.mark.parametrize("name,T", [("case14", 1000), ("synth30", 333), ("synth118", 256),
+                                    ("synth300", 2000), ("synth2383", 200), ("synth9241", 96)])
+def test_montecarlo_matches_oracle(name, T):
+    gc, plan, oplan, vm0, va0 = _setup(name)
+    p0, q0 = montecarlo(gc, T)
+    r = plan.solve(p0, q0, vm0, va0, n_tasks=T)
+    o = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T)
+    assert (r.status == 0).mean() > 0.99
+    _compare(r, o)
+
+
+def test_loadpv_mode_and_per_task_v0():
+    gc, plan, oplan, vm0, va0 = _setup("synth300")
+    T = 130
+    p0, q0 = montecarlo(gc, T, mode="loadpv")
+    rng = np.random.default_rng(1)
+    vmT = vm0[:, None] * (1 + 0.001 * rng.standard_normal((gc.n_bus, T)))
+    vaT = va0[:, None] + 0.001 * rng.standard_normal((gc.n_bus, T))
+    r = plan.solve(p0, q0, vmT, vaT)
+    o = oplan.solve(p0, q0, vmT, vaT)
+    _compare(r, o)
+
+
+def test_shared_injection_set_broadcast():
+    gc, plan, oplan, vm0, va0 = _setup("case14")
+    p0, q0 = gc.profiles(gc.pd, gc.qd)
+    r = plan.solve(p0[:, 0], q0[:, 0], vm0, va0, n_tasks=77)
+    o = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=77)
+    _compare(r, o)
+    assert (r.iterations == 2).all()
+    assert np.abs(r.vm - r.vm[:, :1]).max() == 0.0  # identical tasks -> identical results
+
+
+def test_diverging_task_isolated_and_batch_invariance():
+    gc, plan, oplan, vm0, va0 = _setup("synth118")
+    T = 64
+    p0, q0 = montecarlo(gc, T)
+    p0 = p0.copy(); q0 = q0.copy()
+    p0[:, 5] *= 100.0
+    q0[:, 5] *= 100.0
+    r = plan.solve(p0, q0, vm0, va0)
+    o = oplan.solve(p0, q0, vm0[:, None], va0[:, None])
+    _compare(r, o)
+    assert r.status[5] != 0 and not r.converged[5]
+    # solo runs of a few tasks are bit-identical to their batch results
+    for t in (0, 6, 33, 63):
+        rs = plan.solve(p0[:, t:t + 1], q0[:, t:t + 1], vm0, va0, n_tasks=1)
+        np.testing.assert_array_equal(rs.vm[:, 0], r.vm[:, t])
+        np.testing.assert_array_equal(rs.va[:, 0], r.va[:, t])
+        assert rs.iterations[0] == r.iterations[t]
+
+
+def test_refactor_matches_oracle_bitwise():
+    gc, plan, oplan, vm0, va0 = _setup("synth300")
+    T = 70
+    rng = np.random.default_rng(7)
+    vm = vm0[:, None] * (1 + 0.02 * rng.standard_normal((gc.n_bus, T)))
+    va = va0[:, None] + 0.05 * rng.standard_normal((gc.n_bus, T))
+    p0, q0 = montecarlo(gc, T)
+    plan.stage(p0, q0, vm, va)
+    lu, flags, ms = plan.refactor(reps=2)
+    olu, oflags = oplan.refactor(vm, va)
+    np.testing.assert_array_equal(flags, oflags)
+    np.testing.assert_array_equal(lu, olu)
+    assert ms > 0.0
+
+
+def test_repeat_solve_is_deterministic():
+    gc, plan, oplan, vm0, va0 = _setup("synth300")
+    p0, q0 = montecarlo(gc, 300)
+    a = plan.solve(p0, q0, vm0, va0)
+    b = plan.solve(p0, q0, vm0, va0)
+    np.testing.assert_array_equal(a.vm, b.vm)
+    np.testing.assert_array_equal(a.iterations, b.iterations)
+
+
+@pytest.mark.parametrize("warps", [4, 16])
+def test_lu_warp_count_invariance(warps):
+    """execute_schedule == refactorize_batch bitwise for any worker count."""
+    gc, plan, oplan, vm0, va0 = _setup("synth300")
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, lu_warps=warps)
+    p0, q0 = montecarlo(gc, 100)
+    _compare(plan2.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
