@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- converged power flows per second of the batched Newton-Raphson
+solver (BASELINE.json metric) on a case9241pegase-sized grid, 10k Monte-Carlo
+load scenarios per GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+A *step* is one full batched NR solve of the per-GPU batch (every task from its
+V0 until converged / diverged / max_iter), inputs resident in HBM.  `value` is
+converged PFs of all ranks / max-over-ranks device time (CUDA events on the
+solver stream).  `e2e` is the same metric through the C ABI call with pinned
+host buffers (gbnr_solve: H2D of Sbus, solve, D2H of V / iterations / status).
+`--impl reference` times the CPU restatement of the reference path (the
+oracle, oracle/oracle.c -- the reference itself has no NR/LU code, SURVEY.md
+§0.1) with all host threads on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "converged power flows/sec (10k-scenario batch) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "PF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--case", default="synth9241")
+    ap.add_argument("--tasks", type=int, default=10000, help="tasks per GPU (weak scaling)")
+    ap.add_argument("--total-tasks", type=int, default=0, help="strong scaling: total tasks")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def ensure_built():
+    need = [os.path.join(ROOT, "paper_2101_02270_b200", "libgbnr.so"),
+            os.path.join(ROOT, "oracle", "liboracle.so")]
+    if not all(os.path.exists(p) for p in need):
+        subprocess.run(["make", "-s", "-C", ROOT], check=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def lu_traffic_per_task():
+    """DRAM bytes per task per LU launch from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            d = json.load(fh)
+        return float(d["lu_kernel"]["dram_bytes_per_task"])
+    except Exception:
+        return None
+
+
+def cpu_baseline(gc, case, p_fn, budget_s, threads):
+    """Oracle (CPU restatement of the reference path) on a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_2101_02270_b200 import solver as S
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    vm0, va0 = gc.v_start()
+    oplan = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
+    chunk = max(8 * threads, 64)
+    done = conv = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        p0, q0 = p_fn(done, chunk)
+        r = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=chunk, n_threads=threads)
+        conv += int((r["status"] == 0).sum())
+        done += chunk
+    dt = time.perf_counter() - t0
+    return {"value": conv / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{done} tasks (ids 0..{done - 1}) of the {case} Monte-Carlo workload, "
+                      f"{dt:.1f} s on {threads} threads"}
+
+
+def run_reference(a, rk):
+    """--impl reference: the oracle port with all host threads, rank 0 only."""
+    from paper_2101_02270_b200.case import load_case
+    from paper_2101_02270_b200.scenarios import montecarlo
+    if not rk.is_root:
+        return None
+    gc = load_case(os.path.join(ROOT, "cases", a.case + ".m"))
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_2101_02270_b200 import solver as S
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    vm0, va0 = gc.v_start()
+    oplan = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
+    # one step = a bounded sample sized to ~cpu-seconds/steps of work
+    probe = max(4 * threads, 32)
+    p0, q0 = montecarlo(gc, probe)
+    t0 = time.perf_counter()
+    oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=probe, n_threads=threads)
+    rate = probe / (time.perf_counter() - t0)
+    per_step = int(max(probe, min(a.tasks, rate * max(2.0, 60.0 / max(a.steps + a.warmup, 1)))))
+    per_step = (per_step + threads - 1) // threads * threads
+    p0, q0 = montecarlo(gc, per_step)
+    for _ in range(a.warmup):
+        oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=per_step, n_threads=threads)
+    conv = 0
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        r = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=per_step, n_threads=threads)
+        conv += int((r["status"] == 0).sum())
+    dt = time.perf_counter() - t0
+    value = conv / dt
+    sample = f"{per_step} tasks (ids 0..{per_step - 1}) per step of the {a.case} workload"
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{a.case} Monte-Carlo load scenarios, CPU oracle port",
+                       "case": a.case, "tasks_per_step": per_step, "threads": threads},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    a = parse()
+    ensure_built()
+    from paper_2101_02270_b200 import dist
+    rk = dist.init()
+    if a.impl == "reference":
+        out = run_reference(a, rk)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        dist.finalize(rk)
+        return
+
+    import torch
+    from paper_2101_02270_b200 import solver as S
+    from paper_2101_02270_b200.case import load_case
+    from paper_2101_02270_b200.scenarios import montecarlo
+
+    dev = rk.local_rank if rk.world > 1 else 0
+    gc = load_case(os.path.join(ROOT, "cases", a.case + ".m"))
+    if a.total_tasks:
+        task0, T = dist.shard(a.total_tasks, rk.world, rk.rank)
+        scaling = "strong"
+    else:
+        task0, T = rk.rank * a.tasks, a.tasks
+        scaling = "weak"
+    plan = S.NrPlan.from_case(gc, device=dev, profile=1)
+    st = plan.stats()
+    vm0, va0 = gc.v_start()
+    p0, q0 = montecarlo(gc, T, task0=task0)
+    plan.stage(p0, q0, vm0, va0, n_tasks=T)
+
+    for _ in range(a.warmup):
+        plan.run()
+    dist.barrier(rk)
+    torch.cuda.synchronize(dev)
+    dev_ms = lu_ms = 0.0
+    conv = launches = lu_launches = lu_tasks = 0
+    iters = []
+    with ClockSampler(dev) as clk:
+        w0 = time.perf_counter()
+        for _ in range(a.steps):
+            plan.run()
+            tm = plan.timing()
+            dev_ms += tm["total_ms"]
+            lu_ms += tm["lu_ms"]
+            conv += tm["converged"]
+            lu_launches += tm["lu_launches"]
+            lu_tasks += tm["lu_task_launches"]
+            launches += 1 + sum(tm[f"{k}_launches"] for k in ("npm", "jacobian", "lu", "fsbs", "vupdate"))
+            iters.append(tm["iterations"])
+        wall = time.perf_counter() - w0
+    torch.cuda.synchronize(dev)
+    dist.barrier(rk)
+    job_ms = dist.reduce_max(rk, dev_ms)
+    job_conv = dist.reduce_sum(rk, conv)
+    value = job_conv / (job_ms / 1e3)
+
+    # end to end through the C ABI with pinned host buffers
+    n = gc.n_bus
+    hp0 = torch.from_numpy(np.ascontiguousarray(p0)).pin_memory().numpy()
+    hq0 = torch.from_numpy(np.ascontiguousarray(q0)).pin_memory().numpy()
+    out_vm = torch.empty((n, T), dtype=torch.float64).pin_memory().numpy()
+    out_va = torch.empty((n, T), dtype=torch.float64).pin_memory().numpy()
+    out_it = np.empty(T, np.int32)
+    out_cv = np.empty(T, np.uint8)
+    out_st = np.empty(T, np.int32)
+    out_mm = np.empty(T)
+    import ctypes as C
+    lib = S.lib()
+    ptr = lambda x: x.ctypes.data_as(C.c_void_p)
+    def solve_e2e():
+        rc = lib.gbnr_solve(plan.h, T, None, None, 1, ptr(hp0), ptr(hq0), T, ptr(vm0), ptr(va0), 1,
+                            ptr(out_vm), ptr(out_va), ptr(out_it), ptr(out_cv), ptr(out_st),
+                            ptr(out_mm))
+        S._check(rc)
+    solve_e2e()  # warm
+    dist.barrier(rk)
+    e0 = time.perf_counter()
+    e2e_conv = 0
+    for _ in range(a.e2e_steps):
+        solve_e2e()
+        e2e_conv += int(out_cv.sum())
+    e2e_s = dist.reduce_max(rk, time.perf_counter() - e0)
+    e2e_conv = dist.reduce_sum(rk, e2e_conv)
+    h2d = 2 * n * T * 8 + 2 * n * 8
+    d2h = 2 * n * T * 8 + T * (4 + 1 + 4 + 8)
+
+    # roofline of the dominant kernel (batched LU refactorization)
+    b_lu_task = 8 * (2 * st["nnzLU"] + st["D"])
+    peak, peak_kind = measured_peaks()
+    achieved = b_lu_task * lu_tasks / (lu_ms / 1e3) / 1e9 if lu_ms > 0 else None
+    tr = lu_traffic_per_task()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "traffic": tr * (lu_tasks / max(lu_launches, 1)) if tr else None,
+            "kernel": "lu_kernel (batched frozen-pattern G-P refactorization)",
+            "algorithmic_bytes_per_task": b_lu_task, "peak_kind": peak_kind,
+            "lu_ms_per_launch": lu_ms / max(lu_launches, 1),
+            "lu_share_of_step": lu_ms / dev_ms if dev_ms else None}
+
+    cpu = None
+    if rk.is_root and rk.world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(gc, a.case, lambda t0_, k: montecarlo(gc, k, task0=t0_),
+                           a.cpu_seconds, os.cpu_count() or 1)
+
+    if rk.is_root:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world,
+               "steps": a.steps, "warmup": a.warmup, "ms_per_step": job_ms / a.steps,
+               "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic",
+               "config": {"workload": f"{a.case} (case9241pegase-sized synthetic grid, "
+                                      f"{st['nJ']}-dim Jacobian), Monte-Carlo loads U(0.8,1.2)",
+                          "case": a.case, "tasks_per_gpu": T, "global_batch": T * rk.world,
+                          "parallelism": f"scenario-sharded x{rk.world}, no collective",
+                          "tol": 1e-8, "max_iter": 10,
+                          "newton_iterations_per_step": iters,
+                          "l2": "inputs larger than L2 (LU tape "
+                                f"{st['nnzLU'] * 8 * T / 1e9:.1f} GB per GPU)",
+                          "wall_s_timed": wall},
+               "clocks": clk.summary(),
+               "e2e": {"value": e2e_conv / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h},
+               "gpu_launches": int(launches),
+               "roofline": roof,
+               "cpu_baseline": cpu}
+        print(json.dumps(out), flush=True)
+    plan.close()
+    dist.finalize(rk)
+
+
+if __name__ == "__main__":
+    main()

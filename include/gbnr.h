@@ -61,13 +61,16 @@ typedef struct gbnr_plan gbnr_plan;
 
 typedef struct gbnr_options {
     double tol;            /* mismatch infinity-norm tolerance, p.u. (default 1e-8)   */
-    int32_t max_iter;      /* Newton iterations (default 10)                          */
+    int32_t max_iter;      /* Newton iterations (default 10, at most 30)             */
     double pivot_tol;      /* threshold partial pivoting (default 1e-3) */
     double singular_tol;   /* refactor pivot flag, relative (default 1e-14)          */
     int32_t device;        /* CUDA ordinal; -1 = host-only plan (symbolic only)      */
-    int32_t lu_warps;      /* warps per task tile in LU / FS-BS (0 = default)        */
+    int32_t lu_warps;      /* warps per task tile in LU: 4, 8, 16 (0 = default 8)   */
     int32_t profile;       /* 1 = record per-kernel CUDA-event timings              */
-    int32_t reserved[5];
+    int32_t fs_warps;      /* warps per task tile in FS-BS: 8, 16, 32 (0 = 8)       */
+    int32_t lu_cap;        /* LU working column rows kept in shared memory per warp:
+                              16 or 32 (0 = default 32, -1 = none, work in place)  */
+    int32_t reserved[3];
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);
@@ -125,9 +128,13 @@ int gbnr_run(gbnr_plan* plan);
 int gbnr_fetch(gbnr_plan* plan, double* vm_out, double* va_out, int32_t* iterations_out,
                uint8_t* converged_out, int32_t* status_out, double* max_mismatch_out);
 
-/* Per-kernel device time of the last gbnr_run/gbnr_solve when opt.profile=1.
- * out[0..5] ms: npm, jacobian, lu, fsbs, vupdate, total; out[6..11] launches of
- * the same kernels; out[12] Newton iterations executed; out[13] tasks. */
+/* Per-kernel device time of the last gbnr_run/gbnr_solve (CUDA events on the
+ * solver stream).  out[24]: [0..4] ms of npm, jacobian, lu, fsbs, vupdate when
+ * opt.profile=1 (events recorded around each launch, no host syncs); [5] ms of
+ * the whole solve; [6..10] launches of those kernels; [12] Newton iterations
+ * executed; [13] tasks; [14] sum over LU launches of task tiles with work
+ * (32 tasks each); [15] sum over LU launches of active tasks; [16..18] tasks
+ * converged / diverged / singular. */
 int gbnr_last_timing(const gbnr_plan* plan, double* out);
 
 /* LU-only microbenchmark / parity: the Jacobian at the staged

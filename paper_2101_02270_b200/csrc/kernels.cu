@@ -17,8 +17,6 @@
 //   fsbs_kernel      fs_bs_batch: pull-style rows, same
 //                    progress-counter scheduling, no atomics
 //   vupdate_kernel   update_voltage + unit phasor refresh
-#include <cuda/atomic>
-
 #include "../../include/gbnr.h"
 #include "kernels.hpp"
 #include "numerics.cuh"
@@ -37,20 +35,20 @@ __device__ __forceinline__ double nan_as_inf_abs(double v) {
 // Per-warp progress counters: prog[w] = number of schedule entries warp w has
 // finished.  Entry at schedule position p belongs to warp p % NW, rank p / NW.
 template <int NW>
-__device__ __forceinline__ void wait_done(int* prog, int pos) {
+__device__ __forceinline__ void wait_done(const int* prog, int pos) {
     const int ow = pos % NW, rk = pos / NW;
-    cuda::atomic_ref<int, cuda::thread_scope_block> a(prog[ow]);
-    while (a.load(cuda::memory_order_acquire) <= rk) {
+    const volatile int* f = prog + ow;
+    if (*f <= rk) {
+        while (*f <= rk) {
+        }
     }
+    __threadfence_block();  // acquire: order the data loads after the flag
 }
 
 __device__ __forceinline__ void signal_done(int* prog, int warp, int value, int lane) {
-    __threadfence_block();
+    __threadfence_block();  // release: every lane's stores before the flag
     __syncwarp();
-    if (lane == 0) {
-        cuda::atomic_ref<int, cuda::thread_scope_block> a(prog[warp]);
-        a.store(value, cuda::memory_order_release);
-    }
+    if (lane == 0) *reinterpret_cast<volatile int*>(prog + warp) = value;
 }
 
 // ---------------------------------------------------------------------------
@@ -62,12 +60,11 @@ __global__ void init_kernel(DevView v) {
     const bool real = t < v.n_tasks;
     for (int bus = threadIdx.x >> 5; bus < v.n; bus += blockDim.x >> 5) {
         const size_t o = size_t(bus) * v.bpad + t;
-        if (!real) {
-            v.vm[o] = 1.0;
-            v.va[o] = 0.0;
-        }
+        const double vm = real ? v.vm_in[o] : 1.0, va = real ? v.va_in[o] : 0.0;
+        v.vm[o] = vm;
+        v.va[o] = va;
         double s, c;
-        gb_sincos(v.va[o], &s, &c);
+        gb_sincos(va, &s, &c);
         v.s[o] = s;
         v.c[o] = c;
     }
@@ -87,7 +84,7 @@ __global__ void init_kernel(DevView v) {
 // (row-level parallelism); lane = task.
 // ---------------------------------------------------------------------------
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) npm_kernel(DevView v, int it) {
+__global__ void __launch_bounds__(NW * 32, 3) npm_kernel(DevView v, int it) {
     __shared__ double red[NW][32];
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (v.tile_active[tile] == 0) return;
@@ -142,7 +139,10 @@ __global__ void __launch_bounds__(NW * 32) npm_kernel(DevView v, int it) {
         const int cnt = __popc(__ballot_sync(kFull, act));
         if (lane == 0) {
             v.tile_active[tile] = cnt;
-            if (cnt) atomicAdd(v.active_count + it, cnt);
+            if (cnt) {
+                atomicAdd(v.active_count + it, cnt);       // active tasks after iteration it
+                atomicAdd(v.active_count + 32 + it, 1);    // tiles with work left
+            }
         }
     }
 }
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NW * 32) npm_kernel(DevView v, int it) {
 // Jacobian -> A tape (J nonzeros in LU slot order; fill slots are implicit).
 // ---------------------------------------------------------------------------
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) jacobian_kernel(DevView v) {
+__global__ void __launch_bounds__(NW * 32, 3) jacobian_kernel(DevView v) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (v.tile_active[tile] == 0) return;
     const int t = tile * kTile + lane;
@@ -192,10 +192,111 @@ __global__ void __launch_bounds__(NW * 32) jacobian_kernel(DevView v) {
 // Batched LU refactorization (Alg. 2 operation order per column; Alg. 3-style
 // dependency-driven column parallelism inside the tile's CTA).
 // ---------------------------------------------------------------------------
+// Wait until every schedule position in `pos` (one per lane, -1 = none) is
+// done; the 32 checks run in parallel across the warp.
+template <int NW>
+__device__ __forceinline__ void wait_all(const int* prog, int pos) {
+    const volatile int* pv = prog;
+    bool ok = pos < 0 || pv[pos % NW] > pos / NW;
+    while (!__all_sync(kFull, ok)) ok = pos < 0 || pv[pos % NW] > pos / NW;
+}
+
+// One column of Alg. 2 for the 32 tasks of the tile.  x is the working column
+// (shared memory when it fits, else the LU tape in place); the function is
+// inlined at two call sites so each keeps a concrete address space.
+// Metadata is read warp-coalesced (32 records per load) and broadcast with
+// shuffles, so no per-update load sits on the dependency chain.
+template <int NW>
+__device__ __forceinline__ bool factor_column(const DevView& v, double* x, const double* __restrict__ a,
+                                              double* lut, double* out, const int* prog, int len,
+                                              int dp, int dep0, int ndep, int u0, int nu,
+                                              double stol, int lane, long long* st) {
+    long long t0 = st ? clock64() : 0;
+    // A(:, j): contiguous in the A tape (fill slots hold zeros), 8 loads in flight
+    for (int z0 = 0; z0 < len; z0 += 8) {
+        double av[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) av[q] = z0 + q < len ? a[(z0 + q) * kTile] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (z0 + q < len) x[(z0 + q) * kTile] = av[q];
+    }
+    long long t1 = 0;
+    if (st) {
+        __syncwarp();
+        t1 = clock64();
+        st[0] += t1 - t0;
+    }
+    // every U dependency column must be final before its L(:, k) is read
+    for (int b = 0; b < ndep; b += 32)
+        wait_all<NW>(prog, b + lane < ndep ? __ldg(v.dep_wait + dep0 + b + lane) : -1);
+    __threadfence_block();
+    long long t2 = 0;
+    if (st) {
+        t2 = clock64();
+        st[1] += t2 - t1;
+    }
+    // VMAD stream in Alg. 2 order: x[dst] -= x[k] * L(i, k)
+    const int2* up = reinterpret_cast<const int2*>(v.upd) + u0;
+    int2 rec = lane < nu ? __ldg(up + lane) : make_int2(0, 0);
+    for (int c = 0; c < nu; c += 32) {
+        const int2 rnext = c + 32 + lane < nu ? __ldg(up + c + 32 + lane) : make_int2(0, 0);
+        const int m = min(32, nu - c);
+        double l[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int ls = __shfl_sync(kFull, rec.x, q);
+            l[q] = q < m ? lut[size_t(ls) * kTile] : 0.0;
+        }
+        for (int g = 0; g < m; g += 8) {
+            double ln[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int qq = g + 8 + q;
+                const int ls = __shfl_sync(kFull, rec.x, qq & 31);
+                ln[q] = qq < m ? lut[size_t(ls) * kTile] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int dk = __shfl_sync(kFull, rec.y, (g + q) & 31);
+                if (g + q < m) {
+                    const int dst = dk & 0xffff, kp = dk >> 16;
+                    x[dst * kTile] = fma(-x[kp * kTile], l[q], x[dst * kTile]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) l[q] = ln[q];
+        }
+        rec = rnext;
+    }
+    long long t3 = 0;
+    if (st) {
+        __syncwarp();
+        t3 = clock64();
+        st[2] += t3 - t2;
+    }
+    // pivot check and normalization L = x * (1 / pivot)
+    const double piv = x[dp * kTile];
+    double cmax = 0.0;
+    for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(x[z * kTile]));
+    const bool flagged = isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
+    const double inv = 1.0 / piv;
+    for (int z = 0; z < len; ++z) {
+        const double xv = x[z * kTile];
+        out[z * kTile] = z > dp ? xv * inv : xv;
+    }
+    if (st) {
+        __syncwarp();
+        st[3] += clock64() - t3;
+    }
+    return flagged;
+}
+
 template <int NW, int CAP>
-__global__ void __launch_bounds__(NW * 32) lu_kernel(DevView v) {
+__global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 3 : 1)) lu_kernel(DevView v) {
     extern __shared__ double xs_all[];  // [NW][CAP][32]
     __shared__ int prog[NW];
+    __shared__ unsigned flags[NW];
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (v.tile_active[tile] == 0) return;
     if (threadIdx.x < NW) prog[threadIdx.x] = 0;
@@ -205,58 +306,40 @@ __global__ void __launch_bounds__(NW * 32) lu_kernel(DevView v) {
     double* lut = v.LU + size_t(tile) * v.nnzLU * kTile + lane;
     double* xs = xs_all + size_t(warp) * CAP * kTile + lane;
     const double stol = v.singular_tol;
+    const int4* ci = reinterpret_cast<const int4*>(v.col);
     bool flagged = false;
     int done = 0;
+    long long stv[4] = {0, 0, 0, 0};
+    long long* st = v.lu_stats ? stv : nullptr;
+    int4 c0 = make_int4(0, 0, 0, 0), c1 = make_int4(0, 0, 0, 0);
+    if (warp < v.nJ) {
+        const int j = __ldg(v.lu_sched + warp);
+        c0 = __ldg(ci + 2 * j);
+        c1 = __ldg(ci + 2 * j + 1);
+    }
     for (int p = warp; p < v.nJ; p += NW) {
-        const int j = v.lu_sched[p];
-        const ColInfo ci = v.col[j];
-        const int len = ci.len_dp & 0xffff, dp = ci.len_dp >> 16;
-        double* x = len <= CAP ? xs : lut + size_t(ci.s0) * kTile;
-        // gather A(:, j); fill positions start at zero (Alg. 3 preamble)
-        for (int z = 0; z < len; ++z) {
-            const int a = v.aidx[ci.s0 + z];
-            x[z * kTile] = a >= 0 ? at[size_t(a) * kTile] : 0.0;
+        int4 n0 = c0, n1 = c1;  // prefetch the next column's record
+        if (p + NW < v.nJ) {
+            const int jn = __ldg(v.lu_sched + p + NW);
+            n0 = __ldg(ci + 2 * jn);
+            n1 = __ldg(ci + 2 * jn + 1);
         }
-        // x(L rows) -= x(k) * L(:, k) for the U dependencies k, ascending
-        const int d1 = ci.dep0 + ci.ndep;
-        for (int d = ci.dep0; d < d1; ++d) {
-            const DepInfo di = v.dep[d];
-            wait_done<NW>(prog, di.wait);
-            const int cnt = di.cnt_pos & 0xffff;
-            const double xk = x[(di.cnt_pos >> 16) * kTile];
-            const double* lk = lut + size_t(di.lstart) * kTile;
-            const uint16_t* dst = v.upd + di.upd0;
-            int z = 0;
-            for (; z + 4 <= cnt; z += 4) {
-                const double l0 = lk[(z + 0) * kTile], l1 = lk[(z + 1) * kTile];
-                const double l2 = lk[(z + 2) * kTile], l3 = lk[(z + 3) * kTile];
-                const int e0 = dst[z], e1 = dst[z + 1], e2 = dst[z + 2], e3 = dst[z + 3];
-                x[e0 * kTile] = fma(-xk, l0, x[e0 * kTile]);
-                x[e1 * kTile] = fma(-xk, l1, x[e1 * kTile]);
-                x[e2 * kTile] = fma(-xk, l2, x[e2 * kTile]);
-                x[e3 * kTile] = fma(-xk, l3, x[e3 * kTile]);
-            }
-            for (; z < cnt; ++z) {
-                const int e = dst[z];
-                x[e * kTile] = fma(-xk, lk[z * kTile], x[e * kTile]);
-            }
-        }
-        // pivot check and normalization L = x / pivot
-        const double piv = x[dp * kTile];
-        double cmax = 0.0;
-        for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(x[z * kTile]));
-        if (isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax)) flagged = true;
-        const double inv = 1.0 / piv;
-        double* out = lut + size_t(ci.s0) * kTile;
-        for (int z = 0; z < len; ++z) {
-            const double xv = x[z * kTile];
-            out[z * kTile] = z > dp ? xv * inv : xv;
-        }
+        const int s0 = c0.x, len = c0.y & 0xffff, dp = c0.y >> 16;
+        double* col = lut + size_t(s0) * kTile;
+        if (CAP > 0 && len <= CAP)
+            flagged |= factor_column<NW>(v, xs, at + size_t(s0) * kTile, lut, col, prog, len, dp, c0.z,
+                                         c0.w, c1.x, c1.y, stol, lane, st);
+        else
+            flagged |= factor_column<NW>(v, col, at + size_t(s0) * kTile, lut, col, prog, len, dp, c0.z,
+                                         c0.w, c1.x, c1.y, stol, lane, st);
         ++done;
         signal_done(prog, warp, done, lane);
+        c0 = n0;
+        c1 = n1;
     }
+    if (st && lane == 0)
+        for (int q = 0; q < 4; ++q) v.lu_stats[(size_t(tile) * NW + warp) * 4 + q] = stv[q];
     // any warp may flag the task; combine through shared memory
-    __shared__ unsigned flags[NW];
     const unsigned fb = __ballot_sync(kFull, flagged);
     if (lane == 0) flags[warp] = fb;
     __syncthreads();
@@ -270,9 +353,60 @@ __global__ void __launch_bounds__(NW * 32) lu_kernel(DevView v) {
 
 // ---------------------------------------------------------------------------
 // Forward / backward substitution, pull-style rows with progress counters.
+// Per row: the entry records are read warp-coalesced, the LU loads of the
+// first 8 entries are issued before the dependency check (which runs on all
+// entries in parallel), then b/x loads and the in-order fma chain.
 // ---------------------------------------------------------------------------
+template <int NW, bool BACK>
+__device__ __forceinline__ void tri_solve(const DevView& v, const int32_t* sched,
+                                          const RowInfo* rinfo, const RowEnt* ent,
+                                          const double* __restrict__ lut, double* bt, int* prog,
+                                          int warp, int lane) {
+    const int4* rif = reinterpret_cast<const int4*>(rinfo);
+    const int4* enf = reinterpret_cast<const int4*>(ent);
+    int done = 0;
+    int i = warp < v.nJ ? __ldg(sched + warp) : 0;
+    int4 ri = warp < v.nJ ? __ldg(rif + i) : make_int4(0, 0, 0, 0);
+    for (int p = warp; p < v.nJ; p += NW) {
+        int inext = i;
+        int4 rnext = ri;
+        if (p + NW < v.nJ) {
+            inext = __ldg(sched + p + NW);
+            rnext = __ldg(rif + inext);
+        }
+        const int e0 = ri.x, ne = ri.y;
+        double acc = bt[size_t(i) * kTile];
+        for (int c = 0; c < ne; c += 32) {
+            const int4 en = c + lane < ne ? __ldg(enf + e0 + c + lane) : make_int4(0, 0, -1, 0);
+            const int m = min(32, ne - c);
+            wait_all<NW>(prog, en.z);
+            __threadfence_block();
+            constexpr int G = NW <= 8 ? 8 : (NW <= 16 ? 4 : 2);
+            for (int g = 0; g < m; g += G) {
+                double l[G], xb[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const int sl = __shfl_sync(kFull, en.x, (g + q) & 31);
+                    const int k = __shfl_sync(kFull, en.y, (g + q) & 31);
+                    l[q] = g + q < m ? lut[size_t(sl) * kTile] : 0.0;
+                    xb[q] = g + q < m ? bt[size_t(k) * kTile] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    if (g + q < m) acc = fma(-l[q], xb[q], acc);
+            }
+        }
+        if (BACK) acc = acc / lut[size_t(ri.z) * kTile];
+        bt[size_t(i) * kTile] = acc;
+        ++done;
+        signal_done(prog, warp, done, lane);
+        i = inext;
+        ri = rnext;
+    }
+}
+
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) fsbs_kernel(DevView v, int it) {
+__global__ void __launch_bounds__(NW * 32, (NW <= 16 ? 3 : 1)) fsbs_kernel(DevView v, int it) {
     __shared__ int prog[NW];
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (v.tile_active[tile] == 0) return;
@@ -286,38 +420,14 @@ __global__ void __launch_bounds__(NW * 32) fsbs_kernel(DevView v, int it) {
     __syncthreads();
     const double* __restrict__ lut = v.LU + size_t(tile) * v.nnzLU * kTile + lane;
     double* bt = v.b + size_t(tile) * v.nJ * kTile + lane;
-    int done = 0;
-    for (int p = warp; p < v.nJ; p += NW) {
-        const int i = v.fs_sched[p];
-        const RowInfo ri = v.lrow[i];
-        double acc = bt[size_t(i) * kTile];
-        for (int e = ri.e0; e < ri.e0 + ri.ne; ++e) {
-            const RowEnt en = v.lent[e];
-            wait_done<NW>(prog, en.wait);
-            acc = fma(-lut[size_t(en.slot) * kTile], bt[size_t(en.k) * kTile], acc);
-        }
-        bt[size_t(i) * kTile] = acc;
-        ++done;
-        signal_done(prog, warp, done, lane);
-    }
+    tri_solve<NW, false>(v, v.fs_sched, v.lrow, v.lent, lut, bt, prog, warp, lane);
     __syncthreads();
     if (threadIdx.x < NW) prog[threadIdx.x] = 0;
     __syncthreads();
-    done = 0;
-    for (int p = warp; p < v.nJ; p += NW) {
-        const int i = v.bs_sched[p];
-        const RowInfo ri = v.urow[i];
-        double acc = bt[size_t(i) * kTile];
-        for (int e = ri.e0; e < ri.e0 + ri.ne; ++e) {
-            const RowEnt en = v.uent[e];
-            wait_done<NW>(prog, en.wait);
-            acc = fma(-lut[size_t(en.slot) * kTile], bt[size_t(en.k) * kTile], acc);
-        }
-        bt[size_t(i) * kTile] = acc / lut[size_t(ri.diag) * kTile];
-        ++done;
-        signal_done(prog, warp, done, lane);
-    }
+    tri_solve<NW, true>(v, v.bs_sched, v.urow, v.uent, lut, bt, prog, warp, lane);
 }
+
+
 
 // ---------------------------------------------------------------------------
 // V update for active tasks: va -= dtheta, vm -= d|V|; refresh (cos, sin).
@@ -352,6 +462,7 @@ template <int NW, int CAP>
 void set_lu_smem() {
     cudaFuncSetAttribute(lu_kernel<NW, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          NW * CAP * kTile * int(sizeof(double)));
+    cudaFuncSetAttribute(lu_kernel<NW, CAP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 }  // namespace
@@ -362,10 +473,10 @@ void configure_kernels(const LaunchCfg& c) {
     (void)c;
     set_lu_smem<4, 32>();
     set_lu_smem<8, 32>();
-    set_lu_smem<16, 32>();
     set_lu_smem<8, 16>();
+    set_lu_smem<8, 0>();
     set_lu_smem<16, 16>();
-    set_lu_smem<8, 64>();
+    set_lu_smem<16, 0>();
 }
 
 void launch_init(const DevView& v, cudaStream_t st) { init_kernel<<<v.n_tiles, 256, 0, st>>>(v); }
@@ -386,27 +497,28 @@ void launch_jacobian(const DevView& v, const LaunchCfg& c, cudaStream_t st) {
 
 void launch_lu(const DevView& v, const LaunchCfg& c, cudaStream_t st) {
     const size_t sm = lu_smem_bytes(c);
-    if (c.lu_warps == 4 && c.lu_cap == 32)
+    const int w = c.lu_warps, cap = c.lu_cap;
+    if (w == 4 && cap == 32)
         lu_kernel<4, 32><<<v.n_tiles, 4 * 32, sm, st>>>(v);
-    else if (c.lu_warps == 16 && c.lu_cap == 32)
-        lu_kernel<16, 32><<<v.n_tiles, 16 * 32, sm, st>>>(v);
-    else if (c.lu_warps == 8 && c.lu_cap == 16)
+    else if (w == 8 && cap == 16)
         lu_kernel<8, 16><<<v.n_tiles, 8 * 32, sm, st>>>(v);
-    else if (c.lu_warps == 16 && c.lu_cap == 16)
+    else if (w == 8 && cap == 0)
+        lu_kernel<8, 0><<<v.n_tiles, 8 * 32, 0, st>>>(v);
+    else if (w == 16 && cap == 16)
         lu_kernel<16, 16><<<v.n_tiles, 16 * 32, sm, st>>>(v);
-    else if (c.lu_warps == 8 && c.lu_cap == 64)
-        lu_kernel<8, 64><<<v.n_tiles, 8 * 32, sm, st>>>(v);
+    else if (w == 16 && cap == 0)
+        lu_kernel<16, 0><<<v.n_tiles, 16 * 32, 0, st>>>(v);
     else
-        lu_kernel<8, 32><<<v.n_tiles, 8 * 32, lu_smem_bytes(LaunchCfg{8, c.row_warps, 32}), st>>>(v);
+        lu_kernel<8, 32><<<v.n_tiles, 8 * 32, 8 * 32 * kTile * sizeof(double), st>>>(v);
 }
 
 void launch_fsbs(const DevView& v, const LaunchCfg& c, int it, cudaStream_t st) {
-    if (c.lu_warps == 4)
-        fsbs_kernel<4><<<v.n_tiles, 4 * 32, 0, st>>>(v, it);
-    else if (c.lu_warps == 16)
-        fsbs_kernel<16><<<v.n_tiles, 16 * 32, 0, st>>>(v, it);
-    else
+    if (c.fs_warps == 8)
         fsbs_kernel<8><<<v.n_tiles, 8 * 32, 0, st>>>(v, it);
+    else if (c.fs_warps == 32)
+        fsbs_kernel<32><<<v.n_tiles, 32 * 32, 0, st>>>(v, it);
+    else
+        fsbs_kernel<16><<<v.n_tiles, 16 * 32, 0, st>>>(v, it);
 }
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {

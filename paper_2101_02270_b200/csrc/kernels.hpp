@@ -18,16 +18,17 @@ struct DevView {
     const int32_t *yp, *yi;
     const double *yre, *yim;
     const int32_t *rows, *brow_p, *brow_q, *zcol_t, *zcol_v;
-    const int32_t *lk, *aidx;
+    const int32_t* lk;
     const ColInfo* col;
-    const DepInfo* dep;
-    const uint16_t* upd;
+    const int32_t* dep_wait;
+    const Upd* upd;
     const int32_t* lu_sched;
     const RowInfo *lrow, *urow;
     const RowEnt *lent, *uent;
     const int32_t *fs_sched, *bs_sched;
     // per-task tapes, element-major [elem][bpad]
     double *vm, *va, *c, *s;
+    const double *vm_in, *va_in;  // staged start voltages (kept for repeated runs)
     const double *p0, *q0;
     int32_t s_ld, s_inc;  // p0[bus * s_ld + task * s_inc]
     // per-tile tapes [tile][elem][32]
@@ -39,11 +40,13 @@ struct DevView {
     int32_t *tile_active, *active_count;
     double tol, singular_tol;
     int32_t max_iter, n_tasks;
+    long long* lu_stats;  // optional per-warp cycle breakdown (GBNR_LU_STATS=1)
 };
 
 struct LaunchCfg {
-    int lu_warps = 8;   // warps per CTA in LU / FS-BS
-    int row_warps = 16; // warps per CTA in NPM / Jacobian
+    int lu_warps = 8;   // warps per CTA in LU
+    int fs_warps = 8;   // warps per CTA in FS-BS
+    int row_warps = 8;  // warps per CTA in NPM / Jacobian
     int lu_cap = 32;    // smem working-column capacity (rows) per warp
 };
 

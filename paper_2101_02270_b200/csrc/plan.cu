@@ -6,7 +6,9 @@
 // 4-byte device->host read of the active-task count per iteration to stop as
 // soon as every task has finished (PAPER.md:193 checked convergence on the
 // CPU; here the check itself runs on the device, only the count comes back).
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -76,8 +78,12 @@ struct gbnr_plan {
     bool staged = false;
     gbnr::DevView v{};
     int32_t* h_count = nullptr;   // pinned
-    double timing[16] = {0};
+    double timing[24] = {0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // profiling: an event pair per launch, recorded without host syncs and
+    // resolved once at the end of the solve
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_used;  // (phase, first event index)
 
     ~gbnr_plan() {
         if (!on_device) return;
@@ -88,6 +94,7 @@ struct gbnr_plan {
         if (h_count) cudaFreeHost(h_count);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -106,7 +113,7 @@ struct gbnr_plan {
         v.nnzY = s.nnzY;
         v.n_rows = static_cast<int32_t>(s.rows.size());
         v.nnzLU = static_cast<int32_t>(s.nnzLU);
-        v.nA = static_cast<int32_t>(s.nnzJ);
+        v.nA = static_cast<int32_t>(s.nnzLU);  // A tape in LU slot order, fill slots zero
         v.yp = dev_upload(owned, s.yp);
         v.yi = dev_upload(owned, s.yi);
         v.rows = dev_upload(owned, s.rows);
@@ -115,10 +122,9 @@ struct gbnr_plan {
         v.zcol_t = dev_upload(owned, s.zcol_t);
         v.zcol_v = dev_upload(owned, s.zcol_v);
         v.lk = dev_upload(owned, s.lk);
-        v.aidx = dev_upload(owned, s.aidx);
         v.col = dev_upload(owned, s.col);
-        v.dep = dev_upload(owned, s.dep);
-        v.upd = dev_upload(owned, s.upd_dst);
+        v.dep_wait = dev_upload(owned, s.dep_wait);
+        v.upd = dev_upload(owned, s.upd);
         v.lu_sched = dev_upload(owned, s.lu_sched);
         v.lrow = dev_upload(owned, s.lrow);
         v.urow = dev_upload(owned, s.urow);
@@ -152,11 +158,14 @@ struct gbnr_plan {
         const size_t nb = size_t(sym.n) * bpad * sizeof(double);
         v.vm = static_cast<double*>(alloc(nb));
         v.va = static_cast<double*>(alloc(nb));
+        v.vm_in = static_cast<double*>(alloc(nb));
+        v.va_in = static_cast<double*>(alloc(nb));
         v.c = static_cast<double*>(alloc(nb));
         v.s = static_cast<double*>(alloc(nb));
         v.p0 = static_cast<double*>(alloc(nb));
         v.q0 = static_cast<double*>(alloc(nb));
         v.A = static_cast<double*>(alloc(size_t(n_tiles) * v.nA * gbnr::kTile * sizeof(double)));
+        CK(cudaMemsetAsync(v.A, 0, size_t(n_tiles) * v.nA * gbnr::kTile * sizeof(double), stream));
         v.LU = static_cast<double*>(alloc(size_t(n_tiles) * v.nnzLU * gbnr::kTile * sizeof(double)));
         v.b = static_cast<double*>(alloc(size_t(n_tiles) * v.nJ * gbnr::kTile * sizeof(double)));
         v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
@@ -196,8 +205,8 @@ struct gbnr_plan {
         v.n_tiles = n_tiles;
         v.bpad = n_tiles * gbnr::kTile;
         v.n_tasks = n_tasks;
-        put_tape(v.vm, vm0, n_vsets, n_tasks);
-        put_tape(v.va, va0, n_vsets, n_tasks);
+        put_tape(const_cast<double*>(v.vm_in), vm0, n_vsets, n_tasks);
+        put_tape(const_cast<double*>(v.va_in), va0, n_vsets, n_tasks);
         shared_s = n_ssets == 1 && n_tasks > 1;
         if (shared_s) {
             CK(cudaMemcpyAsync(const_cast<double*>(v.p0), p0, size_t(sym.n) * sizeof(double),
@@ -220,20 +229,33 @@ struct gbnr_plan {
             launch();
             return;
         }
-        CK(cudaEventRecord(ev0, stream));
+        const size_t k = 2 * ev_used.size();
+        while (ev_pool.size() < k + 2) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        CK(cudaEventRecord(ev_pool[k], stream));
         launch();
-        CK(cudaEventRecord(ev1, stream));
-        CK(cudaEventSynchronize(ev1));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev0, ev1));
-        timing[phase] += ms;
-        timing[6 + phase] += 1.0;
+        CK(cudaEventRecord(ev_pool[k + 1], stream));
+        ev_used.emplace_back(phase, int(k));
+    }
+
+    void resolve_profile() {
+        for (const auto& [phase, k] : ev_used) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_pool[k], ev_pool[k + 1]));
+            timing[phase] += ms;
+            timing[6 + phase] += 1.0;
+        }
+        ev_used.clear();
     }
 
     void run() {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_run before gbnr_stage");
         CK(cudaSetDevice(opt.device));
         std::memset(timing, 0, sizeof timing);
+        ev_used.clear();
         cudaEvent_t t0, t1;
         CK(cudaEventCreate(&t0));
         CK(cudaEventCreate(&t1));
@@ -257,11 +279,24 @@ struct gbnr_plan {
             it_done = it;
         }
         CK(cudaEventRecord(t1, stream));
+        CK(cudaMemcpyAsync(h_count, v.active_count, 64 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           stream));
         CK(cudaStreamSynchronize(stream));
+        double tiles = 0, tasks = 0;
+        for (int it = 1; it <= it_done; ++it) {
+            tiles += h_count[32 + it - 1];
+            tasks += h_count[it - 1];
+        }
+        timing[14] = tiles;
+        timing[15] = tasks;
+        std::vector<int32_t> st(size_t(v.n_tasks));
+        CK(cudaMemcpy(st.data(), v.status, st.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (int32_t x : st) timing[16 + (x >= 0 && x <= 2 ? x : 2)] += 1.0;
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, t0, t1));
         cudaEventDestroy(t0);
         cudaEventDestroy(t1);
+        resolve_profile();
         timing[5] = ms;
         timing[12] = it_done;
         timing[13] = v.n_tasks;
@@ -306,6 +341,35 @@ struct gbnr_plan {
         const int32_t nt = v.n_tasks;
         if (flags_out)
             CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
+        if (const char* e = std::getenv("GBNR_LU_STATS"); e && *e == '1') {
+            // one instrumented launch: per-warp clock64 split gather / wait / vmad / write
+            const size_t nst = size_t(v.n_tiles) * cfg.lu_warps * 4;
+            long long* d = nullptr;
+            CK(cudaMalloc(&d, nst * sizeof(long long)));
+            CK(cudaMemset(d, 0, nst * sizeof(long long)));
+            gbnr::DevView w = v;
+            w.lu_stats = d;
+            gbnr::launch_lu(w, cfg, stream);
+            CK(cudaStreamSynchronize(stream));
+            std::vector<long long> h(nst);
+            CK(cudaMemcpy(h.data(), d, nst * sizeof(long long), cudaMemcpyDeviceToHost));
+            cudaFree(d);
+            double sum[4] = {0, 0, 0, 0}, mx = 0;
+            for (size_t i = 0; i < nst / 4; ++i) {
+                double tot = 0;
+                for (int q = 0; q < 4; ++q) {
+                    sum[q] += double(h[4 * i + q]);
+                    tot += double(h[4 * i + q]);
+                }
+                mx = std::max(mx, tot);
+            }
+            const double all = sum[0] + sum[1] + sum[2] + sum[3];
+            std::fprintf(stderr,
+                         "[gbnr] LU warp cycles: gather %.1f%% wait %.1f%% vmad %.1f%% write %.1f%% | "
+                         "mean busy %.3g cyc, max %.3g cyc\n",
+                         100 * sum[0] / all, 100 * sum[1] / all, 100 * sum[2] / all,
+                         100 * sum[3] / all, all / double(nst / 4), mx);
+        }
         if (lu_out) {
             const size_t z = size_t(v.nnzLU);
             std::vector<double> h(size_t(v.n_tiles) * z * gbnr::kTile);
@@ -330,6 +394,7 @@ void gbnr_default_options(gbnr_options* o) {
     o->device = 0;
     o->lu_warps = 8;
     o->profile = 0;
+    o->fs_warps = 8;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -375,11 +440,19 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             p->opt = *opt;
         else
             gbnr_default_options(&p->opt);
-        if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 60)
-            throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 60");
+        if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 30)
+            throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 30");
         const int w = p->opt.lu_warps ? p->opt.lu_warps : 8;
         if (w != 4 && w != 8 && w != 16) throw Error(GBNR_ECONFIG, "lu_warps must be 4, 8 or 16");
         p->cfg.lu_warps = w;
+        const int fw = p->opt.fs_warps ? p->opt.fs_warps : 8;
+        if (fw != 8 && fw != 16 && fw != 32) throw Error(GBNR_ECONFIG, "fs_warps must be 8, 16 or 32");
+        p->cfg.fs_warps = fw;
+        const int cap = p->opt.lu_cap == 0 ? (w == 16 ? 16 : 32) : (p->opt.lu_cap < 0 ? 0 : p->opt.lu_cap);
+        if (cap != 0 && cap != 16 && cap != 32) throw Error(GBNR_ECONFIG, "lu_cap must be -1, 16 or 32");
+        if (w == 16 && cap == 32) throw Error(GBNR_ECONFIG, "lu_warps 16 supports lu_cap 16 or -1");
+        if (w == 4 && cap != 32) throw Error(GBNR_ECONFIG, "lu_warps 4 supports lu_cap 32 only");
+        p->cfg.lu_cap = cap;
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
         if (p->opt.device >= 0) {

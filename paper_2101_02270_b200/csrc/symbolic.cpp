@@ -377,7 +377,8 @@ void Symbolic::analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indi
     }
     if (max_col >= 65536) throw Error(3, "LU column longer than 65535 entries");
 
-    // ---- A tape: the J nonzeros in LU slot order; LU slot -> A index ----
+    // ---- lookup: Ybus slot quadrant -> LU slot of the A tape (fill slots are never
+    //      written and stay zero); aidx marks the J-fed slots (-1 = fill) ----
     std::vector<int32_t> jslot_to_lu(ji.size(), -1);
     for (int32_t r = 0; r < nJ; ++r)
         for (int32_t s = jp[r]; s < jp[r + 1]; ++s) {
@@ -393,7 +394,7 @@ void Symbolic::analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         if (aidx[s] == 0) aidx[s] = na++;
     lk.assign(4 * static_cast<size_t>(nnzY), -1);
     for (size_t q = 0; q < jslot.size(); ++q)
-        if (jslot[q] >= 0) lk[q] = aidx[jslot_to_lu[jslot[q]]];
+        if (jslot[q] >= 0) lk[q] = jslot_to_lu[jslot[q]];
 
     // ---- levels ----
     level.assign(nJ, 0);
@@ -427,28 +428,28 @@ void Symbolic::analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indi
 
     // ---- refactorization program (Alg. 2 with static destinations) ----
     col.resize(nJ);
-    dep.clear();
-    upd_dst.clear();
+    dep_wait.clear();
+    upd.clear();
     std::vector<int32_t> posmap(nJ, -1);
     D = 0;
     max_udeps = 0;
     for (int32_t k = 0; k < nJ; ++k) {
         const int32_t len = cp[k + 1] - cp[k], dp = dpos[k] - cp[k];
-        col[k] = ColInfo{cp[k], len | (dp << 16), int32_t(dep.size()), dp};
+        ColInfo ci{cp[k], len | (dp << 16), int32_t(dep_wait.size()), dp, int32_t(upd.size()), 0, 0, 0};
         max_udeps = std::max(max_udeps, dp);
         for (int32_t z = cp[k]; z < cp[k + 1]; ++z) posmap[ri[z]] = z - cp[k];
         for (int32_t z = cp[k]; z < dpos[k]; ++z) {
             const int32_t j = ri[z];
-            const int32_t cnt = cp[j + 1] - dpos[j] - 1;
-            dep.push_back(DepInfo{dpos[j] + 1, cnt | ((z - cp[k]) << 16), int32_t(upd_dst.size()),
-                                  lu_pos[j]});
+            dep_wait.push_back(lu_pos[j]);
             for (int32_t zz = dpos[j] + 1; zz < cp[j + 1]; ++zz) {
                 const int32_t d = posmap[ri[zz]];
                 if (d < 0) throw Error(2, "frozen LU pattern is not closed");
-                upd_dst.push_back(static_cast<uint16_t>(d));
+                upd.push_back(Upd{zz, d | ((z - cp[k]) << 16)});
             }
-            D += cnt;
+            D += cp[j + 1] - dpos[j] - 1;
         }
+        ci.nu = int32_t(upd.size()) - ci.u0;
+        col[k] = ci;
         for (int32_t z = cp[k]; z < cp[k + 1]; ++z) posmap[ri[z]] = -1;
     }
 

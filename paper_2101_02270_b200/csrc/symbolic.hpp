@@ -38,19 +38,21 @@ YbusCsr build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* f, const int3
 
 std::vector<int32_t> amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix);
 
-// Per-column record of the refactorization program (16 B, one uniform load).
+// Per-column record of the refactorization program (32 B, two uniform loads).
 struct ColInfo {
     int32_t s0;      // first LU slot of the column
     int32_t len_dp;  // len | (diag position << 16)
-    int32_t dep0;    // first dependency record
+    int32_t dep0;    // first entry in dep_wait
     int32_t ndep;    // number of U dependencies (ascending row order)
+    int32_t u0;      // first update record
+    int32_t nu;      // number of update records (= sum of |L(:,k)| over the deps)
+    int32_t pad0, pad1;
 };
-// Per-dependency record: column j uses L(:,k) scaled by x(k).
-struct DepInfo {
-    int32_t lstart;   // LU slot of L(k+1.., k) (first strictly-lower entry of column k)
-    int32_t cnt_pos;  // |L(:,k)| | (position of row k inside column j << 16)
-    int32_t upd0;     // first destination position in upd_dst
-    int32_t wait;     // schedule position of column k (for the progress check)
+// One VMAD element update of Alg. 2: x[dst] -= x[kpos] * LU[lslot], records of
+// a column in dependency-ascending order (the sequential operation order).
+struct Upd {
+    int32_t lslot;     // LU slot of L(i, k)
+    int32_t dst_kpos;  // position of row i in the column | (position of row k << 16)
 };
 // Per-row record for the pull-style triangular solves.
 struct RowInfo {
@@ -76,13 +78,13 @@ struct Symbolic {
     int32_t max_col = 0, max_udeps = 0, levels_lu = 0, levels_fs = 0, levels_bs = 0;
     std::vector<int32_t> row_fwd, col_fwd;  // J row/col -> LU row/col
     std::vector<int32_t> cp, ri, dpos;      // LU CCS in pivot numbering
-    std::vector<int32_t> aidx;              // LU slot -> A tape index (-1 = fill)
-    std::vector<int32_t> lk;                // [4*nnzY] Ybus slot x {Pth,Pvm,Qth,Qvm} -> A index
+    std::vector<int32_t> aidx;              // LU slot -> rank among J-fed slots (-1 = fill)
+    std::vector<int32_t> lk;                // [4*nnzY] Ybus slot x {Pth,Pvm,Qth,Qvm} -> LU slot
     std::vector<int32_t> level;             // LU level per column
     // refactorization program + schedule
     std::vector<ColInfo> col;
-    std::vector<DepInfo> dep;
-    std::vector<uint16_t> upd_dst;
+    std::vector<int32_t> dep_wait;  // schedule position of each U dependency column
+    std::vector<Upd> upd;
     std::vector<int32_t> lu_sched;  // schedule position -> column
     // FS / BS
     std::vector<RowInfo> lrow, urow;

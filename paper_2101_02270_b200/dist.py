@@ -1,0 +1,92 @@
+"""Multi-GPU plumbing: one process per GPU, scenarios sharded, no collective in the solve.
+
+Tasks are independent, so a batch is split into contiguous
+per-rank slices of task ids; each rank generates its own slice with the
+counter-based scenario RNG and runs its own plan on its own device.  The only
+communication is outside the timed solve: a barrier before and after, and a
+max-reduction of the per-rank device times (the job is as slow as its slowest
+rank) plus a sum of the per-rank converged counts.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+
+@dataclass
+class Rank:
+    rank: int = 0
+    world: int = 1
+    local_rank: int = 0
+
+    @property
+    def is_root(self) -> bool:
+        return self.rank == 0
+
+
+def from_env() -> Rank:
+    return Rank(int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+                int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def shard(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced slice [task0, task0 + count) of n_total tasks for rank."""
+    base, extra = divmod(n_total, world)
+    count = base + (1 if rank < extra else 0)
+    task0 = rank * base + min(rank, extra)
+    return task0, count
+
+
+def init(backend: str | None = None) -> Rank:
+    r = from_env()
+    if r.world > 1:
+        import torch.distributed as td
+        if not td.is_initialized():
+            if backend is None:
+                import torch
+                backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                import torch
+                torch.cuda.set_device(r.local_rank)
+            td.init_process_group(backend=backend)
+    return r
+
+
+def _device():
+    import torch
+    import torch.distributed as td
+    return torch.device("cuda", torch.cuda.current_device()) \
+        if td.get_backend() == "nccl" else torch.device("cpu")
+
+
+def barrier(r: Rank) -> None:
+    if r.world > 1:
+        import torch.distributed as td
+        td.barrier()
+
+
+def reduce_max(r: Rank, x: float) -> float:
+    if r.world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as td
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_device())
+    td.all_reduce(t, op=td.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(r: Rank, x: float) -> float:
+    if r.world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as td
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_device())
+    td.all_reduce(t, op=td.ReduceOp.SUM)
+    return float(t.item())
+
+
+def finalize(r: Rank) -> None:
+    if r.world > 1:
+        import torch.distributed as td
+        if td.is_initialized():
+            td.destroy_process_group()

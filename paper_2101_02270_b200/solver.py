@@ -45,7 +45,8 @@ class GbnrError(RuntimeError):
 class Options(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("pivot_tol", C.c_double),
                 ("singular_tol", C.c_double), ("device", C.c_int32), ("lu_warps", C.c_int32),
-                ("profile", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("profile", C.c_int32), ("fs_warps", C.c_int32),
+                ("lu_cap", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 _lib = None
@@ -235,13 +236,18 @@ class NrPlan:
         return self.fetch()
 
     def timing(self) -> dict:
-        out = np.zeros(16)
+        out = np.zeros(24)
         _check(lib().gbnr_last_timing(self.h, out))
         keys = ("npm", "jacobian", "lu", "fsbs", "vupdate", "total")
         d = {f"{k}_ms": float(out[i]) for i, k in enumerate(keys)}
         d.update({f"{k}_launches": int(out[6 + i]) for i, k in enumerate(keys[:5])})
         d["iterations"] = int(out[12])
         d["tasks"] = int(out[13])
+        d["lu_tile_launches"] = int(out[14])
+        d["lu_task_launches"] = int(out[15])
+        d["converged"] = int(out[16])
+        d["diverged"] = int(out[17])
+        d["singular"] = int(out[18])
         return d
 
     def refactor(self, reps: int = 1, want_lu: bool = True):
