@@ -246,7 +246,7 @@ def main():
             conv += tm["converged"]
             lu_launches += tm["lu_launches"]
             lu_tasks += tm["lu_task_launches"]
-            launches += 1 + sum(tm[f"{k}_launches"] for k in ("npm", "jacobian", "lu", "fsbs", "vupdate"))
+            launches += tm["kernels"]
             iters.append(tm["iterations"])
         wall = time.perf_counter() - w0
     torch.cuda.synchronize(dev)

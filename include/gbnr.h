@@ -65,12 +65,12 @@ typedef struct gbnr_options {
     double pivot_tol;      /* threshold partial pivoting (default 1e-3) */
     double singular_tol;   /* refactor pivot flag, relative (default 1e-14)          */
     int32_t device;        /* CUDA ordinal; -1 = host-only plan (symbolic only)      */
-    int32_t lu_warps;      /* warps per task tile in LU: 4, 8, 16 (0 = default 8)   */
-    int32_t profile;       /* 1 = record per-kernel CUDA-event timings              */
-    int32_t fs_warps;      /* warps per task tile in FS-BS: 8, 16, 32 (0 = 8)       */
-    int32_t lu_cap;        /* LU working column rows kept in shared memory per warp:
-                              16 or 32 (0 = default 32, -1 = none, work in place)  */
-    int32_t reserved[3];
+    int32_t lu_warps;      /* reserved (0)                                          */
+    int32_t profile;       /* 1 = record per-phase CUDA-event timings               */
+    int32_t fs_warps;      /* reserved (0)                                          */
+    int32_t lu_cap;        /* reserved (0)                                          */
+    int32_t bulk_min;      /* reserved (0)                                          */
+    int32_t reserved[2];
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);
@@ -134,7 +134,7 @@ int gbnr_fetch(gbnr_plan* plan, double* vm_out, double* va_out, int32_t* iterati
  * the whole solve; [6..10] launches of those kernels; [12] Newton iterations
  * executed; [13] tasks; [14] sum over LU launches of task tiles with work
  * (32 tasks each); [15] sum over LU launches of active tasks; [16..18] tasks
- * converged / diverged / singular. */
+ * converged / diverged / singular; [19] kernels launched by the solve. */
 int gbnr_last_timing(const gbnr_plan* plan, double* out);
 
 /* LU-only microbenchmark / parity: the Jacobian at the staged

@@ -9,55 +9,52 @@
 
 namespace gbnr {
 
-constexpr int kTile = 32;  // tasks per task tile = lanes of a warp
+constexpr int kTile = 32;      // tasks per tile = lanes of a warp
+constexpr int kSuper = 8;      // tiles per super-tile = warps per block (2 KB access runs)
+constexpr int kRowChunk = 32;  // Ybus rows per block in the NPM / Jacobian kernels
 
-// Everything a kernel needs, by value (device pointers + sizes).
+// Everything a kernel needs, by value (device pointers + sizes).  All per-task
+// tapes are element-major: value(elem, task) at elem * bpad + task.
 struct DevView {
-    int32_t n, nJ, nnzY, n_rows, nnzLU, nA, bpad, n_tiles;
+    int32_t n, nJ, nnzY, n_rows, nnzLU, bpad, n_tiles, n_tasks;
     // shared structure (read-only, L2-resident)
     const int32_t *yp, *yi;
     const double *yre, *yim;
     const int32_t *rows, *brow_p, *brow_q, *zcol_t, *zcol_v;
     const int32_t* lk;
     const ColInfo* col;
-    const int32_t* dep_wait;
-    const Upd* upd;
+    const int32_t *upd_ls, *upd_dk;  // update records: LU slot / dst | kpos << 16
     const int32_t* lu_sched;
+    const int32_t *lu_short, *lu_long;  // per-level column lists split by working-set size
     const RowInfo *lrow, *urow;
     const RowEnt *lent, *uent;
     const int32_t *fs_sched, *bs_sched;
-    // per-task tapes, element-major [elem][bpad]
+    // per-task tapes [elem][bpad]
     double *vm, *va, *c, *s;
     const double *vm_in, *va_in;  // staged start voltages (kept for repeated runs)
     const double *p0, *q0;
-    int32_t s_ld, s_inc;  // p0[bus * s_ld + task * s_inc]
-    // per-tile tapes [tile][elem][32]
-    double *A, *LU, *b;
+    int32_t s_ld, s_inc;          // p0[bus * s_ld + task * s_inc]
+    double *A, *LU, *b;           // [nnzLU][bpad], [nnzLU][bpad], [nJ][bpad]
     // per-task state
     int32_t *status, *iters;
     uint8_t *active, *flag;
     double* maxmis;
+    unsigned long long* norm_bits;  // running max-norm (IEEE bits) of the current NPM
     int32_t *tile_active, *active_count;
+    int32_t* it_dev;                // Newton iteration counter on the device
     double tol, singular_tol;
-    int32_t max_iter, n_tasks;
-    long long* lu_stats;  // optional per-warp cycle breakdown (GBNR_LU_STATS=1)
+    int32_t max_iter;
 };
 
-struct LaunchCfg {
-    int lu_warps = 8;   // warps per CTA in LU
-    int fs_warps = 8;   // warps per CTA in FS-BS
-    int row_warps = 8;  // warps per CTA in NPM / Jacobian
-    int lu_cap = 32;    // smem working-column capacity (rows) per warp
-};
-
+size_t lu_smem_bytes();
+void configure_kernels();
 void launch_init(const DevView& v, cudaStream_t st);
-void launch_npm(const DevView& v, const LaunchCfg& c, int it, cudaStream_t st);
-void launch_jacobian(const DevView& v, const LaunchCfg& c, cudaStream_t st);
-void launch_lu(const DevView& v, const LaunchCfg& c, cudaStream_t st);
-void launch_fsbs(const DevView& v, const LaunchCfg& c, int it, cudaStream_t st);
+void launch_npm(const DevView& v, cudaStream_t st);  // NPM + convergence + iteration bump
+void launch_jacobian(const DevView& v, cudaStream_t st);
+void launch_lu_short(const DevView& v, int pos0, int ncols, int maxlen, cudaStream_t st);
+void launch_lu_long(const DevView& v, int pos0, int ncols, int maxlen, cudaStream_t st);
+void launch_tri_level(const DevView& v, bool back, int pos0, int nrows, cudaStream_t st);
 void launch_vupdate(const DevView& v, cudaStream_t st);
 void launch_broadcast(double* dst, const double* src, int32_t n, int32_t bpad, cudaStream_t st);
-size_t lu_smem_bytes(const LaunchCfg& c);
-void configure_kernels(const LaunchCfg& c);
 
 }  // namespace gbnr

@@ -67,20 +67,19 @@ enum Phase { kNpm = 0, kJac, kLu, kFsbs, kVupd, kPhases };
 struct gbnr_plan {
     gbnr::Symbolic sym;
     gbnr_options opt{};
-    gbnr::LaunchCfg cfg;
     bool on_device = false;
     cudaStream_t stream = nullptr;
     std::vector<void*> owned;     // structure buffers
     double* d_scratch = nullptr;  // [n] staging for broadcast sets
     std::vector<void*> batch;     // per-batch tapes
     int32_t cap_tiles = 0;        // allocated tile capacity
-    bool shared_s = true;         // p0/q0 broadcast mode of the staged batch
+    int32_t a_zeroed_bpad = -1;   // layout for which the A tape's fill slots are zero
     bool staged = false;
     gbnr::DevView v{};
     int32_t* h_count = nullptr;   // pinned
     double timing[24] = {0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // profiling: an event pair per launch, recorded without host syncs and
+    // profiling: an event pair per phase, recorded without host syncs and
     // resolved once at the end of the solve
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_used;  // (phase, first event index)
@@ -104,7 +103,7 @@ struct gbnr_plan {
         CK(cudaMallocHost(&h_count, sizeof(int32_t) * 64));
         CK(cudaEventCreate(&ev0));
         CK(cudaEventCreate(&ev1));
-        gbnr::configure_kernels(cfg);
+        gbnr::configure_kernels();
         const gbnr::Symbolic& s = sym;
         CK(cudaMalloc(&d_scratch, size_t(s.n) * sizeof(double)));
         owned.push_back(d_scratch);
@@ -113,7 +112,6 @@ struct gbnr_plan {
         v.nnzY = s.nnzY;
         v.n_rows = static_cast<int32_t>(s.rows.size());
         v.nnzLU = static_cast<int32_t>(s.nnzLU);
-        v.nA = static_cast<int32_t>(s.nnzLU);  // A tape in LU slot order, fill slots zero
         v.yp = dev_upload(owned, s.yp);
         v.yi = dev_upload(owned, s.yi);
         v.rows = dev_upload(owned, s.rows);
@@ -123,15 +121,29 @@ struct gbnr_plan {
         v.zcol_v = dev_upload(owned, s.zcol_v);
         v.lk = dev_upload(owned, s.lk);
         v.col = dev_upload(owned, s.col);
-        v.dep_wait = dev_upload(owned, s.dep_wait);
-        v.upd = dev_upload(owned, s.upd);
+        {
+            // records split and padded so warp-wide 32-record window loads stay in bounds
+            std::vector<int32_t> ls(s.upd.size() + 96, 0), dk(s.upd.size() + 96, 0);
+            for (size_t u = 0; u < s.upd.size(); ++u) {
+                ls[u] = s.upd[u].lslot;
+                dk[u] = s.upd[u].dst_kpos;
+            }
+            v.upd_ls = dev_upload(owned, ls);
+            v.upd_dk = dev_upload(owned, dk);
+        }
         v.lu_sched = dev_upload(owned, s.lu_sched);
+        v.lu_short = dev_upload(owned, s.lu_short);
+        v.lu_long = dev_upload(owned, s.lu_long);
         v.lrow = dev_upload(owned, s.lrow);
         v.urow = dev_upload(owned, s.urow);
         v.lent = dev_upload(owned, s.lent);
         v.uent = dev_upload(owned, s.uent);
         v.fs_sched = dev_upload(owned, s.fs_sched);
         v.bs_sched = dev_upload(owned, s.bs_sched);
+        int32_t* itd = nullptr;
+        CK(cudaMalloc(&itd, sizeof(int32_t)));
+        owned.push_back(itd);
+        v.it_dev = itd;
         v.tol = opt.tol;
         v.singular_tol = opt.singular_tol;
         v.max_iter = opt.max_iter;
@@ -164,15 +176,17 @@ struct gbnr_plan {
         v.s = static_cast<double*>(alloc(nb));
         v.p0 = static_cast<double*>(alloc(nb));
         v.q0 = static_cast<double*>(alloc(nb));
-        v.A = static_cast<double*>(alloc(size_t(n_tiles) * v.nA * gbnr::kTile * sizeof(double)));
-        CK(cudaMemsetAsync(v.A, 0, size_t(n_tiles) * v.nA * gbnr::kTile * sizeof(double), stream));
-        v.LU = static_cast<double*>(alloc(size_t(n_tiles) * v.nnzLU * gbnr::kTile * sizeof(double)));
-        v.b = static_cast<double*>(alloc(size_t(n_tiles) * v.nJ * gbnr::kTile * sizeof(double)));
+        const size_t lub = size_t(v.nnzLU) * bpad * sizeof(double);
+        v.A = static_cast<double*>(alloc(lub));
+        a_zeroed_bpad = -1;
+        v.LU = static_cast<double*>(alloc(lub));
+        v.b = static_cast<double*>(alloc(size_t(v.nJ) * bpad * sizeof(double)));
         v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
         v.iters = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
         v.active = static_cast<uint8_t*>(alloc(bpad));
         v.flag = static_cast<uint8_t*>(alloc(bpad));
         v.maxmis = static_cast<double*>(alloc(bpad * sizeof(double)));
+        v.norm_bits = static_cast<unsigned long long*>(alloc(bpad * sizeof(unsigned long long)));
         v.tile_active = static_cast<int32_t*>(alloc(size_t(n_tiles) * sizeof(int32_t)));
         v.active_count = static_cast<int32_t*>(alloc(64 * sizeof(int32_t)));
         cap_tiles = n_tiles;
@@ -180,7 +194,7 @@ struct gbnr_plan {
 
     // Element-major host [n][sets] -> device [n][bpad] (broadcast when sets == 1).
     void put_tape(double* dst, const double* src, int32_t sets, int32_t n_tasks) {
-        const size_t bpad = size_t(v.n_tiles) * gbnr::kTile;
+        const size_t bpad = size_t(v.bpad);
         if (sets == n_tasks && n_tasks > 1) {
             CK(cudaMemcpy2DAsync(dst, bpad * sizeof(double), src, size_t(n_tasks) * sizeof(double),
                                  size_t(n_tasks) * sizeof(double), sym.n, cudaMemcpyHostToDevice,
@@ -205,10 +219,15 @@ struct gbnr_plan {
         v.n_tiles = n_tiles;
         v.bpad = n_tiles * gbnr::kTile;
         v.n_tasks = n_tasks;
+        if (a_zeroed_bpad != v.bpad) {
+            // fill slots of the A tape are never written by the Jacobian kernel and must
+            // read zero; their element-major addresses move whenever bpad changes
+            CK(cudaMemsetAsync(v.A, 0, size_t(v.nnzLU) * v.bpad * sizeof(double), stream));
+            a_zeroed_bpad = v.bpad;
+        }
         put_tape(const_cast<double*>(v.vm_in), vm0, n_vsets, n_tasks);
         put_tape(const_cast<double*>(v.va_in), va0, n_vsets, n_tasks);
-        shared_s = n_ssets == 1 && n_tasks > 1;
-        if (shared_s) {
+        if (n_ssets == 1 && n_tasks > 1) {
             CK(cudaMemcpyAsync(const_cast<double*>(v.p0), p0, size_t(sym.n) * sizeof(double),
                                cudaMemcpyHostToDevice, stream));
             CK(cudaMemcpyAsync(const_cast<double*>(v.q0), q0, size_t(sym.n) * sizeof(double),
@@ -251,34 +270,58 @@ struct gbnr_plan {
         ev_used.clear();
     }
 
+    // LU: one launch per level (level order = topological order of the column DAG)
+    void launch_lu_all() {
+        const gbnr::Symbolic& s = sym;
+        for (int32_t l = 0; l < s.levels_lu; ++l) {
+            gbnr::launch_lu_short(v, s.lu_short_ptr[l], s.lu_short_ptr[l + 1] - s.lu_short_ptr[l],
+                                  s.lu_short_maxlen[l], stream);
+            gbnr::launch_lu_long(v, s.lu_long_ptr[l], s.lu_long_ptr[l + 1] - s.lu_long_ptr[l],
+                                 s.lu_long_maxlen[l], stream);
+        }
+    }
+
+    // FS then BS, one launch per level
+    void launch_fsbs_all() {
+        const gbnr::Symbolic& s = sym;
+        for (int32_t l = 0; l < s.levels_fs; ++l)
+            gbnr::launch_tri_level(v, false, s.fs_lvl_ptr[l], s.fs_lvl_ptr[l + 1] - s.fs_lvl_ptr[l], stream);
+        for (int32_t l = 0; l < s.levels_bs; ++l)
+            gbnr::launch_tri_level(v, true, s.bs_lvl_ptr[l], s.bs_lvl_ptr[l + 1] - s.bs_lvl_ptr[l], stream);
+    }
+
+    int launches_per_iteration() const {
+        int lu = 0;
+        for (int32_t l = 0; l < sym.levels_lu; ++l)
+            lu += (sym.lu_short_ptr[l + 1] > sym.lu_short_ptr[l]) + (sym.lu_long_ptr[l + 1] > sym.lu_long_ptr[l]);
+        return 1 + lu + sym.levels_fs + sym.levels_bs + 1 + 3;
+    }
+
     void run() {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_run before gbnr_stage");
         CK(cudaSetDevice(opt.device));
         std::memset(timing, 0, sizeof timing);
         ev_used.clear();
-        cudaEvent_t t0, t1;
-        CK(cudaEventCreate(&t0));
-        CK(cudaEventCreate(&t1));
-        CK(cudaEventRecord(t0, stream));
+        CK(cudaEventRecord(ev0, stream));
         CK(cudaMemsetAsync(v.active_count, 0, 64 * sizeof(int32_t), stream));
         gbnr::launch_init(v, stream);
         CK(cudaGetLastError());
-        timed(kNpm, [&] { gbnr::launch_npm(v, cfg, 0, stream); });
+        timed(kNpm, [&] { gbnr::launch_npm(v, stream); });
         int it_done = 0;
         for (int it = 1; it <= opt.max_iter; ++it) {
             CK(cudaMemcpyAsync(h_count, v.active_count + (it - 1), sizeof(int32_t),
                                cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
             if (*h_count == 0) break;
-            timed(kJac, [&] { gbnr::launch_jacobian(v, cfg, stream); });
-            timed(kLu, [&] { gbnr::launch_lu(v, cfg, stream); });
-            timed(kFsbs, [&] { gbnr::launch_fsbs(v, cfg, it, stream); });
+            timed(kJac, [&] { gbnr::launch_jacobian(v, stream); });
+            timed(kLu, [&] { launch_lu_all(); });
+            timed(kFsbs, [&] { launch_fsbs_all(); });
             timed(kVupd, [&] { gbnr::launch_vupdate(v, stream); });
-            timed(kNpm, [&] { gbnr::launch_npm(v, cfg, it, stream); });
+            timed(kNpm, [&] { gbnr::launch_npm(v, stream); });
             CK(cudaGetLastError());
             it_done = it;
         }
-        CK(cudaEventRecord(t1, stream));
+        CK(cudaEventRecord(ev1, stream));
         CK(cudaMemcpyAsync(h_count, v.active_count, 64 * sizeof(int32_t), cudaMemcpyDeviceToHost,
                            stream));
         CK(cudaStreamSynchronize(stream));
@@ -293,13 +336,12 @@ struct gbnr_plan {
         CK(cudaMemcpy(st.data(), v.status, st.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
         for (int32_t x : st) timing[16 + (x >= 0 && x <= 2 ? x : 2)] += 1.0;
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, t0, t1));
-        cudaEventDestroy(t0);
-        cudaEventDestroy(t1);
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
         resolve_profile();
         timing[5] = ms;
         timing[12] = it_done;
         timing[13] = v.n_tasks;
+        timing[19] = double(launches_per_iteration()) * it_done + 4;  // kernels launched
     }
 
     void fetch(double* vm, double* va, int32_t* iters, uint8_t* conv, int32_t* status,
@@ -327,59 +369,48 @@ struct gbnr_plan {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_refactor before gbnr_stage");
         CK(cudaSetDevice(opt.device));
         gbnr::launch_init(v, stream);
-        gbnr::launch_jacobian(v, cfg, stream);
+        gbnr::launch_jacobian(v, stream);
         CK(cudaGetLastError());
-        gbnr::launch_lu(v, cfg, stream);  // warm-up
+        launch_lu_all();  // warm-up
         CK(cudaEventRecord(ev0, stream));
-        for (int32_t r = 0; r < reps; ++r) gbnr::launch_lu(v, cfg, stream);
+        for (int32_t r = 0; r < reps; ++r) launch_lu_all();
         CK(cudaEventRecord(ev1, stream));
         CK(cudaGetLastError());
         CK(cudaEventSynchronize(ev1));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
         if (ms_out) *ms_out = reps > 0 ? ms / reps : 0.0;
-        const int32_t nt = v.n_tasks;
-        if (flags_out)
-            CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
-        if (const char* e = std::getenv("GBNR_LU_STATS"); e && *e == '1') {
-            // one instrumented launch: per-warp clock64 split gather / wait / vmad / write
-            const size_t nst = size_t(v.n_tiles) * cfg.lu_warps * 4;
-            long long* d = nullptr;
-            CK(cudaMalloc(&d, nst * sizeof(long long)));
-            CK(cudaMemset(d, 0, nst * sizeof(long long)));
-            gbnr::DevView w = v;
-            w.lu_stats = d;
-            gbnr::launch_lu(w, cfg, stream);
+        if (const char* e = std::getenv("GBNR_LEVEL_PROFILE"); e && *e == '1') {
+            // per-level device times of one refactorization (diagnostics)
+            std::vector<cudaEvent_t> evs(sym.levels_lu + 1);
+            for (auto& x : evs) CK(cudaEventCreate(&x));
+            for (int32_t l = 0; l < sym.levels_lu; ++l) {
+                CK(cudaEventRecord(evs[l], stream));
+                gbnr::launch_lu_short(v, sym.lu_short_ptr[l], sym.lu_short_ptr[l + 1] - sym.lu_short_ptr[l],
+                                      sym.lu_short_maxlen[l], stream);
+                gbnr::launch_lu_long(v, sym.lu_long_ptr[l], sym.lu_long_ptr[l + 1] - sym.lu_long_ptr[l],
+                                     sym.lu_long_maxlen[l], stream);
+            }
+            CK(cudaEventRecord(evs[sym.levels_lu], stream));
             CK(cudaStreamSynchronize(stream));
-            std::vector<long long> h(nst);
-            CK(cudaMemcpy(h.data(), d, nst * sizeof(long long), cudaMemcpyDeviceToHost));
-            cudaFree(d);
-            double sum[4] = {0, 0, 0, 0}, mx = 0;
-            for (size_t i = 0; i < nst / 4; ++i) {
-                double tot = 0;
-                for (int q = 0; q < 4; ++q) {
-                    sum[q] += double(h[4 * i + q]);
-                    tot += double(h[4 * i + q]);
-                }
-                mx = std::max(mx, tot);
+            double acc = 0;
+            for (int32_t l = 0; l < sym.levels_lu; ++l) {
+                float lm = 0.f;
+                CK(cudaEventElapsedTime(&lm, evs[l], evs[l + 1]));
+                acc += lm;
+                int maxlen = 0;
+                for (int32_t p = sym.lu_lvl_ptr[l]; p < sym.lu_lvl_ptr[l + 1]; ++p)
+                    maxlen = std::max(maxlen, sym.col[sym.lu_sched[p]].len_dp & 0xffff);
+                std::fprintf(stderr, "[gbnr] level %3d cols %5d maxlen %3d  %8.3f ms  cum %8.3f\n", l,
+                             sym.lu_lvl_ptr[l + 1] - sym.lu_lvl_ptr[l], maxlen, lm, acc);
             }
-            const double all = sum[0] + sum[1] + sum[2] + sum[3];
-            std::fprintf(stderr,
-                         "[gbnr] LU warp cycles: gather %.1f%% wait %.1f%% vmad %.1f%% write %.1f%% | "
-                         "mean busy %.3g cyc, max %.3g cyc\n",
-                         100 * sum[0] / all, 100 * sum[1] / all, 100 * sum[2] / all,
-                         100 * sum[3] / all, all / double(nst / 4), mx);
+            for (auto& x : evs) cudaEventDestroy(x);
         }
-        if (lu_out) {
-            const size_t z = size_t(v.nnzLU);
-            std::vector<double> h(size_t(v.n_tiles) * z * gbnr::kTile);
-            CK(cudaMemcpy(h.data(), v.LU, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
-            for (int32_t t = 0; t < nt; ++t) {
-                const size_t tile = t / gbnr::kTile, lane = t % gbnr::kTile;
-                const double* src = h.data() + tile * z * gbnr::kTile + lane;
-                for (size_t s = 0; s < z; ++s) lu_out[s * nt + t] = src[s * gbnr::kTile];
-            }
-        }
+        const int32_t nt = v.n_tasks;
+        if (flags_out) CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
+        if (lu_out)
+            CK(cudaMemcpy2D(lu_out, size_t(nt) * 8, v.LU, size_t(v.bpad) * 8, size_t(nt) * 8,
+                            size_t(v.nnzLU), cudaMemcpyDeviceToHost));
     }
 };
 
@@ -392,7 +423,7 @@ void gbnr_default_options(gbnr_options* o) {
     o->pivot_tol = 1e-3;
     o->singular_tol = 1e-14;
     o->device = 0;
-    o->lu_warps = 8;
+    o->lu_warps = 4;
     o->profile = 0;
     o->fs_warps = 8;
 }
@@ -442,19 +473,10 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             gbnr_default_options(&p->opt);
         if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 30)
             throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 30");
-        const int w = p->opt.lu_warps ? p->opt.lu_warps : 8;
-        if (w != 4 && w != 8 && w != 16) throw Error(GBNR_ECONFIG, "lu_warps must be 4, 8 or 16");
-        p->cfg.lu_warps = w;
-        const int fw = p->opt.fs_warps ? p->opt.fs_warps : 8;
-        if (fw != 8 && fw != 16 && fw != 32) throw Error(GBNR_ECONFIG, "fs_warps must be 8, 16 or 32");
-        p->cfg.fs_warps = fw;
-        const int cap = p->opt.lu_cap == 0 ? (w == 16 ? 16 : 32) : (p->opt.lu_cap < 0 ? 0 : p->opt.lu_cap);
-        if (cap != 0 && cap != 16 && cap != 32) throw Error(GBNR_ECONFIG, "lu_cap must be -1, 16 or 32");
-        if (w == 16 && cap == 32) throw Error(GBNR_ECONFIG, "lu_warps 16 supports lu_cap 16 or -1");
-        if (w == 4 && cap != 32) throw Error(GBNR_ECONFIG, "lu_warps 4 supports lu_cap 32 only");
-        p->cfg.lu_cap = cap;
+        if (p->opt.fs_warps < 0 || p->opt.lu_warps < 0) throw Error(GBNR_ECONFIG, "negative warp count");
+        const int bulk = p->opt.bulk_min ? p->opt.bulk_min : 32;
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
-                       p->opt.pivot_tol);
+                       p->opt.pivot_tol, bulk);
         if (p->opt.device >= 0) {
             int ndev = 0;
             CK(cudaGetDeviceCount(&ndev));

@@ -90,6 +90,14 @@ struct Symbolic {
     std::vector<RowInfo> lrow, urow;
     std::vector<RowEnt> lent, uent;
     std::vector<int32_t> fs_sched, bs_sched;
+    // level pointers into the schedules and the bulk / sync-free split levels
+    std::vector<int32_t> lu_lvl_ptr, fs_lvl_ptr, bs_lvl_ptr;
+    std::vector<int32_t> lu_lvl_maxlen;  // longest column per LU level
+    // per level, columns split by working-set size: short (len <= short_cap) run in
+    // the pipelined kernel, long ones in the large-working-set kernel
+    int32_t short_cap = 24;
+    std::vector<int32_t> lu_short, lu_short_ptr, lu_long, lu_long_ptr, lu_long_maxlen, lu_short_maxlen;
+    int32_t bulk_min = 32, lu_split = 0, fs_split = 0, bs_split = 0;
     // NPM / J row list (non-slack buses) and per-bus b / z positions
     std::vector<int32_t> rows;            // non-slack buses, ascending
     std::vector<int32_t> brow_p, brow_q;  // bus -> LU row of its P / Q equation (-1)
@@ -98,7 +106,7 @@ struct Symbolic {
     void analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indices, const double* y_re,
                  const double* y_im, int32_t ref, const int32_t* pv, int32_t n_pv,
                  const int32_t* pq, int32_t n_pq, const double* vm0, const double* va0,
-                 double pivot_tol);
+                 double pivot_tol, int32_t bulk_min_entries);
 };
 
 }  // namespace gbnr

@@ -46,7 +46,7 @@ class Options(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("pivot_tol", C.c_double),
                 ("singular_tol", C.c_double), ("device", C.c_int32), ("lu_warps", C.c_int32),
                 ("profile", C.c_int32), ("fs_warps", C.c_int32),
-                ("lu_cap", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("lu_cap", C.c_int32), ("bulk_min", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 _lib = None
@@ -248,6 +248,7 @@ class NrPlan:
         d["converged"] = int(out[16])
         d["diverged"] = int(out[17])
         d["singular"] = int(out[18])
+        d["kernels"] = int(out[19])
         return d
 
     def refactor(self, reps: int = 1, want_lu: bool = True):

@@ -117,11 +117,14 @@ def test_repeat_solve_is_deterministic():
     np.testing.assert_array_equal(a.iterations, b.iterations)
 
 
-@pytest.mark.parametrize("warps", [4, 16])
-def test_lu_warp_count_invariance(warps):
-    """execute_schedule == refactorize_batch bitwise for any worker count."""
+@pytest.mark.parametrize("bulk_min,fs_warps", [(1, 16), (8, 8), (100000, 32)])
+def test_schedule_split_invariance(bulk_min, fs_warps):
+    """execute_schedule == refactorize_batch bitwise for any execution plan:
+    moving columns between the level launches and the sync-free tail, and changing
+    the FS-BS warp count, never changes a bit."""
     gc, plan, oplan, vm0, va0 = _setup("synth300")
     ip, ix, _, yr, yi = S.build_ybus(gc)
-    plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, lu_warps=warps)
+    plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0,
+                     bulk_min=bulk_min, fs_warps=fs_warps)
     p0, q0 = montecarlo(gc, 100)
     _compare(plan2.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))

@@ -17,7 +17,8 @@ vm0, va0 = gc.v_start()
 p0, q0 = montecarlo(gc, T)
 for lw, cap in lws:
     for fw in fws:
-        plan = S.NrPlan.from_case(gc, device=0, profile=1, lu_warps=lw, fs_warps=fw, lu_cap=cap)
+        plan = S.NrPlan.from_case(gc, device=0, profile=1, fs_warps=fw,
+                                  bulk_min=int(os.environ.get("BULK", "0")))
         st = plan.stats()
         plan.stage(p0, q0, vm0, va0)
         best = None
