@@ -1,0 +1,121 @@
+"""Generate tests/golden/*.npz from the REFERENCE ITSELF (test fixtures).
+
+Runs the reference's own header-only substrate, compiled in place from
+/root/reference/proj/include by `make -C oracle ref` into oracle/_ref/libgbref.so
+(oracle/ref_shim.cpp), on every case under cases/ and stores what it returns:
+
+  * parse_case      case_io.hpp:345-351 -> n_bus, n_branch, slack, pv, pq
+                    (typing rule case_io.hpp:228-236, finalize_case grid.hpp:123-173)
+  * build_ybus      grid.hpp:208-243   -> indptr, indices, diag_ptr, y_re, y_im
+  * assemble_profiles grid.hpp:299-344 -> p0, q0 (case loads and a 3-set scaled
+                    table), vm_start, va_start (the V0 rule :331-342)
+  * amd_order       amd.hpp:29-157     -> forward permutation of the reduced
+                    Jacobian pattern (built by tests/util.py)
+  * the SPEC.md known-answer examples of sparse_core
+
+/root/reference does not exist on the GPU box; the fixtures are committed and
+the tests only read them.  Usage:  python tools/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")]
+
+import pyoracle as po  # noqa: E402
+import util  # noqa: E402
+
+CASES = ("case14", "synth30", "synth118", "synth300", "synth2383", "synth9241")
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def case_golden(ref: po.Reference, name: str) -> dict:
+    with open(util.case_path(name)) as fh:
+        rc = ref.parse(fh.read())
+    pv, pq = rc.sets()
+    ip, ix, dg, yr, yi = rc.ybus()
+    p_mw, q_mvar = rc.loads()
+    p0, q0, vm0, va0 = rc.profiles(p_mw, q_mvar)
+    scale = np.array([0.8, 1.0, 1.2])
+    p3, q3, _, _ = rc.profiles(p_mw[:, None] * scale, q_mvar[:, None] * scale)
+    nJ, cp, ri = util.j_pattern_ccs(rc.n_bus, ip, ix, rc.slack, pv, pq)
+    fwd = ref.amd(nJ, cp, ri)
+    return dict(n_bus=rc.n_bus, n_branch=rc.n_branch, slack=rc.slack, pv=pv, pq=pq,
+                indptr=ip, indices=ix, diag=dg, y_re=yr, y_im=yi, p_mw=p_mw, q_mvar=q_mvar,
+                p0=p0[:, 0], q0=q0[:, 0], p0_3=p3, q0_3=q3, scale_3=scale, vm_start=vm0,
+                va_start=va0, nJ=nJ, j_col_ptr=cp, j_row_ix=ri, amd_fwd=fwd)
+
+
+def sparse_kats(ref: po.Reference) -> dict:
+    """SPEC.md sparse_core examples, evaluated by the reference."""
+    L = ref.lib
+    out = {}
+
+    def crs(n_rows, n_cols, entries):
+        r = np.array([e[0] for e in entries], np.int32)
+        c = np.array([e[1] for e in entries], np.int32)
+        cap = len(entries) + n_rows
+        rp = np.zeros(n_rows + 1, np.int32); ci = np.zeros(cap, np.int32)
+        dg = np.zeros(n_rows, np.int32); nnz = po.C.c_int32()
+        assert L.ref_crs_from_coords(n_rows, n_cols, len(entries), r, c, cap, rp, ci, dg,
+                                     po.C.byref(nnz)) == 0, ref.err()
+        return rp, ci[:nnz.value].copy(), dg
+
+    # SPEC.md:52 n=2 {(0,0),(0,1),(1,1)}; :53 n=1 empty (diagonal inserted);
+    # :54 Fig. 4a 3x3 shape
+    for key, (n, ent) in {"n2": (2, [(0, 0), (0, 1), (1, 1)]), "n1_empty": (1, []),
+                          "fig4a": (3, [(0, 0), (0, 1), (0, 2), (1, 0), (1, 1), (2, 0), (2, 2)])}.items():
+        rp, ci, dg = crs(n, n, ent)
+        out[f"crs_{key}_row_ptr"], out[f"crs_{key}_col_ix"], out[f"crs_{key}_diag"] = rp, ci, dg
+    # SPEC.md:61 upper-triangular 2x2 -> CCS col_ptr [0,1,3]
+    rp, ci, _ = crs(2, 2, [(0, 0), (0, 1), (1, 1)])
+    cp = np.zeros(3, np.int32); rix = np.zeros(3, np.int32); mp = np.zeros(3, np.int32)
+    assert L.ref_crs_to_ccs(2, 2, rp, ci, cp, rix, mp) == 0, ref.err()
+    out["ccs_upper2_col_ptr"], out["ccs_upper2_row_ix"], out["ccs_upper2_map"] = cp, rix, mp
+    # SPEC.md:71 scatter lookup with the swap permutation on a full 2x2
+    rp, ci, _ = crs(2, 2, [(0, 0), (0, 1), (1, 0), (1, 1)])
+    cp = np.zeros(3, np.int32); rix = np.zeros(4, np.int32); mp = np.zeros(4, np.int32)
+    assert L.ref_crs_to_ccs(2, 2, rp, ci, cp, rix, mp) == 0, ref.err()
+    swap = np.array([1, 0], np.int32); ident = np.array([0, 1], np.int32)
+    lk = np.zeros(4, np.int32)
+    assert L.ref_scatter_lookup(2, rp, ci, swap, swap, 2, cp, rix, ident, ident, lk) == 0, ref.err()
+    out["scatter_swap_lookup"] = lk
+    # SPEC.md:289 AMD of a diagonal matrix; SPEC.md:290 arrow matrix (hub = 0)
+    n = 10
+    out["amd_diag_fwd"] = ref.amd(n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32))
+    cols = [[0] + list(range(1, n))] + [[0, j] for j in range(1, n)]
+    cp = np.cumsum([0] + [len(c) for c in cols]).astype(np.int32)
+    out["amd_arrow_col_ptr"] = cp
+    out["amd_arrow_row_ix"] = np.concatenate([np.array(c, np.int32) for c in cols])
+    out["amd_arrow_fwd"] = ref.amd(n, cp, out["amd_arrow_row_ix"])
+    return out
+
+
+def main():
+    po.build(ref=True)
+    ref = po.Reference()
+    os.makedirs(OUT, exist_ok=True)
+    manifest = {"generator": "tools/make_golden.py",
+                "source": "reference headers /root/reference/proj/include/gridbatch compiled "
+                          "in place via oracle/ref_shim.cpp (oracle/_ref/libgbref.so)",
+                "cases": {}}
+    for name in CASES:
+        g = case_golden(ref, name)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **g)
+        manifest["cases"][name] = {k: int(g[k]) for k in ("n_bus", "n_branch", "slack", "nJ")}
+        manifest["cases"][name].update(n_pv=len(g["pv"]), n_pq=len(g["pq"]),
+                                       nnzY=int(g["indptr"][-1]))
+        print(name, manifest["cases"][name], flush=True)
+    np.savez_compressed(os.path.join(OUT, "sparse_kats.npz"), **sparse_kats(ref))
+    with open(os.path.join(OUT, "MANIFEST.json"), "w") as fh:
+        json.dump(manifest, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
