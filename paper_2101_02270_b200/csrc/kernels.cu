@@ -1,26 +1,22 @@
 // kernels.cu -- hand-written sm_100a FP64 kernels of one Newton-Raphson iteration.
 //
-// Layout.  Every per-task tape is element-major, exactly the
-// reference's BatchTape (batch_tape.hpp:6-9): value(elem, task) at
-// elem * bpad + task, bpad = 32 * n_tiles.  A *tile* is the 32 tasks of one
-// warp (one lane per task, 256 B per warp access).  A thread block is 8 warps =
-// 8 consecutive tiles (a *super-tile*, 256 tasks) that process the SAME
-// structural element (bus row, LU column, triangular-solve row) in lockstep, so
-// every global access of a block is a 2 KB contiguous run.  HBM only streams at
-// copy speed for runs of >= 2 KB on B200 (tools/membench.cu: 256 B random
-// runs reach 1.1 TB/s, 2 KB runs 6.7 TB/s), which is what this layout buys.
+// Layout.  Voltage / injection / right-hand-side tapes are
+// element-major, exactly the reference's BatchTape (batch_tape.hpp:6-9):
+// value(elem, task) at elem * bpad + task, bpad = 32 * n_tiles.  The two
+// [nnzLU]-slot tapes (A = Jacobian in LU slot order, LU = factors) are
+// *tile-blocked*: value(slot, task) at (tile * nnzLU + slot) * 32 + lane, so a
+// column of one tile is one contiguous run (one TMA bulk copy).  A *tile* is the
+// 32 tasks of one warp, one lane per task.
 //
 //   npm_kernel / conv_kernel   compute_npm + convergence (Alg. 1)
 //   jacobian_kernel            update_jacobian into the A tape via the static lookup
 //                              (signs per SURVEY App. B)
-//   lu_level_kernel            refactorize_batch (Alg. 2 operation order)
-//                              scheduled level by level (Alg. 3 stage 1):
-//                              one launch per level, block = (super-tile, column)
-//   tri_level_kernel           fs_bs_batch: pull-style rows per level,
-//                              no atomics (deterministic)
+//   lu_walk_kernel<FS>         refactorize_batch (Alg. 2 operation order)
+//                              fused with the forward substitution:
+//                              one warp walks one tile through every column (walk.hpp)
+//   bs_walk_kernel             backward substitution, one warp per tile, rows in reverse
 //   vupdate_kernel             update_voltage + unit phasor refresh
-// Scenarios are independent, so no kernel ever needs a grid-wide barrier; the
-// level order is carried by stream order.
+// Scenarios are independent, so no kernel ever needs a grid-wide barrier.
 #include "../../include/gbnr.h"
 #include "kernels.hpp"
 #include "numerics.cuh"
@@ -89,6 +85,7 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
     if (tile < 0) return;
     const int t = tile * kTile + lane;
     const size_t bp = v.bpad;
+    double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;  // tile-blocked b tape
     double nrm = 0.0;
     const int r1 = min(v.n_rows, int(blockIdx.x + 1) * kRowChunk);
     for (int ri = blockIdx.x * kRowChunk; ri < r1; ++ri) {
@@ -106,12 +103,12 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
         double P, Q;
         injection(vre, vim, ire, iim, P, Q);
         const double fp = P - v.p0[size_t(r) * v.s_ld + size_t(t) * v.s_inc];
-        v.b[size_t(__ldg(v.brow_p + r)) * bp + t] = fp;
+        b_t[size_t(__ldg(v.brow_p + r)) * kTile] = fp;
         nrm = fmax(nrm, nan_as_inf_abs(fp));
         const int bq = __ldg(v.brow_q + r);
         if (bq >= 0) {
             const double fq = Q - v.q0[size_t(r) * v.s_ld + size_t(t) * v.s_inc];
-            v.b[size_t(bq) * bp + t] = fq;
+            b_t[size_t(bq) * kTile] = fq;
             nrm = fmax(nrm, nan_as_inf_abs(fq));
         }
     }
@@ -155,7 +152,8 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
 __global__ void bump_kernel(DevView v) { *v.it_dev += 1; }
 
 // ---------------------------------------------------------------------------
-// Jacobian -> A tape (LU slot order; fill slots are never written and stay 0).
+// Jacobian -> A tape (LU slot order, tile-blocked; fill slots are never
+// written and stay 0).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -165,6 +163,7 @@ __global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
     const bool act = v.active[t] != 0;
     if (blockIdx.x == 0) v.flag[t] = 0;  // pivot flags of this iteration's refactorization
     const size_t bp = v.bpad;
+    double* a_t = v.A + size_t(tile) * v.nnzLU * kTile + lane;  // tile-blocked A tape
     const int r1 = min(v.n_rows, int(blockIdx.x + 1) * kRowChunk);
     for (int ri = blockIdx.x * kRowChunk; ri < r1; ++ri) {
         const int r = __ldg(v.rows + ri);
@@ -188,220 +187,30 @@ __global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
             jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
             const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
             if (act) {
-                if (l.x >= 0) v.A[size_t(l.x) * bp + t] = j[0];
-                if (l.y >= 0) v.A[size_t(l.y) * bp + t] = j[1];
-                if (l.z >= 0) v.A[size_t(l.z) * bp + t] = j[2];
-                if (l.w >= 0) v.A[size_t(l.w) * bp + t] = j[3];
+                if (l.x >= 0) a_t[size_t(l.x) * kTile] = j[0];
+                if (l.y >= 0) a_t[size_t(l.y) * kTile] = j[1];
+                if (l.z >= 0) a_t[size_t(l.z) * kTile] = j[2];
+                if (l.w >= 0) a_t[size_t(l.w) * kTile] = j[3];
             }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// LU column engine (cp.async).  The working column x (len slot rows of the
-// warp's 32 tasks) and a 32-row ring of L values live in shared memory; every
-// global->shared move is an asynchronous 16 B-per-lane copy (two 256 B rows per
-// warp instruction), so a warp keeps up to (len + 32) rows in flight without
-// spending registers.  Update records sit in three 32-record register windows
-// (consume / issue / prefetch) broadcast with shuffles.  The per-element
-// operation order is exactly Alg. 2's, so results are bit-identical.
+// Tile walks (walk.hpp).  One warp = one tile = one CTA.  Shared memory is a
+// ring of step blocks plus a staging ring, filled by cp.async.bulk (TMA) copies
+// that complete on mbarriers (expect_tx).  Lane 0 issues the host-planned ops
+// as the warp passes their events; every lane computes its own task.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-// lanes 0-15 copy row a, lanes 16-31 row b (a row = the 32 tasks of one slot)
-__device__ __forceinline__ void cp_rows(double* da, const double* sa, double* db, const double* sb,
-                                        int lane) {
-    const int c = (lane & 15) * 2;
-    if (lane < 16) {
-        if (da) cp16(da + c, sa + c);
-    } else {
-        if (db) cp16(db + c, sb + c);
-    }
-}
-
-constexpr int kRing = 32;  // ring rows = one record window
-
-// issue the L-value copies of updates [u, u+8) into ring rows u % 32; the LU
-// slot of update u+q sits in lane (u+q) % 32 of the issue window w
-__device__ __forceinline__ void ring_issue(double* ring, const double* lu_t, size_t bp, int w, int u,
-                                           int nu, int lane) {
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-        const int a = u + q, b = u + q + 1;
-        const int la = __shfl_sync(kFull, w, a & 31), lb = __shfl_sync(kFull, w, b & 31);
-        cp_rows(a < nu ? ring + (a & 31) * kTile : nullptr, lu_t + size_t(la) * bp,
-                b < nu ? ring + (b & 31) * kTile : nullptr, lu_t + size_t(lb) * bp, lane);
-    }
-}
-
-// One column j of Alg. 2 for the 32 tasks of a tile.  a_t / lu_t point at the
-// tile's first task (no lane offset); x rows are 32 doubles.
-__device__ __forceinline__ bool column_async(const DevView& v, double* xw, double* ring,
-                                             const double* a_t, double* lu_t, int s0, int len,
-                                             int dp, int u0, int nu, int lane) {
-    const size_t bp = v.bpad;
-    const int* ls = v.upd_ls + u0;
-    const int* dk = v.upd_dk + u0;
-    const int wls0 = __ldg(ls + lane);  // ls window 0 (prologue issue)
-    int wdk = __ldg(dk + lane);         // dk window 0
-    int wls = __ldg(ls + 32 + lane);    // ls window 1
-    int wls_n = __ldg(ls + 64 + lane);  // ls window 2 (prefetch)
-    int wdk_n = __ldg(dk + 32 + lane);  // dk window 1 (prefetch)
-    const double* a_col = a_t + size_t(s0) * bp;
-    for (int z = 0; z < len; z += 2)
-        cp_rows(xw + z * kTile, a_col + size_t(z) * bp, z + 1 < len ? xw + (z + 1) * kTile : nullptr,
-                a_col + size_t(z + 1) * bp, lane);
-    cp_commit();
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        ring_issue(ring, lu_t, bp, wls0, g * 8, nu, lane);
-        cp_commit();
-    }
-    cp_wait<4>();
-    __syncwarp();
-    double* xl = xw + lane;
-    const double* rl = ring + lane;
-    for (int u = 0; u < nu; u += 8) {
-        cp_wait<3>();
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int d = __shfl_sync(kFull, wdk, (u + q) & 31);
-            if (u + q < nu) {
-                const int dst = d & 0xffff, kp = d >> 16;
-                xl[dst * kTile] = fma(-xl[kp * kTile], rl[((u + q) & 31) * kTile], xl[dst * kTile]);
-            }
-        }
-        __syncwarp();
-        ring_issue(ring, lu_t, bp, wls, u + 32, nu, lane);
-        cp_commit();
-        if (((u + 8) & 31) == 0) {  // crossed into the next record window
-            wdk = wdk_n;
-            wls = wls_n;
-            const int nb = u + 8 + 32;
-            wdk_n = nb < nu ? __ldg(dk + nb + lane) : 0;
-            wls_n = nb + 32 < nu ? __ldg(ls + nb + 32 + lane) : 0;
-        }
-    }
-    cp_wait<0>();
-    __syncwarp();
-    // pivot check and normalization L = x * (1 / pivot)
-    const double piv = xl[dp * kTile];
-    double cmax = 0.0;
-    for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(xl[z * kTile]));
-    const bool flagged = isfinite(cmax) && (piv == 0.0 || fabs(piv) < v.singular_tol * cmax);
-    const double inv = 1.0 / piv;
-    double* out = lu_t + size_t(s0) * bp + lane;
-    for (int z = 0; z < len; ++z) {
-        const double xv = xl[z * kTile];
-        out[size_t(z) * bp] = z > dp ? xv * inv : xv;
-    }
-    return flagged;
-}
-
-// Long columns (len > CAPX): the working column stays in the LU tape (in place),
-// L loads batched 8 at a time in registers.  Same operation order.
-__device__ __forceinline__ bool column_inplace(const DevView& v, const double* a_t, double* lu_t,
-                                               int s0, int len, int dp, int u0, int nu, int lane) {
-    const size_t bp = v.bpad;
-    const double* a = a_t + size_t(s0) * bp + lane;
-    double* x = lu_t + size_t(s0) * bp + lane;
-    const double* lut = lu_t + lane;
-    for (int z0 = 0; z0 < len; z0 += 8) {
-        double av[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) av[q] = z0 + q < len ? a[size_t(z0 + q) * bp] : 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (z0 + q < len) x[size_t(z0 + q) * bp] = av[q];
-    }
-    const int* ls = v.upd_ls + u0;
-    const int* dk = v.upd_dk + u0;
-    for (int c = 0; c < nu; c += 32) {
-        const int wl = __ldg(ls + c + lane), wd = __ldg(dk + c + lane);
-        const int m = min(32, nu - c);
-        for (int g = 0; g < m; g += 8) {
-            double l[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int s = __shfl_sync(kFull, wl, (g + q) & 31);
-                l[q] = g + q < m ? lut[size_t(s) * bp] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int d = __shfl_sync(kFull, wd, (g + q) & 31);
-                if (g + q < m) {
-                    const size_t dst = size_t(d & 0xffff) * bp, kp = size_t(d >> 16) * bp;
-                    x[dst] = fma(-x[kp], l[q], x[dst]);
-                }
-            }
-        }
-    }
-    const double piv = x[size_t(dp) * bp];
-    double cmax = 0.0;
-    for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(x[size_t(z) * bp]));
-    const bool flagged = isfinite(cmax) && (piv == 0.0 || fabs(piv) < v.singular_tol * cmax);
-    const double inv = 1.0 / piv;
-    for (int z = dp + 1; z < len; ++z) x[size_t(z) * bp] *= inv;
-    return flagged;
-}
-
-// One launch per level: block (super-tile, column of the level), warp = tile.
-// All U dependencies sit in earlier levels, complete by stream order.
-template <int CAPX>
-__global__ void __launch_bounds__(256) lu_level_kernel(DevView v, const int32_t* sched, int pos0) {
-    extern __shared__ double sm_all[];  // per warp [CAPX + 32 ring][32]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = my_tile(v, blockIdx.x, warp);
-    if (tile < 0) return;
-    const int j = __ldg(sched + pos0 + blockIdx.y);
-    const int4* ci = reinterpret_cast<const int4*>(v.col);
-    const int4 c0 = __ldg(ci + 2 * j), c1 = __ldg(ci + 2 * j + 1);
-    const int s0 = c0.x, len = c0.y & 0xffff, dp = c0.y >> 16;
-    const double* a_t = v.A + size_t(tile) * kTile;
-    double* lu_t = v.LU + size_t(tile) * kTile;
-    bool flagged;
-    if (len <= CAPX) {
-        double* xw = sm_all + size_t(warp) * (CAPX + kRing) * kTile;
-        flagged = column_async(v, xw, xw + CAPX * kTile, a_t, lu_t, s0, len, dp, c1.x, c1.y, lane);
-    } else {
-        flagged = column_inplace(v, a_t, lu_t, s0, len, dp, c1.x, c1.y, lane);
-    }
-    if (flagged) v.flag[size_t(tile) * kTile + lane] = 1;
-}
-
-// ---------------------------------------------------------------------------
-// Warp-specialized TMA pipeline for the short columns of a level.
-//
-// Persistent blocks (one per SM) walk (column, super-tile) items round-robin.
-// Warp 8 is the producer: with cp.async.bulk (the TMA engine, no registers, no
-// per-lane addressing) it copies each item's A rows -- 2 KB = one super-tile's
-// slice of a slot row -- into one of two x buffers, and the L rows every update
-// of the item reads into a ring of 8-row stages, all completion-tracked by
-// mbarriers (expect_tx).  Warps 0-7 are consumers, one per tile of the
-// super-tile: they wait on the stage barriers, apply Alg. 2's updates in order
-// out of shared memory, normalise, write the column back and release buffers.
-// The producer runs up to a whole ring ahead across item boundaries, so HBM
-// sees long streams of 2 KB requests with deep queues.
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
     unsigned ok;
@@ -412,8 +221,12 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
         : "memory");
     return ok != 0;
 }
+// Bounded wait: a plan bug must fail loudly (trap -> CUDA error), never hang the GPU.
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    if (mbar_try(b, parity)) return;
+    const long long t0 = clock64();
     while (!mbar_try(b, parity)) {
+        if (clock64() - t0 > (1ll << 33)) __trap();
     }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -423,260 +236,240 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-
-constexpr int kPipeStages = 6;  // ring stages of 8 rows
-constexpr int kRowBytes = kSuper * kTile * 8;  // 2 KB: one super-tile's slice of a slot row
-constexpr int kPipeThreads = (kSuper + 1) * 32;
-
-constexpr int kPipeXRows = 48;  // x region: 4 x 12, 3 x 16 or 2 x 24 rows (per level)
-struct PipeSmem {
-    double x[kPipeXRows][kSuper * kTile];
-    double ring[kPipeStages][8][kSuper * kTile];
-    unsigned long long x_full[4], x_empty[4], r_full[kPipeStages], r_empty[kPipeStages];
-};
-
-__global__ void __launch_bounds__(kPipeThreads, 1) lu_pipe_kernel(DevView v, const int32_t* sched,
-                                                                  int pos0, int ncols, int nxb) {
-    extern __shared__ __align__(128) unsigned char pipe_raw[];
-    PipeSmem& S = *reinterpret_cast<PipeSmem*>(pipe_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int n_st = (v.n_tiles + kSuper - 1) / kSuper, items = ncols * n_st;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) {
-            mbar_init(&S.x_full[i], 1);
-            mbar_init(&S.x_empty[i], kSuper);
-        }
-        for (int i = 0; i < kPipeStages; ++i) {
-            mbar_init(&S.r_full[i], 1);
-            mbar_init(&S.r_empty[i], kSuper);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    const size_t bp = v.bpad;
-    const int4* ci = reinterpret_cast<const int4*>(v.col);
-    int n_item = 0, stage = 0;
-    for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int cidx = item / n_st, st = item - cidx * n_st;
-        // skip super-tiles with nothing left to solve (same decision on every warp)
-        bool any = false;
-        for (int w = 0; w < kSuper; ++w) {
-            const int tl = st * kSuper + w;
-            any |= tl < v.n_tiles && v.tile_active[tl] != 0;
-        }
-        if (!any) continue;
-        const int j = __ldg(sched + pos0 + cidx);
-        const int4 c0 = __ldg(ci + 2 * j), c1 = __ldg(ci + 2 * j + 1);
-        const int s0 = c0.x, len = c0.y & 0xffff, dp = c0.y >> 16, u0 = c1.x, nu = c1.y;
-        const int xb = n_item % nxb;                    // x buffer of this item
-        const unsigned xpar = (n_item / nxb) & 1;
-        double (*xbuf)[kSuper * kTile] = S.x + xb * (kPipeXRows / nxb);
-        const size_t col_off = size_t(st) * kSuper * kTile;  // first task of the super-tile
-        if (warp == kSuper) {
-            // ---------------- producer ----------------
-            mbar_wait(&S.x_empty[xb], xpar ^ 1);
-            if (lane == 0) mbar_expect_tx(&S.x_full[xb], unsigned(len) * kRowBytes);
-            __syncwarp();
-            if (lane < len) bulk_g2s(xbuf[lane], v.A + size_t(s0 + lane) * bp + col_off, kRowBytes, &S.x_full[xb]);
-            const int* ls = v.upd_ls + u0;
-            for (int u = 0; u < nu; u += 8, ++stage) {
-                const int slot = stage % kPipeStages;
-                const unsigned spar = (stage / kPipeStages) & 1;
-                const int m = min(8, nu - u);
-                const int lsv = lane < m ? __ldg(ls + u + lane) : 0;
-                mbar_wait(&S.r_empty[slot], spar ^ 1);
-                if (lane == 0) mbar_expect_tx(&S.r_full[slot], unsigned(m) * kRowBytes);
-                __syncwarp();
-                if (lane < m) bulk_g2s(S.ring[slot][lane], v.LU + size_t(lsv) * bp + col_off, kRowBytes, &S.r_full[slot]);
-            }
-        } else {
-            // ---------------- consumers ----------------
-            const int tile = st * kSuper + warp;
-            const bool act = tile < v.n_tiles && v.tile_active[tile] != 0;
-            const int* dk = v.upd_dk + u0;
-            mbar_wait(&S.x_full[xb], xpar);
-            double* xl = &xbuf[0][warp * kTile + lane];
-            int wdk = __ldg(dk + lane);
-            for (int u = 0; u < nu; u += 8, ++stage) {
-                const int slot = stage % kPipeStages;
-                const unsigned spar = (stage / kPipeStages) & 1;
-                const int m = min(8, nu - u);
-                mbar_wait(&S.r_full[slot], spar);
-                if (act) {
-                    const double* rl = &S.ring[slot][0][warp * kTile + lane];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int d = __shfl_sync(kFull, wdk, (u + q) & 31);
-                        if (q < m) {
-                            const int dst = d & 0xffff, kp = d >> 16;
-                            xl[dst * (kSuper * kTile)] =
-                                fma(-xl[kp * (kSuper * kTile)], rl[q * (kSuper * kTile)], xl[dst * (kSuper * kTile)]);
-                        }
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.r_empty[slot]);
-                if (((u + 8) & 31) == 0) wdk = u + 8 < nu ? __ldg(dk + u + 8 + lane) : 0;
-            }
-            if (act) {
-                // pivot check and normalization L = x * (1 / pivot)
-                const double piv = xl[dp * (kSuper * kTile)];
-                double cmax = 0.0;
-                for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(xl[z * (kSuper * kTile)]));
-                const bool flagged = isfinite(cmax) && (piv == 0.0 || fabs(piv) < v.singular_tol * cmax);
-                const double inv = 1.0 / piv;
-                double* out = v.LU + size_t(s0) * bp + size_t(tile) * kTile + lane;
-                for (int z = 0; z < len; ++z) {
-                    const double xv = xl[z * (kSuper * kTile)];
-                    out[size_t(z) * bp] = z > dp ? xv * inv : xv;
-                }
-                if (flagged) v.flag[size_t(tile) * kTile + lane] = 1;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.x_empty[xb]);
-        }
-        ++n_item;
-    }
+// generic-proxy writes -> later async-proxy (TMA) accesses
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialized TMA pipeline for one triangular-solve level (rows of L for
-// FS, of U for BS).  Item = (row i, super-tile).  The producer warp copies,
-// per item, a head slot {b(i) row, diag row (BS)} and, in 8-entry stages, the
-// (LU(i,k) row, b(k) row) pairs of the row's entries; consumers accumulate in
-// the fixed per-element order (k ascending for FS, descending for BS).
-// ---------------------------------------------------------------------------
-constexpr int kTriStages = 5;
-constexpr int kTriHeads = 8;
-struct TriSmem {
-    double ring[kTriStages][8][2][kSuper * kTile];  // [stage][entry][LU row, b row]
-    double head[kTriHeads][2][kSuper * kTile];      // [slot][b(i) row, diag row]
-    unsigned long long r_full[kTriStages], r_empty[kTriStages], h_full[kTriHeads], h_empty[kTriHeads];
+// The walk's program is a word stream (walk.hpp kRec*) paged through shared
+// memory by TMA; every lane reads the same words (smem broadcast).
+constexpr int kWalkBars = 32;   // op i completes on barrier i % 32
+constexpr int kWalkPages = 4;   // resident program pages
+
+struct Prog {
+    double* R;                  // smem rows [ring_rows + stage_rows][32]
+    int32_t* pg;                // smem pages [kWalkPages][page_words]
+    unsigned long long* bar;    // op barriers [kWalkBars]
+    unsigned long long* pbar;   // page barriers [kWalkPages]
+    const int32_t* gs;          // stream in global memory
+    const int32_t* cur;         // next record
+    const char* tape[3];        // this tile's A, LU and b tapes (256 B rows)
+    int W, n_pages, page;
 };
 
-template <bool BACK>
-__global__ void __launch_bounds__(kPipeThreads, 1) tri_pipe_kernel(DevView v, int pos0, int nrows) {
-    extern __shared__ __align__(128) unsigned char tri_raw[];
-    TriSmem& S = *reinterpret_cast<TriSmem*>(tri_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int n_st = (v.n_tiles + kSuper - 1) / kSuper, items = nrows * n_st;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kTriStages; ++i) {
-            mbar_init(&S.r_full[i], 1);
-            mbar_init(&S.r_empty[i], kSuper);
-        }
-        for (int i = 0; i < kTriHeads; ++i) {
-            mbar_init(&S.h_full[i], 1);
-            mbar_init(&S.h_empty[i], kSuper);
-        }
+__device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, Prog& P, int tile, int lane) {
+    extern __shared__ __align__(128) unsigned char walk_smem[];
+    P.R = reinterpret_cast<double*>(walk_smem);
+    P.pg = reinterpret_cast<int32_t*>(walk_smem + size_t(w.ring_rows + w.stage_rows) * kTile * 8);
+    P.bar = reinterpret_cast<unsigned long long*>(P.pg + size_t(kWalkPages) * w.page_words);
+    P.pbar = P.bar + kWalkBars;
+    P.gs = w.stream;
+    P.W = w.page_words;
+    P.n_pages = w.n_pages;
+    P.page = 0;
+    P.cur = P.pg;
+    P.tape[kTapeA] = reinterpret_cast<const char*>(v.A + size_t(tile) * v.nnzLU * kTile);
+    P.tape[kTapeLU] = reinterpret_cast<const char*>(v.LU + size_t(tile) * v.nnzLU * kTile);
+    P.tape[kTapeB] = reinterpret_cast<const char*>(v.b + size_t(tile) * v.nJ * kTile);
+    mbar_init(P.bar + lane, 1);
+    if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
+    if (lane == 0) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    const size_t bp = v.bpad;
-    const int32_t* sched = BACK ? v.bs_sched : v.fs_sched;
-    const int4* rif = reinterpret_cast<const int4*>(BACK ? v.urow : v.lrow);
-    const int4* enf = reinterpret_cast<const int4*>(BACK ? v.uent : v.lent);
-    int n_item = 0, stage = 0;
-    for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int r = item / n_st, st = item - r * n_st;
-        bool any = false;
-        for (int w = 0; w < kSuper; ++w) {
-            const int tl = st * kSuper + w;
-            any |= tl < v.n_tiles && v.tile_active[tl] != 0;
+        for (int p = 0; p < kWalkPages && p < P.n_pages; ++p) {
+            mbar_expect_tx(P.pbar + p, unsigned(P.W) * 4u);
+            bulk_g2s(P.pg + p * P.W, P.gs + size_t(p) * P.W, unsigned(P.W) * 4u, P.pbar + p);
         }
-        if (!any) continue;
-        const int i = __ldg(sched + pos0 + r);
-        const int4 ri = __ldg(rif + i);
-        const int e0 = ri.x, ne = ri.y;
-        const int hs = n_item % kTriHeads;
-        const unsigned hpar = (n_item / kTriHeads) & 1;
-        const size_t col_off = size_t(st) * kSuper * kTile;
-        if (warp == kSuper) {
-            // ---------------- producer ----------------
-            mbar_wait(&S.h_empty[hs], hpar ^ 1);
-            if (lane == 0) mbar_expect_tx(&S.h_full[hs], (BACK ? 2u : 1u) * kRowBytes);
-            __syncwarp();
-            if (lane == 0) bulk_g2s(S.head[hs][0], v.b + size_t(i) * bp + col_off, kRowBytes, &S.h_full[hs]);
-            if (BACK && lane == 1)
-                bulk_g2s(S.head[hs][1], v.LU + size_t(ri.z) * bp + col_off, kRowBytes, &S.h_full[hs]);
-            for (int c = 0; c < ne; c += 8, ++stage) {
-                const int slot = stage % kTriStages;
-                const unsigned spar = (stage / kTriStages) & 1;
-                const int m = min(8, ne - c);
-                const int4 en = lane < m ? __ldg(enf + e0 + c + lane) : make_int4(0, 0, 0, 0);
-                mbar_wait(&S.r_empty[slot], spar ^ 1);
-                if (lane == 0) mbar_expect_tx(&S.r_full[slot], unsigned(2 * m) * kRowBytes);
-                __syncwarp();
-                if (lane < m) {
-                    bulk_g2s(S.ring[slot][lane][0], v.LU + size_t(en.x) * bp + col_off, kRowBytes, &S.r_full[slot]);
-                    bulk_g2s(S.ring[slot][lane][1], v.b + size_t(en.y) * bp + col_off, kRowBytes, &S.r_full[slot]);
-                }
-            }
-        } else {
-            // ---------------- consumers ----------------
-            const int tile = st * kSuper + warp;
-            const bool act = tile < v.n_tiles && v.tile_active[tile] != 0;
-            const int off = warp * kTile + lane;
-            mbar_wait(&S.h_full[hs], hpar);
-            double acc = S.head[hs][0][off];
-            for (int c = 0; c < ne; c += 8, ++stage) {
-                const int slot = stage % kTriStages;
-                const unsigned spar = (stage / kTriStages) & 1;
-                const int m = min(8, ne - c);
-                mbar_wait(&S.r_full[slot], spar);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (q < m) acc = fma(-S.ring[slot][q][0][off], S.ring[slot][q][1][off], acc);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.r_empty[slot]);
-            }
-            if (BACK) acc = acc / S.head[hs][1][off];
-            if (act) v.b[size_t(i) * bp + size_t(tile) * kTile + lane] = acc;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.h_empty[hs]);
-        }
-        ++n_item;
     }
+    __syncwarp();
+    mbar_wait(P.pbar, 0);
 }
 
-// ---------------------------------------------------------------------------
-// Triangular solves, one launch per level: block (super-tile, row), warp =
-// tile.  Pull-style rows: FS  y(i) = b(i) - sum_k L(i,k) y(k)  (k ascending),
-// BS x(i) = (y(i) - sum_k U(i,k) x(k)) / U(i,i)  (k descending) -- the same
-// per-element order as the column-oriented sequential FS/BS, no atomics.
-// ---------------------------------------------------------------------------
-template <bool BACK>
-__global__ void __launch_bounds__(256) tri_level_kernel(DevView v, int pos0) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = my_tile(v, blockIdx.x, warp);
-    if (tile < 0) return;
-    const size_t bp = v.bpad;
-    const int i = __ldg((BACK ? v.bs_sched : v.fs_sched) + pos0 + blockIdx.y);
-    const int4 ri = __ldg(reinterpret_cast<const int4*>(BACK ? v.urow : v.lrow) + i);
-    const int4* enf = reinterpret_cast<const int4*>(BACK ? v.uent : v.lent);
-    const double* __restrict__ lut = v.LU + size_t(tile) * kTile + lane;
-    double* bt = v.b + size_t(tile) * kTile + lane;
-    double acc = bt[size_t(i) * bp];
-    const int e0 = ri.x, ne = ri.y;
-    for (int c = 0; c < ne; c += 32) {
-        const int4 en = c + lane < ne ? __ldg(enf + e0 + c + lane) : make_int4(0, 0, 0, 0);
-        const int m = min(32, ne - c);
-        for (int g = 0; g < m; g += 8) {
-            double l[8], xb[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int sl = __shfl_sync(kFull, en.x, (g + q) & 31);
-                const int k = __shfl_sync(kFull, en.y, (g + q) & 31);
-                l[q] = g + q < m ? lut[size_t(sl) * bp] : 0.0;
-                xb[q] = g + q < m ? bt[size_t(k) * bp] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (g + q < m) acc = fma(-l[q], xb[q], acc);
+__device__ __forceinline__ void prog_next_page(Prog& P, int lane) {
+    __syncwarp();
+    const int slot = P.page & (kWalkPages - 1);
+    if (lane == 0 && P.page + kWalkPages < P.n_pages) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(P.pbar + slot, unsigned(P.W) * 4u);
+        bulk_g2s(P.pg + slot * P.W, P.gs + size_t(P.page + kWalkPages) * P.W, unsigned(P.W) * 4u, P.pbar + slot);
+    }
+    ++P.page;
+    const int ns = P.page & (kWalkPages - 1);
+    P.cur = P.pg + ns * P.W;
+    mbar_wait(P.pbar + ns, unsigned((P.page / kWalkPages) & 1));
+}
+
+// kRecIssue: lane 0 arms the op's barrier and issues its bulk copies.
+__device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32_t* r, int lane) {
+    const int ncopy = (r[0] >> 4) & 0xfff;
+    if (!(v.dbg & 2)) fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
+    __syncwarp();
+    if (lane == 0) {
+        unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
+        mbar_expect_tx(bar, unsigned(r[2]));
+        const unsigned rbase = smem_u32(P.R);
+        for (int i = 0; i < ncopy; ++i) {
+            const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
+            const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    rbase + smem * (kTile * 8u)),
+                "l"(P.tape[c & 3] + size_t(slot) * (kTile * 8)), "r"(rows * (kTile * 8u)), "r"(smem_u32(bar))
+                : "memory");
         }
     }
-    if (BACK) acc = acc / lut[size_t(ri.z) * bp];
-    bt[size_t(i) * bp] = acc;
+    return 3 + 2 * ncopy;
+}
+
+__device__ __forceinline__ void prog_wait(const Prog& P, int op) {
+    mbar_wait(P.bar + (op & (kWalkBars - 1)), unsigned((op / kWalkBars) & 1));
+}
+
+// Forward walk: Alg. 2 column by column (+ forward substitution when FS).
+template <bool FS>
+__global__ void __launch_bounds__(32) lu_walk_kernel(DevView v, WalkView w) {
+    const int tile = blockIdx.x, lane = threadIdx.x;
+    if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
+    Prog P;
+    prog_begin(v, w, P, tile, lane);
+    double* lu_t = v.LU + size_t(tile) * v.nnzLU * kTile + lane;
+    double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
+    const double stol = v.singular_tol;
+    bool flagged = false;
+    double* x = P.R;
+    int len = 0, dp = 0, lslot = 0, brow = 0;
+    double acc_y = 0.0;
+    for (;;) {
+        const int32_t* r = P.cur;
+        const int32_t h = r[0];
+        const int type = h & 15;
+        if (type == kRecIssue) {
+            P.cur += prog_issue(v, P, r, lane);
+        } else if (type == kRecDep) {
+            const int op = (h >> 4) - 1;
+            const int kpos_fs = r[1], nrows = r[2] & 0xffff, src_row = int(unsigned(r[2]) >> 16);
+            const int ysrc = r[3];
+            if (op >= 0) prog_wait(P, op);
+            const double* src = P.R + size_t(src_row) * kTile + lane;
+            if (nrows > 0) {
+                const double mult = x[(kpos_fs & 0xffff) * kTile];
+                const int32_t* dw = r + 4;
+                int q = 0;
+                for (; q + 4 <= nrows; q += 4) {
+                    const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1];
+                    const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
+                    const int d2 = w1 & 0xffff, d3 = int(unsigned(w1) >> 16);
+                    const double l0 = src[q * kTile], l1 = src[(q + 1) * kTile];
+                    const double l2 = src[(q + 2) * kTile], l3 = src[(q + 3) * kTile];
+                    double a0 = x[d0 * kTile], a1 = x[d1 * kTile], a2 = x[d2 * kTile], a3 = x[d3 * kTile];
+                    a0 = fma(-mult, l0, a0);
+                    a1 = fma(-mult, l1, a1);
+                    a2 = fma(-mult, l2, a2);
+                    a3 = fma(-mult, l3, a3);
+                    x[d0 * kTile] = a0;
+                    x[d1 * kTile] = a1;
+                    x[d2 * kTile] = a2;
+                    x[d3 * kTile] = a3;
+                }
+                for (; q < nrows; ++q) {
+                    const int32_t wq = dw[q >> 1];
+                    const int d0 = (q & 1) ? int(unsigned(wq) >> 16) : (wq & 0xffff);
+                    x[d0 * kTile] = fma(-mult, src[q * kTile], x[d0 * kTile]);
+                }
+            }
+            if (FS) {
+                const int fspos = int(unsigned(kpos_fs) >> 16);
+                if (fspos != 0xffff) acc_y = fma(-src[fspos * kTile], P.R[size_t(ysrc) * kTile + lane], acc_y);
+            }
+            P.cur += 4 + ((nrows + 1) >> 1);
+        } else if (type == kRecStep) {
+            const int ring = r[1] & 0xffff;
+            len = int(unsigned(r[1]) >> 16);
+            dp = r[2];
+            lslot = r[3];
+            brow = r[4];
+            const int op = r[5];
+            P.cur += 6;
+            prog_wait(P, op);
+            x = P.R + size_t(ring) * kTile + lane;
+            acc_y = FS ? x[len * kTile] : 0.0;
+        } else if (type == kRecEnd) {
+            // pivot check and normalization L = x * (1 / pivot)
+            const double piv = x[dp * kTile];
+            double cmax = 0.0;
+            for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(x[z * kTile]));
+            flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
+            const double inv = 1.0 / piv;
+            double* lcol = lu_t + size_t(lslot) * kTile;  // diagonal, then L rows
+            lcol[0] = piv;
+            for (int z = dp + 1; z < len; ++z) {
+                const double lv = x[z * kTile] * inv;
+                x[z * kTile] = lv;
+                lcol[size_t(z - dp) * kTile] = lv;
+            }
+            for (int z = 0; z < dp; ++z) lu_t[size_t(r[1 + z]) * kTile] = x[z * kTile];
+            if (FS) {
+                x[len * kTile] = acc_y;
+                b_t[size_t(brow) * kTile] = acc_y;
+            }
+            if (!(v.dbg & 1)) fence_proxy_async_global();  // later TMA re-fetches of this column see it
+            P.cur += 1 + dp;
+        } else if (type == kRecPage) {
+            prog_next_page(P, lane);
+        } else {
+            break;
+        }
+    }
+    if (flagged && v.active[tile * kTile + lane]) v.flag[tile * kTile + lane] = 1;
+}
+
+// Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
+__global__ void __launch_bounds__(32) bs_walk_kernel(DevView v, WalkView w) {
+    const int tile = blockIdx.x, lane = threadIdx.x;
+    if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
+    Prog P;
+    prog_begin(v, w, P, tile, lane);
+    double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
+    double* blk = P.R;
+    int ne = 0, e = 0, brow = 0;
+    double acc = 0.0;
+    for (;;) {
+        const int32_t* r = P.cur;
+        const int32_t h = r[0];
+        const int type = h & 15;
+        if (type == kRecIssue) {
+            P.cur += prog_issue(v, P, r, lane);
+        } else if (type == kRecDep) {
+            const int op = (h >> 4) - 1;
+            const int ysrc = r[1];
+            if (op >= 0) prog_wait(P, op);
+            acc = fma(-blk[e * kTile], P.R[size_t(ysrc) * kTile + lane], acc);
+            ++e;
+            P.cur += 2;
+        } else if (type == kRecStep) {
+            const int ring = r[1] & 0xffff;
+            ne = int(unsigned(r[1]) >> 16);
+            brow = r[4];
+            const int op = r[5];
+            P.cur += 6;
+            prog_wait(P, op);
+            blk = P.R + size_t(ring) * kTile + lane;
+            acc = blk[ne * kTile];
+            e = 0;
+        } else if (type == kRecEnd) {
+            const double xi = acc / blk[(ne + 1) * kTile];
+            blk[ne * kTile] = xi;
+            b_t[size_t(brow) * kTile] = xi;
+            if (!(v.dbg & 1)) fence_proxy_async_global();
+            P.cur += 1;
+        } else if (type == kRecPage) {
+            prog_next_page(P, lane);
+        } else {
+            break;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -698,15 +491,16 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
         return;
     }
     const size_t bp = v.bpad;
+    const double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;  // tile-blocked b tape
     const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
     for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
         const int zt = __ldg(v.zcol_t + bus);
         if (zt < 0) continue;
         const size_t o = size_t(bus) * bp + t;
-        const double va = v.va[o] - v.b[size_t(zt) * bp + t];
+        const double va = v.va[o] - b_t[size_t(zt) * kTile];
         v.va[o] = va;
         const int zv = __ldg(v.zcol_v + bus);
-        if (zv >= 0) v.vm[o] = v.vm[o] - v.b[size_t(zv) * bp + t];
+        if (zv >= 0) v.vm[o] = v.vm[o] - b_t[size_t(zv) * kTile];
         double s, c;
         gb_sincos(va, &s, &c);
         v.s[o] = s;
@@ -719,32 +513,23 @@ __global__ void broadcast_kernel(double* dst, const double* src, int32_t n, int3
     if (i < size_t(n) * bpad) dst[i] = src[i / bpad];
 }
 
-constexpr int kCapX = 24;     // lu_level_kernel: 8 x (24 + 32) x 256 B = 112 KB -> 2 blocks / SM
-constexpr int kCapLong = 80;  // long-column levels: 8 x (80 + 32) x 256 B = 224 KB
-
 unsigned n_super(const DevView& v) { return unsigned((v.n_tiles + kSuper - 1) / kSuper); }
-
-int g_num_sms = 148;
 
 }  // namespace
 
-size_t lu_smem_bytes() { return size_t(kSuper) * (kCapX + kRing) * kTile * sizeof(double); }
-static size_t long_smem_bytes() { return size_t(kSuper) * (kCapLong + kRing) * kTile * sizeof(double); }
+size_t walk_smem_bytes(const WalkView& w) {
+    return size_t(w.ring_rows + w.stage_rows) * kTile * 8 + size_t(kWalkPages) * w.page_words * 4 +
+           size_t(kWalkBars + kWalkPages) * 8;
+}
 
 void configure_kernels() {
-    cudaFuncSetAttribute(lu_level_kernel<kCapX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(lu_smem_bytes()));
-    cudaFuncSetAttribute(lu_level_kernel<kCapX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(lu_level_kernel<kCapLong>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(long_smem_bytes()));
-    cudaFuncSetAttribute(lu_level_kernel<kCapLong>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(lu_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PipeSmem)));
-    cudaFuncSetAttribute(tri_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(TriSmem)));
-    cudaFuncSetAttribute(tri_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(TriSmem)));
-    cudaFuncSetAttribute(lu_pipe_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    const int max_smem = 227 * 1024;
+    cudaFuncSetAttribute(lu_walk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    cudaFuncSetAttribute(lu_walk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    cudaFuncSetAttribute(bs_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    cudaFuncSetAttribute(lu_walk_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(lu_walk_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(bs_walk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 void launch_init(const DevView& v, cudaStream_t st) {
@@ -761,36 +546,16 @@ void launch_jacobian(const DevView& v, cudaStream_t st) {
     jacobian_kernel<<<dim3(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v)), 256, 0, st>>>(v);
 }
 
-// Level launch: wide levels use the persistent pipelined kernel (one block per
-// SM); levels holding a column longer than the pipeline's 24-row working set
-// use the one-item-per-block kernel with an 80-row working set; the rest the
-// one-item kernel with 2 blocks per SM.
-void launch_lu_short(const DevView& v, int pos0, int ncols, int maxlen, cudaStream_t st) {
-    if (ncols <= 0) return;
-    const size_t items = size_t(ncols) * n_super(v);
-    const unsigned grid = unsigned(std::min<size_t>(items, size_t(g_num_sms)));
-    const int nxb = maxlen <= 12 ? 4 : (maxlen <= 16 ? 3 : 2);  // x buffers in flight
-    lu_pipe_kernel<<<grid, kPipeThreads, sizeof(PipeSmem), st>>>(v, v.lu_short, pos0, ncols, nxb);
+void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {
+    const size_t smem = walk_smem_bytes(w);
+    if (fs)
+        lu_walk_kernel<true><<<unsigned(v.n_tiles), kTile, smem, st>>>(v, w);
+    else
+        lu_walk_kernel<false><<<unsigned(v.n_tiles), kTile, smem, st>>>(v, w);
 }
 
-void launch_lu_long(const DevView& v, int pos0, int ncols, int maxlen, cudaStream_t st) {
-    if (ncols <= 0) return;
-    if (maxlen > kCapX)
-        lu_level_kernel<kCapLong><<<dim3(n_super(v), unsigned(ncols)), 256, long_smem_bytes(), st>>>(
-            v, v.lu_long, pos0);
-    else
-        lu_level_kernel<kCapX><<<dim3(n_super(v), unsigned(ncols)), 256, lu_smem_bytes(), st>>>(
-            v, v.lu_long, pos0);
-}
-
-void launch_tri_level(const DevView& v, bool back, int pos0, int nrows, cudaStream_t st) {
-    if (nrows <= 0) return;
-    const size_t items = size_t(nrows) * n_super(v);
-    const unsigned grid = unsigned(std::min<size_t>(items, size_t(g_num_sms)));
-    if (back)
-        tri_pipe_kernel<true><<<grid, kPipeThreads, sizeof(TriSmem), st>>>(v, pos0, nrows);
-    else
-        tri_pipe_kernel<false><<<grid, kPipeThreads, sizeof(TriSmem), st>>>(v, pos0, nrows);
+void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st) {
+    bs_walk_kernel<<<unsigned(v.n_tiles), kTile, walk_smem_bytes(w), st>>>(v, w);
 }
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {

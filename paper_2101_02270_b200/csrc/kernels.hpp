@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "symbolic.hpp"
+#include "walk.hpp"
 
 namespace gbnr {
 
@@ -22,19 +23,13 @@ struct DevView {
     const double *yre, *yim;
     const int32_t *rows, *brow_p, *brow_q, *zcol_t, *zcol_v;
     const int32_t* lk;
-    const ColInfo* col;
-    const int32_t *upd_ls, *upd_dk;  // update records: LU slot / dst | kpos << 16
-    const int32_t* lu_sched;
-    const int32_t *lu_short, *lu_long;  // per-level column lists split by working-set size
-    const RowInfo *lrow, *urow;
-    const RowEnt *lent, *uent;
-    const int32_t *fs_sched, *bs_sched;
     // per-task tapes [elem][bpad]
     double *vm, *va, *c, *s;
     const double *vm_in, *va_in;  // staged start voltages (kept for repeated runs)
     const double *p0, *q0;
     int32_t s_ld, s_inc;          // p0[bus * s_ld + task * s_inc]
-    double *A, *LU, *b;           // [nnzLU][bpad], [nnzLU][bpad], [nJ][bpad]
+    double *A, *LU;               // tile-blocked [n_tiles][nnzLU][32]
+    double* b;                    // tile-blocked [n_tiles][nJ][32]: F, then y (forward walk), then dx
     // per-task state
     int32_t *status, *iters;
     uint8_t *active, *flag;
@@ -44,16 +39,22 @@ struct DevView {
     int32_t* it_dev;                // Newton iteration counter on the device
     double tol, singular_tol;
     int32_t max_iter;
+    int32_t dbg;                    // experiment switches (GBNR_DBG), 0 in production
 };
 
-size_t lu_smem_bytes();
+// Device copy of a Walk (walk.hpp).
+struct WalkView {
+    const int32_t* stream;  // program words (walk.hpp kRec*)
+    int32_t n_pages, page_words, pages, ring_rows, stage_rows, barriers;
+};
+
+size_t walk_smem_bytes(const WalkView& w);
 void configure_kernels();
 void launch_init(const DevView& v, cudaStream_t st);
 void launch_npm(const DevView& v, cudaStream_t st);  // NPM + convergence + iteration bump
 void launch_jacobian(const DevView& v, cudaStream_t st);
-void launch_lu_short(const DevView& v, int pos0, int ncols, int maxlen, cudaStream_t st);
-void launch_lu_long(const DevView& v, int pos0, int ncols, int maxlen, cudaStream_t st);
-void launch_tri_level(const DevView& v, bool back, int pos0, int nrows, cudaStream_t st);
+void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st);
+void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st);
 void launch_vupdate(const DevView& v, cudaStream_t st);
 void launch_broadcast(double* dst, const double* src, int32_t n, int32_t bpad, cudaStream_t st);
 

@@ -66,6 +66,9 @@ enum Phase { kNpm = 0, kJac, kLu, kFsbs, kVupd, kPhases };
 
 struct gbnr_plan {
     gbnr::Symbolic sym;
+    gbnr::LuLayout lay;
+    gbnr::Walk wf, wl, wb;           // forward LU+FS, LU-only, backward walks
+    gbnr::WalkView vf{}, vl{}, vb{};
     gbnr_options opt{};
     bool on_device = false;
     cudaStream_t stream = nullptr;
@@ -73,7 +76,6 @@ struct gbnr_plan {
     double* d_scratch = nullptr;  // [n] staging for broadcast sets
     std::vector<void*> batch;     // per-batch tapes
     int32_t cap_tiles = 0;        // allocated tile capacity
-    int32_t a_zeroed_bpad = -1;   // layout for which the A tape's fill slots are zero
     bool staged = false;
     gbnr::DevView v{};
     int32_t* h_count = nullptr;   // pinned
@@ -120,33 +122,32 @@ struct gbnr_plan {
         v.zcol_t = dev_upload(owned, s.zcol_t);
         v.zcol_v = dev_upload(owned, s.zcol_v);
         v.lk = dev_upload(owned, s.lk);
-        v.col = dev_upload(owned, s.col);
-        {
-            // records split and padded so warp-wide 32-record window loads stay in bounds
-            std::vector<int32_t> ls(s.upd.size() + 96, 0), dk(s.upd.size() + 96, 0);
-            for (size_t u = 0; u < s.upd.size(); ++u) {
-                ls[u] = s.upd[u].lslot;
-                dk[u] = s.upd[u].dst_kpos;
-            }
-            v.upd_ls = dev_upload(owned, ls);
-            v.upd_dk = dev_upload(owned, dk);
-        }
-        v.lu_sched = dev_upload(owned, s.lu_sched);
-        v.lu_short = dev_upload(owned, s.lu_short);
-        v.lu_long = dev_upload(owned, s.lu_long);
-        v.lrow = dev_upload(owned, s.lrow);
-        v.urow = dev_upload(owned, s.urow);
-        v.lent = dev_upload(owned, s.lent);
-        v.uent = dev_upload(owned, s.uent);
-        v.fs_sched = dev_upload(owned, s.fs_sched);
-        v.bs_sched = dev_upload(owned, s.bs_sched);
+        vf = upload_walk(wf);
+        vl = upload_walk(wl);
+        vb = upload_walk(wb);
         int32_t* itd = nullptr;
         CK(cudaMalloc(&itd, sizeof(int32_t)));
         owned.push_back(itd);
         v.it_dev = itd;
+        if (const char* d = std::getenv("GBNR_DBG")) v.dbg = std::atoi(d);
         v.tol = opt.tol;
         v.singular_tol = opt.singular_tol;
         v.max_iter = opt.max_iter;
+    }
+
+    gbnr::WalkView upload_walk(const gbnr::Walk& w) {
+        gbnr::WalkView x{};
+        x.stream = dev_upload(owned, w.stream);
+        x.n_pages = w.n_pages;
+        x.page_words = w.page_words;
+        x.pages = w.pages;
+        x.ring_rows = w.ring_rows;
+        x.stage_rows = w.stage_rows;
+        x.barriers = w.barriers;
+        if (w.barriers != 32 || w.pages != 4) throw Error(GBNR_ECONFIG, "walk kernels use 32 barriers, 4 pages");
+        if (gbnr::walk_smem_bytes(x) > 227 * 1024)
+            throw Error(GBNR_ECONFIG, "walk needs more shared memory than a B200 CTA has");
+        return x;
     }
 
     void set_ybus(const double* re, const double* im) {
@@ -178,7 +179,9 @@ struct gbnr_plan {
         v.q0 = static_cast<double*>(alloc(nb));
         const size_t lub = size_t(v.nnzLU) * bpad * sizeof(double);
         v.A = static_cast<double*>(alloc(lub));
-        a_zeroed_bpad = -1;
+        // fill slots of the A tape are never written by the Jacobian kernel and
+        // must read zero; tile-blocked addresses do not depend on the batch size
+        CK(cudaMemsetAsync(v.A, 0, lub, stream));
         v.LU = static_cast<double*>(alloc(lub));
         v.b = static_cast<double*>(alloc(size_t(v.nJ) * bpad * sizeof(double)));
         v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
@@ -219,12 +222,6 @@ struct gbnr_plan {
         v.n_tiles = n_tiles;
         v.bpad = n_tiles * gbnr::kTile;
         v.n_tasks = n_tasks;
-        if (a_zeroed_bpad != v.bpad) {
-            // fill slots of the A tape are never written by the Jacobian kernel and must
-            // read zero; their element-major addresses move whenever bpad changes
-            CK(cudaMemsetAsync(v.A, 0, size_t(v.nnzLU) * v.bpad * sizeof(double), stream));
-            a_zeroed_bpad = v.bpad;
-        }
         put_tape(const_cast<double*>(v.vm_in), vm0, n_vsets, n_tasks);
         put_tape(const_cast<double*>(v.va_in), va0, n_vsets, n_tasks);
         if (n_ssets == 1 && n_tasks > 1) {
@@ -270,32 +267,12 @@ struct gbnr_plan {
         ev_used.clear();
     }
 
-    // LU: one launch per level (level order = topological order of the column DAG)
-    void launch_lu_all() {
-        const gbnr::Symbolic& s = sym;
-        for (int32_t l = 0; l < s.levels_lu; ++l) {
-            gbnr::launch_lu_short(v, s.lu_short_ptr[l], s.lu_short_ptr[l + 1] - s.lu_short_ptr[l],
-                                  s.lu_short_maxlen[l], stream);
-            gbnr::launch_lu_long(v, s.lu_long_ptr[l], s.lu_long_ptr[l + 1] - s.lu_long_ptr[l],
-                                 s.lu_long_maxlen[l], stream);
-        }
-    }
+    // LU refactorization fused with the forward substitution, then the
+    // backward substitution: one launch each (tile walks, walk.hpp)
+    void launch_lu_all() { gbnr::launch_lu_walk(v, vf, true, stream); }
+    void launch_fsbs_all() { gbnr::launch_bs_walk(v, vb, stream); }
 
-    // FS then BS, one launch per level
-    void launch_fsbs_all() {
-        const gbnr::Symbolic& s = sym;
-        for (int32_t l = 0; l < s.levels_fs; ++l)
-            gbnr::launch_tri_level(v, false, s.fs_lvl_ptr[l], s.fs_lvl_ptr[l + 1] - s.fs_lvl_ptr[l], stream);
-        for (int32_t l = 0; l < s.levels_bs; ++l)
-            gbnr::launch_tri_level(v, true, s.bs_lvl_ptr[l], s.bs_lvl_ptr[l + 1] - s.bs_lvl_ptr[l], stream);
-    }
-
-    int launches_per_iteration() const {
-        int lu = 0;
-        for (int32_t l = 0; l < sym.levels_lu; ++l)
-            lu += (sym.lu_short_ptr[l + 1] > sym.lu_short_ptr[l]) + (sym.lu_long_ptr[l + 1] > sym.lu_long_ptr[l]);
-        return 1 + lu + sym.levels_fs + sym.levels_bs + 1 + 3;
-    }
+    static int launches_per_iteration() { return 7; }  // jac, lu+fs, bs, vupd, npm, conv, bump
 
     void run() {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_run before gbnr_stage");
@@ -371,46 +348,28 @@ struct gbnr_plan {
         gbnr::launch_init(v, stream);
         gbnr::launch_jacobian(v, stream);
         CK(cudaGetLastError());
-        launch_lu_all();  // warm-up
+        gbnr::launch_lu_walk(v, vl, false, stream);  // warm-up
         CK(cudaEventRecord(ev0, stream));
-        for (int32_t r = 0; r < reps; ++r) launch_lu_all();
+        for (int32_t r = 0; r < reps; ++r) gbnr::launch_lu_walk(v, vl, false, stream);
         CK(cudaEventRecord(ev1, stream));
         CK(cudaGetLastError());
         CK(cudaEventSynchronize(ev1));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
         if (ms_out) *ms_out = reps > 0 ? ms / reps : 0.0;
-        if (const char* e = std::getenv("GBNR_LEVEL_PROFILE"); e && *e == '1') {
-            // per-level device times of one refactorization (diagnostics)
-            std::vector<cudaEvent_t> evs(sym.levels_lu + 1);
-            for (auto& x : evs) CK(cudaEventCreate(&x));
-            for (int32_t l = 0; l < sym.levels_lu; ++l) {
-                CK(cudaEventRecord(evs[l], stream));
-                gbnr::launch_lu_short(v, sym.lu_short_ptr[l], sym.lu_short_ptr[l + 1] - sym.lu_short_ptr[l],
-                                      sym.lu_short_maxlen[l], stream);
-                gbnr::launch_lu_long(v, sym.lu_long_ptr[l], sym.lu_long_ptr[l + 1] - sym.lu_long_ptr[l],
-                                     sym.lu_long_maxlen[l], stream);
-            }
-            CK(cudaEventRecord(evs[sym.levels_lu], stream));
-            CK(cudaStreamSynchronize(stream));
-            double acc = 0;
-            for (int32_t l = 0; l < sym.levels_lu; ++l) {
-                float lm = 0.f;
-                CK(cudaEventElapsedTime(&lm, evs[l], evs[l + 1]));
-                acc += lm;
-                int maxlen = 0;
-                for (int32_t p = sym.lu_lvl_ptr[l]; p < sym.lu_lvl_ptr[l + 1]; ++p)
-                    maxlen = std::max(maxlen, sym.col[sym.lu_sched[p]].len_dp & 0xffff);
-                std::fprintf(stderr, "[gbnr] level %3d cols %5d maxlen %3d  %8.3f ms  cum %8.3f\n", l,
-                             sym.lu_lvl_ptr[l + 1] - sym.lu_lvl_ptr[l], maxlen, lm, acc);
-            }
-            for (auto& x : evs) cudaEventDestroy(x);
-        }
         const int32_t nt = v.n_tasks;
         if (flags_out) CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
-        if (lu_out)
-            CK(cudaMemcpy2D(lu_out, size_t(nt) * 8, v.LU, size_t(v.bpad) * 8, size_t(nt) * 8,
-                            size_t(v.nnzLU), cudaMemcpyDeviceToHost));
+        if (lu_out) {
+            // tile-blocked tape -> element-major CCS order [nnzLU][n_tasks]
+            const size_t z = size_t(v.nnzLU);
+            std::vector<double> tape(size_t(v.n_tiles) * z * gbnr::kTile);
+            CK(cudaMemcpy(tape.data(), v.LU, tape.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            for (size_t c = 0; c < z; ++c) {
+                const size_t ts = size_t(lay.tape_of_ccs[c]);
+                for (int32_t t = 0; t < nt; ++t)
+                    lu_out[c * nt + t] = tape[(size_t(t / gbnr::kTile) * z + ts) * gbnr::kTile + t % gbnr::kTile];
+            }
+        }
     }
 };
 
@@ -423,9 +382,11 @@ void gbnr_default_options(gbnr_options* o) {
     o->pivot_tol = 1e-3;
     o->singular_tol = 1e-14;
     o->device = 0;
-    o->lu_warps = 4;
+    o->ring_rows = 176;
     o->profile = 0;
-    o->fs_warps = 8;
+    o->stage_rows = 80;
+    o->prefetch = 8;
+    o->headroom = 2;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -473,10 +434,19 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             gbnr_default_options(&p->opt);
         if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 30)
             throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 30");
-        if (p->opt.fs_warps < 0 || p->opt.lu_warps < 0) throw Error(GBNR_ECONFIG, "negative warp count");
-        const int bulk = p->opt.bulk_min ? p->opt.bulk_min : 32;
+        if (p->opt.ring_rows < 0 || p->opt.stage_rows < 0 || p->opt.prefetch < 0 || p->opt.headroom < 0)
+            throw Error(GBNR_ECONFIG, "negative walk parameter");
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
-                       p->opt.pivot_tol, bulk);
+                       p->opt.pivot_tol);
+        p->lay = gbnr::build_lu_layout(p->sym);
+        gbnr::WalkConfig wc;
+        if (p->opt.ring_rows) wc.ring_rows = p->opt.ring_rows;
+        if (p->opt.stage_rows) wc.stage_rows = p->opt.stage_rows;
+        if (p->opt.prefetch) wc.prefetch = p->opt.prefetch;
+        if (p->opt.headroom) wc.headroom = p->opt.headroom;
+        p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
+        p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
+        p->wb = gbnr::build_backward_walk(p->sym, p->lay, wc);
         if (p->opt.device >= 0) {
             int ndev = 0;
             CK(cudaGetDeviceCount(&ndev));
@@ -560,6 +530,48 @@ int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* 
 
 int gbnr_last_timing(const gbnr_plan* p, double* out) {
     return guarded([&] { std::memcpy(out, p->timing, sizeof p->timing); });
+}
+
+static const gbnr::Walk& pick_walk(const gbnr_plan* p, int32_t which) {
+    if (which == 0) return p->wf;
+    if (which == 1) return p->wl;
+    if (which == 2) return p->wb;
+    throw Error(GBNR_ECONFIG, "walk index must be 0, 1 or 2");
+}
+
+int gbnr_walk_info(const gbnr_plan* p, int32_t which, int64_t* o) {
+    return guarded([&] {
+        const gbnr::Walk& w = pick_walk(p, which);
+        const int64_t vals[17] = {w.n_steps, int64_t(w.dep.size()), int64_t(w.dst.size()),
+                                  int64_t(w.op.size()), int64_t(w.ut.size()), w.ring_rows,
+                                  w.stage_rows, w.barriers, w.events, w.ring_dep_rows,
+                                  w.fetched_rows, int64_t(w.smem_bytes()),
+                                  int64_t(w.stream.size()), w.page_words, w.pages, w.n_pages,
+                                  int64_t(w.copies.size())};
+        std::memcpy(o, vals, sizeof vals);
+    });
+}
+
+int gbnr_walk_export(const gbnr_plan* p, int32_t which, int32_t part, void* dst) {
+    return guarded([&] {
+        const gbnr::Walk& w = pick_walk(p, which);
+        auto put = [&](const auto& vec) {
+            if (!vec.empty()) std::memcpy(dst, vec.data(), vec.size() * sizeof(vec[0]));
+        };
+        switch (part) {
+            case 0: put(w.step); break;
+            case 1: put(w.dep); break;
+            case 2: put(w.dst); break;
+            case 3: put(w.op); break;
+            case 4: put(w.ut); break;
+            case 5: put(p->lay.tape_of_ccs); break;
+            case 6: put(p->lay.lslot); break;
+            case 7: put(p->lay.ucrs0); break;
+            case 8: put(w.stream); break;
+            case 9: put(w.copies); break;
+            default: throw Error(GBNR_ECONFIG, "walk part must be 0..9");
+        }
+    });
 }
 
 int gbnr_refactor(gbnr_plan* p, int32_t reps, double* lu_out, uint8_t* flags_out, double* ms_out) {

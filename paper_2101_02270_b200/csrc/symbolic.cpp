@@ -184,8 +184,7 @@ std::vector<int32_t> amd_order(int32_t n, const int32_t* col_ptr, const int32_t*
 void Symbolic::analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indices,
                        const double* y_re, const double* y_im, int32_t ref_bus, const int32_t* pv,
                        int32_t n_pv, const int32_t* pq, int32_t n_pq, const double* vm0,
-                       const double* va0, double pivot_tol, int32_t bulk_min_entries) {
-    bulk_min = bulk_min_entries;
+                       const double* va0, double pivot_tol) {
     n = n_bus;
     ref = ref_bus;
     npv = n_pv;
@@ -413,114 +412,15 @@ void Symbolic::analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         levels_bs = std::max(levels_bs, bl[k] + 1);
         for (int32_t z = cp[k]; z < dpos[k]; ++z) bl[ri[z]] = std::max(bl[ri[z]], bl[k] + 1);
     }
-    auto schedule = [&](const std::vector<int32_t>& lev, std::vector<int32_t>& order,
-                        std::vector<int32_t>& pos) {
-        order.resize(nJ);
-        for (int32_t i = 0; i < nJ; ++i) order[i] = i;
-        std::stable_sort(order.begin(), order.end(),
-                         [&](int32_t a, int32_t b) { return lev[a] < lev[b]; });
-        pos.assign(nJ, 0);
-        for (int32_t p = 0; p < nJ; ++p) pos[order[p]] = p;
-    };
-    std::vector<int32_t> lu_pos, fs_pos, bs_pos;
-    schedule(level, lu_sched, lu_pos);
-    schedule(fl, fs_sched, fs_pos);
-    schedule(bl, bs_sched, bs_pos);
-    // level pointers and the bulk / sync-free split (Alg. 3 stages):
-    // LU and FS: the prefix of levels with >= bulk_min entries runs as one
-    // whole-GPU launch per level, the rest in the per-tile sync-free kernel.
-    // BS runs the other way round (its narrow levels come first).
-    auto lvl_ptr = [&](const std::vector<int32_t>& lev, int32_t nlev) {
-        std::vector<int32_t> ptr(nlev + 1, 0);
-        for (int32_t i = 0; i < nJ; ++i) ptr[lev[i] + 1]++;
-        for (int32_t l = 0; l < nlev; ++l) ptr[l + 1] += ptr[l];
-        return ptr;
-    };
-    lu_lvl_ptr = lvl_ptr(level, levels_lu);
-    lu_lvl_maxlen.assign(levels_lu, 0);
-    for (int32_t k = 0; k < nJ; ++k)
-        lu_lvl_maxlen[level[k]] = std::max(lu_lvl_maxlen[level[k]], cp[k + 1] - cp[k]);
-    lu_short.clear();
-    lu_long.clear();
-    lu_short_ptr.assign(levels_lu + 1, 0);
-    lu_long_ptr.assign(levels_lu + 1, 0);
-    lu_long_maxlen.assign(levels_lu, 0);
-    lu_short_maxlen.assign(levels_lu, 0);
-    for (int32_t l = 0; l < levels_lu; ++l) {
-        for (int32_t p = lu_lvl_ptr[l]; p < lu_lvl_ptr[l + 1]; ++p) {
-            const int32_t k = lu_sched[p], len = cp[k + 1] - cp[k];
-            if (len <= short_cap) {
-                lu_short.push_back(k);
-                lu_short_maxlen[l] = std::max(lu_short_maxlen[l], len);
-            } else {
-                lu_long.push_back(k);
-                lu_long_maxlen[l] = std::max(lu_long_maxlen[l], len);
-            }
-        }
-        lu_short_ptr[l + 1] = int32_t(lu_short.size());
-        lu_long_ptr[l + 1] = int32_t(lu_long.size());
-    }
-    fs_lvl_ptr = lvl_ptr(fl, levels_fs);
-    bs_lvl_ptr = lvl_ptr(bl, levels_bs);
-    auto wide_prefix = [&](const std::vector<int32_t>& ptr, int32_t nlev) {
-        int32_t l = 0;
-        while (l < nlev && ptr[l + 1] - ptr[l] >= bulk_min) ++l;
-        return l;
-    };
-    lu_split = wide_prefix(lu_lvl_ptr, levels_lu);
-    fs_split = wide_prefix(fs_lvl_ptr, levels_fs);
-    {
-        int32_t l = 0;  // BS: narrow prefix goes to the sync-free kernel
-        while (l < levels_bs && bs_lvl_ptr[l + 1] - bs_lvl_ptr[l] < bulk_min) ++l;
-        bs_split = l;
-    }
-    const int32_t lu_p0 = lu_lvl_ptr[lu_split], fs_p0 = fs_lvl_ptr[fs_split];
-    const int32_t bs_p1 = bs_lvl_ptr[bs_split];
-
-    // ---- refactorization program (Alg. 2 with static destinations) ----
-    col.resize(nJ);
-    dep_wait.clear();
-    upd.clear();
-    std::vector<int32_t> posmap(nJ, -1);
+    // ---- VMAD count D = sum over U dependencies k of |L(:,k)| ----
     D = 0;
     max_udeps = 0;
     for (int32_t k = 0; k < nJ; ++k) {
-        const int32_t len = cp[k + 1] - cp[k], dp = dpos[k] - cp[k];
-        ColInfo ci{cp[k], len | (dp << 16), int32_t(dep_wait.size()), dp, int32_t(upd.size()), 0, 0, 0};
-        max_udeps = std::max(max_udeps, dp);
-        for (int32_t z = cp[k]; z < cp[k + 1]; ++z) posmap[ri[z]] = z - cp[k];
+        max_udeps = std::max(max_udeps, dpos[k] - cp[k]);
         for (int32_t z = cp[k]; z < dpos[k]; ++z) {
             const int32_t j = ri[z];
-            dep_wait.push_back(lu_pos[j] >= lu_p0 ? lu_pos[j] - lu_p0 : -1);
-            for (int32_t zz = dpos[j] + 1; zz < cp[j + 1]; ++zz) {
-                const int32_t d = posmap[ri[zz]];
-                if (d < 0) throw Error(2, "frozen LU pattern is not closed");
-                upd.push_back(Upd{zz, d | ((z - cp[k]) << 16)});
-            }
             D += cp[j + 1] - dpos[j] - 1;
         }
-        ci.nu = int32_t(upd.size()) - ci.u0;
-        col[k] = ci;
-        for (int32_t z = cp[k]; z < cp[k + 1]; ++z) posmap[ri[z]] = -1;
-    }
-
-    // ---- row lists for pull-style FS (L, ascending k) and BS (U, descending k) ----
-    std::vector<std::vector<std::pair<int32_t, int32_t>>> Lrow(nJ), Urow(nJ);  // (k, slot)
-    for (int32_t k = 0; k < nJ; ++k) {
-        for (int32_t z = cp[k]; z < dpos[k]; ++z) Urow[ri[z]].emplace_back(k, z);
-        for (int32_t z = dpos[k] + 1; z < cp[k + 1]; ++z) Lrow[ri[z]].emplace_back(k, z);
-    }
-    lrow.resize(nJ);
-    urow.resize(nJ);
-    lent.clear();
-    uent.clear();
-    for (int32_t i = 0; i < nJ; ++i) {
-        std::sort(Lrow[i].begin(), Lrow[i].end());
-        lrow[i] = RowInfo{int32_t(lent.size()), int32_t(Lrow[i].size()), dpos[i], 0};
-        for (auto [k, z] : Lrow[i]) lent.push_back(RowEnt{z, k, fs_pos[k] >= fs_p0 ? fs_pos[k] - fs_p0 : -1, 0});
-        std::sort(Urow[i].begin(), Urow[i].end(), std::greater<>());
-        urow[i] = RowInfo{int32_t(uent.size()), int32_t(Urow[i].size()), dpos[i], 0};
-        for (auto [k, z] : Urow[i]) uent.push_back(RowEnt{z, k, bs_pos[k] < bs_p1 ? bs_pos[k] : -1, 0});
     }
 
     // ---- NPM / J row list, b rows and z columns per bus ----

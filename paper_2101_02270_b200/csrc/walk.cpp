@@ -1,0 +1,532 @@
+// walk.cpp -- host planner of the tile-owned LU/FS and BS walks (see walk.hpp).
+#include "walk.hpp"
+
+#include <algorithm>
+#include <deque>
+#include <limits>
+#include <string>
+
+namespace gbnr {
+
+namespace {
+
+constexpr int32_t kInf = std::numeric_limits<int32_t>::max();
+
+WCopy copy(int32_t tape, int32_t slot, int32_t rows, int32_t smem_rel) {
+    return WCopy{tape | (rows << 8), slot, smem_rel, 0};
+}
+int32_t copy_rows(const WCopy& c) { return c.tape_rows >> 8; }
+
+// What a step loads into its own ring block, and what each dependency needs.
+struct DepIn {
+    int32_t producer;        // producing step
+    int32_t ring_src = -1;   // rows relative to the producer's block
+    int32_t ring_ysrc = -1;
+    std::vector<WCopy> fetch;  // copies relative to a staging allocation
+    int32_t fetch_rows = 0;
+    int32_t stage_src = -1, stage_ysrc = -1;
+    WDep rec{};                // payload fields (kpos_fs, nrows, u0)
+};
+struct StepIn {
+    int32_t blk_rows = 0;
+    std::vector<WCopy> copies;  // smem relative to the block
+    std::vector<DepIn> deps;
+    WStep rec{};                // payload fields (len_dp, lslot, ut0, brow)
+};
+
+// Allocate rows [cur, cur+n) in a ring of `cap` rows; skip to the start when
+// the request does not fit before the end (TMA copies must be contiguous).
+int32_t ring_alloc(int32_t& cur, int32_t n, int32_t cap) {
+    if (cur + n > cap) cur = 0;
+    const int32_t at = cur;
+    cur += n;
+    return at;
+}
+
+Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
+    const int32_t T = static_cast<int32_t>(steps.size());
+    Walk w;
+    int32_t max_blk = 0, max_fetch = 0;
+    for (const StepIn& s : steps) {
+        max_blk = std::max(max_blk, s.blk_rows);
+        for (const DepIn& d : s.deps) max_fetch = std::max(max_fetch, d.fetch_rows);
+    }
+    w.ring_rows = std::max(cfg.ring_rows, max_blk);
+    w.stage_rows = std::max(cfg.stage_rows, max_fetch);
+    w.barriers = cfg.barriers;
+    w.n_steps = T;
+    const int32_t XR = w.ring_rows, SR = w.stage_rows, NB = w.barriers;
+
+    // 1. ring placement and first overwriter of every block
+    std::vector<int32_t> ring(T), ovw(T, kInf);
+    std::vector<std::vector<int32_t>> ovl(T);
+    {
+        int32_t cur = 0;
+        std::deque<int32_t> live;
+        for (int32_t t = 0; t < T; ++t) {
+            ring[t] = ring_alloc(cur, steps[t].blk_rows, XR);
+            const int32_t a = ring[t], b = a + steps[t].blk_rows;
+            std::deque<int32_t> keep;
+            for (int32_t c : live) {
+                const int32_t ca = ring[c], cb = ca + steps[c].blk_rows;
+                if (ca < b && a < cb && steps[t].blk_rows > 0 && steps[c].blk_rows > 0) {
+                    ovw[c] = t;
+                    ovl[t].push_back(c);
+                } else {
+                    keep.push_back(c);
+                }
+            }
+            keep.push_back(t);
+            live.swap(keep);
+        }
+    }
+    // 2. ring residency of every dependency; last ring reader of every block
+    std::vector<int32_t> lastuser(T);
+    for (int32_t t = 0; t < T; ++t) lastuser[t] = t;
+    std::vector<std::vector<char>> resident(T);
+    for (int32_t t = 0; t < T; ++t) {
+        resident[t].resize(steps[t].deps.size());
+        for (size_t d = 0; d < steps[t].deps.size(); ++d) {
+            const DepIn& di = steps[t].deps[d];
+            if (di.producer >= t) throw Error(3, "walk dependency is not earlier in the walk");
+            const bool res = ovw[di.producer] == kInf || t + cfg.headroom < ovw[di.producer];
+            resident[t][d] = res;
+            if (res) lastuser[di.producer] = std::max(lastuser[di.producer], t);
+        }
+    }
+    // 3. consumer events: one after every dependency, one when the step is done
+    std::vector<int64_t> ev0(T + 1);
+    int64_t e = 0;
+    for (int32_t t = 0; t < T; ++t) {
+        ev0[t] = e;
+        e += int64_t(steps[t].deps.size()) + 1;
+    }
+    ev0[T] = e;
+    w.events = e;
+    if (e >= kInf) throw Error(3, "walk too long");
+    auto ev_dep = [&](int32_t t, size_t d) { return int32_t(ev0[t] + int64_t(d)); };
+    auto ev_done = [&](int32_t t) { return t < 0 ? -1 : int32_t(ev0[t + 1] - 1); };
+
+    // 4. ops in consumption order with their issue events.  One op per step
+    //    carries the step's block AND every re-fetched dependency whose staging
+    //    region fits beside the others (a "chunk"); a step whose fetches exceed
+    //    the staging ring continues in further chunks, each waited on at its
+    //    first dependency.
+    struct Live {
+        int32_t a, b, release;
+    };
+    std::deque<Live> stage_live;
+    int32_t scur = 0;
+    std::vector<int32_t> release;  // per op: event after which its mbarrier may be re-armed
+    std::vector<int32_t> tag_of_copy;  // content tag per copy (verification)
+    std::vector<int32_t> dep_tag0(T + 1, 0);  // tag of dependency (t, d) = T + dep_tag0[t] + d
+    for (int32_t t = 0; t < T; ++t) dep_tag0[t + 1] = dep_tag0[t] + int32_t(steps[t].deps.size());
+    std::vector<int32_t> tag_producer(dep_tag0[T], -1), op_of_tag(dep_tag0[T], kInf);
+    for (int32_t t = 0; t < T; ++t)
+        for (size_t d = 0; d < steps[t].deps.size(); ++d) tag_producer[dep_tag0[t] + d] = steps[t].deps[d].producer;
+
+    struct Chunk {
+        std::vector<WCopy> cps;
+        std::vector<int32_t> tags;
+        int32_t after = -1, consume = -1, rel = -1, lo = kInf, hi = -1;  // staging span
+    };
+    auto push_chunk = [&](Chunk& c) {
+        const int32_t s = static_cast<int32_t>(w.op.size());
+        int32_t after = c.after;
+        if (s >= NB) after = std::max(after, release[s - NB]);
+        if (s > 0) after = std::max(after, w.op[s - 1].after);
+        if (after > c.consume) throw Error(3, "walk plan infeasible (shared-memory rings too small)");
+        WOp o{};
+        o.after = after;
+        o.ncopy = static_cast<int32_t>(c.cps.size());
+        o.c0 = static_cast<int32_t>(w.copies.size());
+        for (size_t i = 0; i < c.cps.size(); ++i) {
+            o.bytes += copy_rows(c.cps[i]) * 256;
+            w.copies.push_back(c.cps[i]);
+            tag_of_copy.push_back(c.tags[i]);
+            if (c.tags[i] >= T) op_of_tag[c.tags[i] - T] = s;
+        }
+        w.op.push_back(o);
+        release.push_back(c.rel);
+        return s;
+    };
+    for (int32_t t = 0; t < T; ++t) {
+        StepIn& si = steps[t];
+        WStep rec = si.rec;
+        rec.ring = ring[t];
+        rec.dep0 = static_cast<int32_t>(w.dep.size());
+        rec.ndep = static_cast<int32_t>(si.deps.size());
+        w.block_rows += si.blk_rows;
+        Chunk ch;
+        ch.after = ev_done(t - cfg.prefetch - 1);
+        for (int32_t c : ovl[t]) ch.after = std::max(ch.after, ev_done(std::max(c, lastuser[c])));
+        ch.consume = ev_done(t - 1);
+        ch.rel = int32_t(ev0[t]);  // barrier free once the step-start wait has passed
+        for (WCopy c : si.copies) {
+            c.smem += ring[t];
+            ch.cps.push_back(c);
+            ch.tags.push_back(t);
+        }
+        bool first_chunk = true;
+        std::vector<size_t> chunk_deps;  // deps (indices into w.dep) of the open chunk
+        auto close_chunk = [&]() {
+            const int32_t op = push_chunk(ch);
+            if (first_chunk)
+                rec.op = op;
+            else
+                w.dep[chunk_deps.front()].op = op;  // waited on at its first dependency
+            first_chunk = false;
+            chunk_deps.clear();
+        };
+        for (size_t d = 0; d < si.deps.size(); ++d) {
+            DepIn& di = si.deps[d];
+            WDep dr = di.rec;
+            dr.op = -1;
+            if (resident[t][d]) {
+                dr.src = di.ring_src >= 0 ? ring[di.producer] + di.ring_src : -1;
+                dr.ysrc = di.ring_ysrc >= 0 ? ring[di.producer] + di.ring_ysrc : -1;
+                w.ring_dep_rows += di.fetch_rows;
+                w.dep.push_back(dr);
+                continue;
+            }
+            if (di.fetch_rows <= 0) throw Error(3, "walk dependency with nothing to fetch");
+            int32_t cur = scur;
+            const int32_t at = XR + ring_alloc(cur, di.fetch_rows, SR);
+            // a region overlapping this chunk's own staging span starts a new chunk
+            if (!ch.tags.empty() && at < ch.hi && ch.lo < at + di.fetch_rows) {
+                close_chunk();
+                ch = Chunk{};
+                ch.after = ev_done(t - cfg.prefetch - 1);
+                ch.consume = d == 0 ? ev_done(t - 1) : ev_dep(t, d - 1);
+                ch.rel = ev_dep(t, d);
+            }
+            scur = cur;
+            ch.lo = std::min(ch.lo, at);
+            ch.hi = std::max(ch.hi, at + di.fetch_rows);
+            if (di.producer >= 0) ch.after = std::max(ch.after, ev_done(di.producer));
+            std::deque<Live> keep;
+            for (const Live& l : stage_live) {
+                if (l.a < at + di.fetch_rows && at < l.b)
+                    ch.after = std::max(ch.after, l.release);
+                else
+                    keep.push_back(l);
+            }
+            keep.push_back(Live{at, at + di.fetch_rows, ev_dep(t, d)});
+            stage_live.swap(keep);
+            for (WCopy c : di.fetch) {
+                c.smem += at;
+                ch.cps.push_back(c);
+                ch.tags.push_back(T + dep_tag0[t] + int32_t(d));
+            }
+            dr.src = di.stage_src >= 0 ? at + di.stage_src : -1;
+            dr.ysrc = di.stage_ysrc >= 0 ? at + di.stage_ysrc : -1;
+            w.fetched_rows += di.fetch_rows;
+            chunk_deps.push_back(w.dep.size());
+            w.dep.push_back(dr);
+        }
+        close_chunk();
+        w.step.push_back(rec);
+    }
+
+    // 5. independent verification: replay the consumer's events, issue ops at
+    //    their events and check that no shared-memory row is overwritten while
+    //    its content is still to be read, that every op is issued before it is
+    //    waited on, that every read finds the content it expects, and that
+    //    every fetch of produced data follows its producer.
+    {
+        const int32_t rows = XR + SR;
+        const int32_t n_tags = T + dep_tag0[T];
+        std::vector<int32_t> need(n_tags, -1);  // last event reading each content tag
+        for (int32_t t = 0; t < T; ++t) {
+            need[t] = std::max(need[t], ev_done(t));
+            for (int32_t d = 0; d < w.step[t].ndep; ++d) {
+                const int32_t p = steps[t].deps[d].producer;
+                const int32_t g = resident[t][d] ? p : T + dep_tag0[t] + d;
+                need[g] = std::max(need[g], ev_dep(t, d));
+            }
+        }
+        std::vector<int32_t> row_tag(rows, -1);
+        size_t next = 0;
+        auto issue_upto = [&](int32_t ev) {
+            while (next < w.op.size() && w.op[next].after <= ev) {
+                const WOp& o = w.op[next];
+                for (int32_t i = 0; i < o.ncopy; ++i) {
+                    const WCopy& c = w.copies[o.c0 + i];
+                    const int32_t a = c.smem, n = copy_rows(c), g = tag_of_copy[o.c0 + i];
+                    if (a < 0 || a + n > rows) throw Error(3, "walk copy outside shared memory");
+                    for (int32_t r = a; r < a + n; ++r) {
+                        if (row_tag[r] >= 0 && need[row_tag[r]] > ev)
+                            throw Error(3, "walk plan overwrites live shared memory (row " +
+                                               std::to_string(r) + ")");
+                        row_tag[r] = g;
+                    }
+                    if (g >= T) {  // a re-fetch of produced data: its producer must be done
+                        const int32_t p = tag_producer[g - T];
+                        if (p >= 0 && ev < ev_done(p))
+                            throw Error(3, "walk fetch issued before its producer finished");
+                    }
+                }
+                ++next;
+            }
+        };
+        auto expect = [&](int32_t row, int32_t g) {
+            if (row >= 0 && row_tag[row] != g) throw Error(3, "walk reads content that is not there");
+        };
+        issue_upto(-1);
+        int32_t waited = -1;
+        for (int32_t t = 0; t < T; ++t) {
+            const WStep& st = w.step[t];
+            if (size_t(st.op) >= next) throw Error(3, "walk waits on an unissued op");
+            waited = std::max(waited, st.op);
+            expect(st.ring, t);
+            for (int32_t d = 0; d < st.ndep; ++d) {
+                const WDep& dr = w.dep[st.dep0 + d];
+                if (dr.op >= 0) {
+                    if (size_t(dr.op) >= next) throw Error(3, "walk waits on an unissued fetch");
+                    waited = std::max(waited, dr.op);
+                }
+                const int32_t p = steps[t].deps[d].producer;
+                const int32_t g = resident[t][d] ? p : T + dep_tag0[t] + d;
+                expect(dr.src, g);
+                expect(dr.ysrc, g);
+                if (!resident[t][d] && op_of_tag[g - T] > waited)
+                    throw Error(3, "walk reads a fetch it never waited for");
+                issue_upto(ev_dep(t, d));
+            }
+            issue_upto(ev_done(t));
+        }
+        if (next != w.op.size()) throw Error(3, "walk ops left unissued");
+    }
+    return w;
+}
+
+// Serialise a verified walk into the word stream the kernels interpret:
+// prologue issues, then per step: STEP, (DEP, ISSUE*) per dependency, END,
+// ISSUE* -- each ISSUE placed right after the consumer event it waits for.
+void encode_stream(Walk& w, bool forward, const WalkConfig& cfg) {
+    std::vector<int32_t> st;
+    int32_t W = cfg.page_words;
+    // longest record decides the page size
+    int32_t longest = 4;
+    for (const WOp& o : w.op) longest = std::max(longest, 3 + 2 * o.ncopy);
+    for (const WStep& s : w.step) {
+        const int32_t dp = forward ? (s.len_dp >> 16) : 0;
+        longest = std::max(longest, 1 + dp);
+        for (int32_t d = 0; d < s.ndep; ++d)
+            longest = std::max(longest, 4 + (w.dep[s.dep0 + d].nrows + 1) / 2);
+    }
+    W = std::max(W, (longest + 1 + 3) / 4 * 4);
+    auto emit = [&](const std::vector<int32_t>& rec) {
+        const int32_t used = int32_t(st.size() % size_t(W));
+        if (used + int32_t(rec.size()) > W - 1) {
+            st.push_back(kRecPage);
+            while (st.size() % size_t(W)) st.push_back(0);
+        }
+        st.insert(st.end(), rec.begin(), rec.end());
+    };
+    size_t next = 0;
+    auto issue_upto = [&](int64_t ev) {
+        while (next < w.op.size() && w.op[next].after <= ev) {
+            const WOp& o = w.op[next];
+            std::vector<int32_t> rec{kRecIssue | (o.ncopy << 4), int32_t(next), o.bytes};
+            for (int32_t i = 0; i < o.ncopy; ++i) {
+                const WCopy& c = w.copies[o.c0 + i];
+                const int32_t tape = c.tape_rows & 0xff, rows = c.tape_rows >> 8;
+                if (rows >= 1024 || c.smem >= (1 << 20)) throw Error(3, "walk copy too large to encode");
+                rec.push_back(tape | (rows << 2) | (c.smem << 12));
+                rec.push_back(c.slot);
+            }
+            emit(rec);
+            ++next;
+        }
+    };
+    issue_upto(-1);
+    int64_t ev = 0;
+    for (const WStep& s : w.step) {
+        if (forward) {
+            const int32_t len = s.len_dp & 0xffff, dp = s.len_dp >> 16;
+            emit({kRecStep | (s.ndep << 4), s.ring | (len << 16), dp, s.lslot, s.brow, s.op});
+            for (int32_t d = 0; d < s.ndep; ++d) {
+                const WDep& e = w.dep[s.dep0 + d];
+                if (e.src >= 65536 || e.nrows >= 65536) throw Error(3, "walk dependency too large to encode");
+                std::vector<int32_t> rec{kRecDep | ((e.op + 1) << 4), e.kpos_fs,
+                                         e.nrows | (std::max(e.src, 0) << 16), e.ysrc};
+                for (int32_t r = 0; r < e.nrows; r += 2) {
+                    const int32_t lo = w.dst[e.u0 + r];
+                    const int32_t hi = r + 1 < e.nrows ? w.dst[e.u0 + r + 1] : 0;
+                    rec.push_back(lo | (hi << 16));
+                }
+                emit(rec);
+                issue_upto(ev++);
+            }
+            std::vector<int32_t> end{kRecEnd | (dp << 4)};
+            for (int32_t z = 0; z < dp; ++z) end.push_back(w.ut[s.ut0 + z]);
+            emit(end);
+            issue_upto(ev++);
+        } else {
+            emit({kRecStep | (s.ndep << 4), s.ring | (s.len_dp << 16), 0, s.lslot, s.brow, s.op});
+            for (int32_t d = 0; d < s.ndep; ++d) {
+                const WDep& e = w.dep[s.dep0 + d];
+                emit({kRecDep | ((e.op + 1) << 4), e.ysrc});
+                issue_upto(ev++);
+            }
+            emit({kRecEnd});
+            issue_upto(ev++);
+        }
+    }
+    if (next != w.op.size()) throw Error(3, "walk stream left ops unissued");
+    emit({kRecDone});
+    while (st.size() % size_t(W)) st.push_back(0);
+    w.stream = std::move(st);
+    w.page_words = W;
+    w.pages = cfg.pages;
+    w.n_pages = int32_t(w.stream.size() / size_t(W));
+}
+
+}  // namespace
+
+LuLayout build_lu_layout(const Symbolic& s) {
+    const int32_t nJ = s.nJ;
+    LuLayout lay;
+    lay.lslot.resize(nJ);
+    int32_t at = 0;
+    for (int32_t k = 0; k < nJ; ++k) {
+        lay.lslot[k] = at;
+        at += s.cp[k + 1] - s.dpos[k];
+    }
+    // U rows: entries (k descending) of row i
+    std::vector<int32_t> cnt(nJ, 0);
+    for (int32_t k = 0; k < nJ; ++k)
+        for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) cnt[s.ri[z]]++;
+    lay.ucrs0.assign(nJ + 1, 0);
+    lay.ucrs0[0] = at;
+    for (int32_t i = 0; i < nJ; ++i) lay.ucrs0[i + 1] = lay.ucrs0[i] + cnt[i];
+    if (lay.ucrs0[nJ] != s.nnzLU) throw Error(2, "LU layout does not cover the pattern");
+    lay.tape_of_ccs.assign(s.nnzLU, -1);
+    std::vector<int32_t> fill(nJ, 0);
+    for (int32_t k = nJ - 1; k >= 0; --k)  // descending k within each row
+        for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) {
+            const int32_t i = s.ri[z];
+            lay.tape_of_ccs[z] = lay.ucrs0[i] + fill[i]++;
+        }
+    for (int32_t k = 0; k < nJ; ++k)
+        for (int32_t z = s.dpos[k]; z < s.cp[k + 1]; ++z) lay.tape_of_ccs[z] = lay.lslot[k] + (z - s.dpos[k]);
+    return lay;
+}
+
+// Forward walk: column m of Alg. 2 (+ row m of the forward substitution).
+// Block of column m: its A rows (len) [+ the b row, replaced by y_m].
+// Dependencies, ascending k: the union of the U pattern of column m (LU
+// updates) and the L pattern of row m (FS terms).
+Walk build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg) {
+    const int32_t nJ = s.nJ;
+    std::vector<std::vector<int32_t>> lrow(nJ);  // k with L(m,k) != 0, ascending
+    if (with_fs)
+        for (int32_t k = 0; k < nJ; ++k)
+            for (int32_t z = s.dpos[k] + 1; z < s.cp[k + 1]; ++z) lrow[s.ri[z]].push_back(k);
+    std::vector<StepIn> steps(nJ);
+    std::vector<int32_t> posmap(nJ, -1);
+    std::vector<uint16_t> dst;
+    std::vector<int32_t> ut;
+    for (int32_t m = 0; m < nJ; ++m) {
+        const int32_t c0 = s.cp[m], len = s.cp[m + 1] - c0, dp = s.dpos[m] - c0;
+        StepIn& si = steps[m];
+        si.blk_rows = len + (with_fs ? 1 : 0);
+        si.copies.push_back(copy(kTapeA, c0, len, 0));
+        if (with_fs) si.copies.push_back(copy(kTapeB, m, 1, len));
+        si.rec.len_dp = len | (dp << 16);
+        si.rec.lslot = lay.lslot[m];
+        si.rec.ut0 = static_cast<int32_t>(ut.size());
+        si.rec.brow = m;
+        for (int32_t z = c0; z < s.dpos[m]; ++z) ut.push_back(lay.tape_of_ccs[z]);
+        for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = z - c0;
+        // merge U deps (rows < m of column m) with the L row of m
+        std::vector<int32_t> ks;
+        for (int32_t z = c0; z < s.dpos[m]; ++z) ks.push_back(s.ri[z]);
+        ks.insert(ks.end(), lrow[m].begin(), lrow[m].end());
+        std::sort(ks.begin(), ks.end());
+        ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+        for (int32_t k : ks) {
+            DepIn di;
+            di.producer = k;
+            const int32_t lk0 = s.dpos[k] + 1, nl = s.cp[k + 1] - lk0;  // L(:,k) rows
+            const int32_t kpos = posmap[k];
+            const bool upd = kpos >= 0 && kpos < dp;
+            int32_t fspos = 0xffff;
+            if (with_fs) {
+                const int32_t* b = s.ri.data() + lk0;
+                const int32_t* f = std::lower_bound(b, b + nl, m);
+                if (f != b + nl && *f == m) fspos = int32_t(f - b);
+            }
+            if (!upd && fspos == 0xffff) throw Error(2, "walk dependency without a role");
+            di.rec.kpos_fs = (upd ? kpos : 0xffff) | (fspos << 16);
+            di.rec.nrows = upd ? nl : 0;
+            di.rec.u0 = static_cast<int32_t>(dst.size());
+            if (upd)
+                for (int32_t zz = lk0; zz < lk0 + nl; ++zz) {
+                    const int32_t d = posmap[s.ri[zz]];
+                    if (d < 0) throw Error(2, "frozen LU pattern is not closed");
+                    dst.push_back(static_cast<uint16_t>(d));
+                }
+            const int32_t klen = s.cp[k + 1] - s.cp[k], kdp = s.dpos[k] - s.cp[k];
+            di.ring_src = kdp + 1;
+            di.ring_ysrc = with_fs ? klen : -1;
+            di.fetch.push_back(copy(kTapeLU, lay.lslot[k] + 1, nl, 0));
+            di.stage_src = 0;
+            di.fetch_rows = nl;
+            if (with_fs) {
+                di.fetch.push_back(copy(kTapeB, k, 1, nl));
+                di.stage_ysrc = nl;
+                di.fetch_rows = nl + 1;
+            }
+            if (nl == 0) {  // nothing below the diagonal: never a dependency
+                throw Error(2, "walk dependency on an empty L column");
+            }
+            si.deps.push_back(std::move(di));
+        }
+        for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = -1;
+    }
+    Walk w = plan(steps, cfg);
+    w.dst = std::move(dst);
+    w.ut = std::move(ut);
+    encode_stream(w, true, cfg);
+    return w;
+}
+
+// Backward walk: rows i = nJ-1 .. 0.  Block of row i: its U entries (CRS,
+// descending k), the y_i row (replaced by x_i) and the diagonal U(i,i).
+// Dependencies: x_k for every U(i,k), descending k.
+Walk build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg) {
+    const int32_t nJ = s.nJ;
+    std::vector<std::vector<int32_t>> urow(nJ);  // k descending
+    for (int32_t k = nJ - 1; k >= 0; --k)
+        for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) urow[s.ri[z]].push_back(k);
+    std::vector<StepIn> steps(nJ);
+    for (int32_t t = 0; t < nJ; ++t) {
+        const int32_t i = nJ - 1 - t;
+        const int32_t ne = static_cast<int32_t>(urow[i].size());
+        StepIn& si = steps[t];
+        si.blk_rows = ne + 2;
+        if (ne > 0) si.copies.push_back(copy(kTapeLU, lay.ucrs0[i], ne, 0));
+        si.copies.push_back(copy(kTapeB, i, 1, ne));
+        si.copies.push_back(copy(kTapeLU, lay.lslot[i], 1, ne + 1));
+        si.rec.len_dp = ne;
+        si.rec.lslot = lay.lslot[i];
+        si.rec.brow = i;
+        for (int32_t k : urow[i]) {
+            DepIn di;
+            di.producer = nJ - 1 - k;
+            const int32_t kne = static_cast<int32_t>(urow[k].size());
+            di.ring_ysrc = kne;
+            di.fetch.push_back(copy(kTapeB, k, 1, 0));
+            di.stage_ysrc = 0;
+            di.fetch_rows = 1;
+            si.deps.push_back(std::move(di));
+        }
+    }
+    Walk w = plan(steps, cfg);
+    encode_stream(w, false, cfg);
+    return w;
+}
+
+}  // namespace gbnr

@@ -1,0 +1,126 @@
+// walk.hpp -- tile-owned sequential walks over the frozen LU (host plans).
+//
+// The level-scheduled refactorization of PAPER.md Alg. 3 / SPEC.md:319-327
+// launches once per level and reads every L(:,k) from HBM once per dependent
+// column.  On B200 the batch is only ~313 tiles of 32 scenarios, so instead
+// each tile is walked by ONE warp through all columns in elimination order
+// (a topological order of the column DAG, so Alg. 2's per-element operation
+// order is unchanged and results stay bit-identical):
+//
+//   * forward walk  = refactorize_batch fused with the
+//                     forward substitution of fs_bs_batch:
+//                     at column m the dependencies k ascending are exactly
+//                     the columns whose L(:,k) holds L(m,k) (structurally
+//                     symmetric J), so y_m = b_m - sum_k L(m,k) y_k rides along;
+//   * backward walk = the backward substitution, rows in reverse order over a
+//                     row-major copy of U written by the forward walk.
+//
+// Shared memory holds a ring of recently produced column blocks and a staging
+// ring; all global->shared movement is cp.async.bulk (TMA) into mbarrier-
+// tracked slots.  The plan below is the complete, static program of those
+// copies: which step's data lives where in shared memory, which dependency is
+// still resident in the ring (most are: AMD puts a column's dependencies just
+// before it) and which must be re-fetched, and after which consumer event each
+// copy may be issued.  It is computed once per plan on the host, shared by all
+// tiles, and verified by a host simulation before it is ever launched.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "symbolic.hpp"
+
+namespace gbnr {
+
+enum : int32_t { kTapeA = 0, kTapeLU = 1, kTapeB = 2 };
+
+// One step (LU column / BS row).  32 B, two uniform int4 loads.
+struct WStep {
+    int32_t ring;    // smem row of the step's block
+    int32_t len_dp;  // forward: len | dp << 16; backward: number of U entries
+    int32_t dep0;    // first WDep
+    int32_t ndep;    // number of WDep
+    int32_t lslot;   // LU-tape slot of the diagonal (L+diag region, len-dp rows)
+    int32_t ut0;     // forward: first index into the U-scatter list (dp entries)
+    int32_t op;      // op carrying the block
+    int32_t brow;    // b-tape row of the step (LU row / column index)
+};
+// One dependency of a step.  32 B.
+struct WDep {
+    int32_t kpos_fs;  // forward: kpos | fspos << 16 (0xffff = none)
+    int32_t nrows;    // forward: rows of L(:,k) applied (0 = FS-only)
+    int32_t src;      // smem row of L(:,k) (forward) / of nothing (backward)
+    int32_t ysrc;     // smem row of y_k (forward) / x_k (backward)
+    int32_t u0;       // forward: first destination record
+    int32_t op;       // op to wait on, -1 = resident in the ring
+    int32_t pad0, pad1;
+};
+// One TMA bulk copy: nrows 256 B rows of tape `tape` from slot/row `slot`.
+struct WCopy {
+    int32_t tape_rows;  // tape | nrows << 8
+    int32_t slot;
+    int32_t smem;       // destination smem row
+    int32_t pad;
+};
+struct WOp {
+    int32_t after;  // issue once the consumer has passed this event (-1 = prologue)
+    int32_t ncopy;
+    int32_t bytes;  // expect_tx total
+    int32_t c0;     // first copy in Walk::copies
+};
+
+struct WalkConfig {
+    int32_t ring_rows = 176;    // XR
+    int32_t stage_rows = 80;    // SR (grown to the largest single fetch if needed)
+    int32_t barriers = 32;      // mbarriers (op i uses barrier i % 32)
+    int32_t prefetch = 8;       // steps an op may run ahead of its consumer
+    int32_t headroom = 2;       // ring residency margin (steps) before an overwrite
+    int32_t page_words = 512;   // program-stream page (grown to the longest record)
+    int32_t pages = 4;          // program-stream pages resident in shared memory
+};
+
+// The device program of a walk: one int32 word stream the warp interprets in
+// order, streamed through shared memory in pages by TMA.  Records (word 0 low
+// 4 bits = type) never straddle a page; kRecPage moves to the next page.
+enum : int32_t {
+    kRecIssue = 1,  // 1 | ncopy << 4, op, bytes, {tape | rows << 2 | smem << 12, slot} x ncopy
+    kRecStep = 2,   // 2 | ndep << 4, ring | len << 16 (fwd) / ring | ne << 16 (bwd), dp, lslot, brow, op
+    kRecDep = 3,    // fwd: 3 | (op + 1) << 4, kpos_fs, nrows | src << 16, ysrc, dst u16 pairs
+                    // bwd: 3 | (op + 1) << 4, ysrc
+    kRecEnd = 4,    // 4 | dp << 4, U-CRS tape slots [dp] (fwd)
+    kRecPage = 5,
+    kRecDone = 6,
+};
+
+struct Walk {
+    int32_t ring_rows = 0, stage_rows = 0, barriers = 0, n_steps = 0;
+    std::vector<WStep> step;
+    std::vector<WDep> dep;
+    std::vector<uint16_t> dst;  // forward: destination position per applied L row
+    std::vector<WOp> op;
+    std::vector<WCopy> copies;
+    std::vector<int32_t> ut;    // forward: U-part CCS slot -> U-CRS tape slot (by step)
+    int64_t events = 0, ring_dep_rows = 0, fetched_rows = 0, block_rows = 0;
+    // device program (encode_stream)
+    std::vector<int32_t> stream;
+    int32_t page_words = 0, pages = 0, n_pages = 0;
+    size_t smem_bytes() const {
+        return size_t(ring_rows + stage_rows) * 256 + size_t(pages) * page_words * 4 +
+               size_t(barriers + pages) * 8;
+    }
+};
+
+// LU tape layout of the walks: the L+diag part of every column contiguous
+// (column-major, diagonal first) followed by U row-major (each row's entries in
+// descending column order, the backward walk's consumption order).
+struct LuLayout {
+    std::vector<int32_t> lslot;        // [nJ] slot of the diagonal of column k
+    std::vector<int32_t> ucrs0;        // [nJ+1] first U-CRS slot of row i
+    std::vector<int32_t> tape_of_ccs;  // [nnzLU] CCS slot -> tape slot
+};
+
+LuLayout build_lu_layout(const Symbolic& s);
+Walk build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg);
+Walk build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg);
+
+}  // namespace gbnr

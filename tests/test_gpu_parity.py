@@ -117,14 +117,15 @@ def test_repeat_solve_is_deterministic():
     np.testing.assert_array_equal(a.iterations, b.iterations)
 
 
-@pytest.mark.parametrize("bulk_min,fs_warps", [(1, 16), (8, 8), (100000, 32)])
-def test_schedule_split_invariance(bulk_min, fs_warps):
+@pytest.mark.parametrize("opts", [dict(ring_rows=40, stage_rows=24, prefetch=3),
+                                  dict(ring_rows=64, stage_rows=40, prefetch=1, headroom=1),
+                                  dict(ring_rows=384, stage_rows=128, prefetch=16, headroom=4)])
+def test_walk_plan_invariance(opts):
     """execute_schedule == refactorize_batch bitwise for any execution plan:
-    moving columns between the level launches and the sync-free tail, and changing
-    the FS-BS warp count, never changes a bit."""
+    shrinking / growing the shared-memory rings moves dependencies between ring
+    residency and TMA re-fetches and changes every copy's issue point, never a bit."""
     gc, plan, oplan, vm0, va0 = _setup("synth300")
     ip, ix, _, yr, yi = S.build_ybus(gc)
-    plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0,
-                     bulk_min=bulk_min, fs_warps=fs_warps)
+    plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, **opts)
     p0, q0 = montecarlo(gc, 100)
     _compare(plan2.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))

@@ -1,0 +1,271 @@
+"""Host replay of the tile-walk copy programs (walk.hpp) -- CPU only.
+
+The LU+FS and BS walks are driven by a static program of TMA copies planned on
+the host (which step's block lives where in shared memory, which dependency is
+still resident, which must be re-fetched, and after which consumer event each
+copy may be issued).  This test replays that program exactly as the kernels do
+-- copies take effect when issued, the warp consumes in order -- on a 32-lane
+tile, with numpy standing in for shared memory and the tapes.  A copy issued
+too early (before its producer wrote the data) or a ring row overwritten while
+still needed shows up as a wrong factor, so the result is compared BITWISE with
+a plain sequential Alg. 2 / FS / BS over the same numbers (both sides use the
+same unfused arithmetic here; the GPU's fused arithmetic is checked against the
+oracle by the -m gpu parity tests).
+"""
+import numpy as np
+import pytest
+
+import util
+from paper_2101_02270_b200 import solver as S
+from paper_2101_02270_b200.case import load_case
+from newtonpf_scipy import dsbus_dv, ybus_matrix
+
+TAPE_A, TAPE_LU, TAPE_B = 0, 1, 2
+
+
+def jacobian_tape(gc, plan, lanes=32, seed=0):
+    """A values (LU CCS slot order) of `lanes` tasks at perturbed voltages."""
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    Y = ybus_matrix(ip, ix, yr, yi, gc.n_bus)
+    ex = plan.export()
+    cp, ri = ex["col_ptr"], ex["row_ix"]
+    nJ = len(ex["row_fwd"])
+    pos = {}
+    for j in range(nJ):
+        for s in range(cp[j], cp[j + 1]):
+            pos[(ri[s], j)] = s
+    vm0, va0 = gc.v_start()
+    rng = np.random.default_rng(seed)
+    pvpq = np.r_[gc.pv, gc.pq]
+    A = np.zeros((cp[-1], lanes))
+    for t in range(lanes):
+        V = vm0 * (1 + 0.01 * rng.standard_normal(gc.n_bus)) * np.exp(1j * (va0 + 0.02 * rng.standard_normal(gc.n_bus)))
+        dVm, dVa = dsbus_dv(Y, V)
+        J = np.block([[dVa[np.ix_(pvpq, pvpq)].real.toarray(), dVm[np.ix_(pvpq, gc.pq)].real.toarray()],
+                      [dVa[np.ix_(gc.pq, pvpq)].imag.toarray(), dVm[np.ix_(gc.pq, gc.pq)].imag.toarray()]])
+        rr, cc = np.nonzero(J)
+        for a, b in zip(rr, cc):
+            A[pos[(ex["row_fwd"][a], ex["col_fwd"][b])], t] = J[a, b]
+    b = rng.standard_normal((nJ, lanes))
+    return ex, A, b
+
+
+def sequential(ex, A, b):
+    """Alg. 2 + push FS + push BS, CCS storage (the oracle's operation order)."""
+    cp, ri = ex["col_ptr"], ex["row_ix"]
+    nJ = len(cp) - 1
+    lu = A.copy()
+    dpos = np.zeros(nJ, np.int64)
+    for k in range(nJ):
+        rows = ri[cp[k]:cp[k + 1]]
+        dpos[k] = cp[k] + int(np.searchsorted(rows, k))
+        posm = {r: z for z, r in enumerate(rows)}
+        x = lu[cp[k]:cp[k + 1]]
+        for z in range(dpos[k] - cp[k]):
+            j = rows[z]
+            xj = x[z].copy()
+            for zz in range(dpos[j] + 1, cp[j + 1]):
+                d = posm[ri[zz]]
+                x[d] = x[d] - xj * lu[zz]
+        dp = dpos[k] - cp[k]
+        inv = 1.0 / x[dp]
+        x[dp + 1:] = x[dp + 1:] * inv
+    y = b.copy()
+    for k in range(nJ):
+        for z in range(dpos[k] + 1, cp[k + 1]):
+            y[ri[z]] = y[ri[z]] - lu[z] * y[k]
+    x = y.copy()
+    for k in range(nJ - 1, -1, -1):
+        x[k] = x[k] / lu[dpos[k]]
+        for z in range(cp[k], dpos[k]):
+            x[ri[z]] = x[ri[z]] - lu[z] * x[k]
+    return lu, y, x
+
+
+REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE = 1, 2, 3, 4, 5, 6
+
+
+class Machine:
+    """The kernels' view of a walk: paged program words, smem rows, op barriers."""
+
+    def __init__(self, w, tapes):
+        info = w["info"]
+        self.tapes = tapes
+        self.R = np.full((info["ring_rows"] + info["stage_rows"], 32), np.nan)
+        self.W, self.NP, self.NB = info["page_words"], info["pages"], info["barriers"]
+        self.gs = w["stream"].astype(np.int64)
+        self.n_pages = info["n_pages"]
+        assert len(self.gs) == self.n_pages * self.W
+        self.pages = np.zeros((self.NP, self.W), np.int64)
+        for p in range(min(self.NP, self.n_pages)):
+            self.pages[p] = self.gs[p * self.W:(p + 1) * self.W]
+        self.page, self.off = 0, 0
+        self.issued = set()
+        self.n_issued = 0
+
+    def rec(self):
+        return self.pages[self.page % self.NP, self.off:]
+
+    def next_page(self):
+        if self.page + self.NP < self.n_pages:
+            q = self.page + self.NP
+            self.pages[self.page % self.NP] = self.gs[q * self.W:(q + 1) * self.W]
+        self.page += 1
+        self.off = 0
+
+    def issue(self, r):
+        ncopy = (int(r[0]) >> 4) & 0xFFF
+        op = int(r[1])
+        assert op == self.n_issued, "ops must be issued in order"
+        nbytes = 0
+        for i in range(ncopy):
+            c, slot = int(r[3 + 2 * i]), int(r[4 + 2 * i])
+            tape, rows, smem = c & 3, (c >> 2) & 1023, c >> 12
+            self.R[smem:smem + rows] = self.tapes[tape][slot:slot + rows]
+            nbytes += rows * 256
+        assert nbytes == r[2]
+        self.issued.add(op)
+        self.n_issued += 1
+        return 3 + 2 * ncopy
+
+    def wait(self, op):
+        assert op in self.issued, f"waits on unissued op {op}"
+        # the barrier of op may be re-armed only after this wait
+        assert self.n_issued <= op + self.NB, "barrier re-armed before its wait"
+
+
+def replay_forward(w, A, b_tape, nnz, fs=True):
+    LU = np.full((nnz, 32), np.nan)
+    M = Machine(w, {TAPE_A: A, TAPE_LU: LU, TAPE_B: b_tape})
+    assert w["info"]["barriers"] == 32 and w["info"]["pages"] == 4
+    R = M.R
+    x = acc = None
+    ln = dp = lslot = brow = 0
+    while True:
+        r = M.rec()
+        h = int(r[0])
+        t = h & 15
+        if t == REC_ISSUE:
+            M.off += M.issue(r)
+        elif t == REC_DEP:
+            op = (h >> 4) - 1
+            kpos_fs, nrows, src, ysrc = int(r[1]), int(r[2]) & 0xFFFF, (int(r[2]) >> 16) & 0xFFFF, int(r[3])
+            if op >= 0:
+                M.wait(op)
+            if nrows > 0:
+                mult = x[kpos_fs & 0xFFFF].copy()
+                for q in range(nrows):
+                    wq = int(r[4 + q // 2])
+                    d = (wq >> 16) & 0xFFFF if q & 1 else wq & 0xFFFF
+                    x[d] = x[d] - mult * R[src + q]
+            fsp = (kpos_fs >> 16) & 0xFFFF
+            if fs and fsp != 0xFFFF:
+                acc = acc - R[src + fsp] * R[ysrc]
+            M.off += 4 + (nrows + 1) // 2
+        elif t == REC_STEP:
+            ring, ln = int(r[1]) & 0xFFFF, int(r[1]) >> 16
+            dp, lslot, brow, op = int(r[2]), int(r[3]), int(r[4]), int(r[5])
+            M.off += 6
+            M.wait(op)
+            x = R[ring:ring + ln]
+            acc = R[ring + ln].copy() if fs else None
+        elif t == REC_END:
+            piv = x[dp].copy()
+            inv = 1.0 / piv
+            LU[lslot] = piv
+            for z in range(dp + 1, ln):
+                x[z] = x[z] * inv
+                LU[lslot + z - dp] = x[z]
+            for z in range(dp):
+                LU[int(r[1 + z])] = x[z]
+            if fs:
+                R[ring + ln] = acc
+                b_tape[brow] = acc
+            M.off += 1 + dp
+        elif t == REC_PAGE:
+            M.next_page()
+        else:
+            assert t == REC_DONE
+            break
+    assert M.n_issued == w["info"]["n_ops"]
+    return LU
+
+
+def replay_backward(w, LU, b_tape):
+    M = Machine(w, {TAPE_A: None, TAPE_LU: LU, TAPE_B: b_tape})
+    R = M.R
+    blk = acc = None
+    ne = e = brow = ring = 0
+    while True:
+        r = M.rec()
+        h = int(r[0])
+        t = h & 15
+        if t == REC_ISSUE:
+            M.off += M.issue(r)
+        elif t == REC_DEP:
+            op = (h >> 4) - 1
+            if op >= 0:
+                M.wait(op)
+            acc = acc - R[ring + e] * R[int(r[1])]
+            e += 1
+            M.off += 2
+        elif t == REC_STEP:
+            ring, ne = int(r[1]) & 0xFFFF, int(r[1]) >> 16
+            brow, op = int(r[4]), int(r[5])
+            M.off += 6
+            M.wait(op)
+            acc = R[ring + ne].copy()
+            e = 0
+        elif t == REC_END:
+            xi = acc / R[ring + ne + 1]
+            R[ring + ne] = xi
+            b_tape[brow] = xi
+            M.off += 1
+        elif t == REC_PAGE:
+            M.next_page()
+        else:
+            assert t == REC_DONE
+            break
+    assert M.n_issued == w["info"]["n_ops"]
+
+
+@pytest.mark.parametrize("name,opts", [("case14", {}), ("synth118", {}), ("synth300", {}),
+                                       ("synth300", dict(ring_rows=40, stage_rows=24, prefetch=3)),
+                                       ("synth300", dict(ring_rows=400, stage_rows=200, prefetch=20)),
+                                       ("synth2383", dict(ring_rows=64, stage_rows=40, prefetch=5,
+                                                          headroom=1))])
+def test_walk_replay_bitwise(name, opts):
+    gc = load_case(util.case_path(name))
+    plan = S.NrPlan.from_case(gc, device=-1, **opts)
+    ex, A, b = jacobian_tape(gc, plan)
+    lu_ref, y_ref, x_ref = sequential(ex, A, b)
+    wf, wl, wb = plan.walk_export(0), plan.walk_export(1), plan.walk_export(2)
+    toc = wf["tape_of_ccs"]
+    nnz = len(toc)
+    b_tape = b.copy()
+    LU = replay_forward(wf, A, b_tape, nnz, fs=True)
+    np.testing.assert_array_equal(LU[toc], lu_ref)
+    np.testing.assert_array_equal(b_tape, y_ref)
+    replay_backward(wb, LU, b_tape)
+    np.testing.assert_array_equal(b_tape, x_ref)
+    LU2 = replay_forward(wl, A, b.copy(), nnz, fs=False)
+    np.testing.assert_array_equal(LU2[toc], lu_ref)
+    plan.close()
+
+
+def test_walk_stats_and_layout():
+    gc = load_case(util.case_path("synth300"))
+    plan = S.NrPlan.from_case(gc, device=-1)
+    st = plan.stats()
+    for which in (0, 1, 2):
+        info = plan.walk_info(which)
+        assert info["n_steps"] == st["nJ"]
+        assert info["smem_bytes"] + 1024 <= 228 * 1024 // 3  # three tile walkers per SM
+    w = plan.walk_export(0)
+    toc = w["tape_of_ccs"]
+    assert sorted(toc.tolist()) == list(range(st["nnzLU"]))  # a permutation of the slots
+    # LU-only walk fetches no right-hand side rows
+    wl = plan.walk_export(1)
+    assert not ((wl["copies"]["tape_rows"] & 0xFF) == TAPE_B).any()
+    assert wl["op"]["ncopy"].sum() == len(wl["copies"])
+    plan.close()
