@@ -65,12 +65,13 @@ typedef struct gbnr_options {
     double pivot_tol;      /* threshold partial pivoting (default 1e-3) */
     double singular_tol;   /* refactor pivot flag, relative (default 1e-14)          */
     int32_t device;        /* CUDA ordinal; -1 = host-only plan (symbolic only)      */
-    int32_t ring_rows;     /* tile-walk ring of step blocks, 256 B rows (0 = 176)  */
+    int32_t ring_rows;     /* per-walker ring of step blocks, 256 B rows (0 = auto) */
     int32_t profile;       /* 1 = record per-phase CUDA-event timings               */
-    int32_t stage_rows;    /* tile-walk staging ring rows (0 = 80)                 */
+    int32_t stage_rows;    /* per-walker staging ring rows (0 = auto)              */
     int32_t prefetch;      /* steps a walk copy may run ahead (0 = 8)              */
     int32_t headroom;      /* ring residency margin in steps (0 = 2)               */
-    int32_t reserved[2];
+    int32_t walkers;       /* warps per tile walking disjoint subtrees (0 = 4, <= 8) */
+    int32_t reserved;
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);
@@ -139,14 +140,15 @@ int gbnr_last_timing(const gbnr_plan* plan, double* out);
 
 /* Tile-walk execution plans (the static TMA copy programs of the LU+FS, LU-only
  * and BS walks).  which: 0 forward LU+FS, 1 LU only, 2 backward.
- * out[17]: n_steps, n_deps, n_dst, n_ops, n_ut, ring_rows, stage_rows, barriers,
- * events, ring-resident dependency rows, fetched rows, shared-memory bytes,
- * program words, page words, resident pages, program pages, n_copies. */
+ * out[16]: steps, walkers, phases, smem rows, page words, pages per walker,
+ * barriers per walker, program words, events, ring-resident dependency rows,
+ * fetched rows, ops, copies, shared-memory bytes per CTA, first walker's ring
+ * rows and staging rows. */
 int gbnr_walk_info(const gbnr_plan* plan, int32_t which, int64_t* out);
-/* Raw plan arrays for host-side replay (tests): part 0 steps (32 B each), 1 deps
- * (32 B), 2 dst (uint16), 3 ops (16 B), 4 ut (int32), 5 tape_of_ccs (int32
- * [nnzLU]), 6 lslot (int32 [nJ]), 7 ucrs0 (int32 [nJ+1]), 8 program words (int32),
- * 9 copies (16 B). */
+/* Raw walk arrays for host-side replay (tests): part 0 program words (int32,
+ * walker-major pages), 1 first page per walker (int32 [walkers+1]), 2 owner
+ * (int32 [nJ]: phase-0 walker of each column, -1 = top), 3 tape_of_ccs (int32
+ * [nnzLU]), 4 lslot (int32 [nJ]), 5 ucrs0 (int32 [nJ+1]). */
 int gbnr_walk_export(const gbnr_plan* plan, int32_t which, int32_t part, void* dst);
 
 /* LU-only microbenchmark / parity: the Jacobian at the staged

@@ -260,15 +260,21 @@ struct Prog {
     int W, n_pages, page;
 };
 
-__device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, Prog& P, int tile, int lane) {
+// Shared memory of a walk CTA: [rows][32] doubles shared by the walkers (each
+// phase's plan gives every walker a disjoint share), then per walker its
+// program pages and its op / page mbarriers.
+__device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, Prog& P, int tile, int warp,
+                                           int lane) {
     extern __shared__ __align__(128) unsigned char walk_smem[];
     P.R = reinterpret_cast<double*>(walk_smem);
-    P.pg = reinterpret_cast<int32_t*>(walk_smem + size_t(w.ring_rows + w.stage_rows) * kTile * 8);
-    P.bar = reinterpret_cast<unsigned long long*>(P.pg + size_t(kWalkPages) * w.page_words);
+    unsigned char* mine = walk_smem + size_t(w.rows) * kTile * 8 +
+                          size_t(warp) * (size_t(kWalkPages) * w.page_words * 4 + (kWalkBars + kWalkPages) * 8);
+    P.pg = reinterpret_cast<int32_t*>(mine);
+    P.bar = reinterpret_cast<unsigned long long*>(mine + size_t(kWalkPages) * w.page_words * 4);
     P.pbar = P.bar + kWalkBars;
-    P.gs = w.stream;
     P.W = w.page_words;
-    P.n_pages = w.n_pages;
+    P.gs = w.stream + size_t(w.wpage0[warp]) * P.W;
+    P.n_pages = w.wpage0[warp + 1] - w.wpage0[warp];
     P.page = 0;
     P.cur = P.pg;
     P.tape[kTapeA] = reinterpret_cast<const char*>(v.A + size_t(tile) * v.nnzLU * kTile);
@@ -305,20 +311,20 @@ __device__ __forceinline__ void prog_next_page(Prog& P, int lane) {
 __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32_t* r, int lane) {
     const int ncopy = (r[0] >> 4) & 0xfff;
     if (!(v.dbg & 2)) fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
+    unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
     __syncwarp();
-    if (lane == 0) {
-        unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
-        mbar_expect_tx(bar, unsigned(r[2]));
-        const unsigned rbase = smem_u32(P.R);
-        for (int i = 0; i < ncopy; ++i) {
-            const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
-            const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                    rbase + smem * (kTile * 8u)),
-                "l"(P.tape[c & 3] + size_t(slot) * (kTile * 8)), "r"(rows * (kTile * 8u)), "r"(smem_u32(bar))
-                : "memory");
-        }
+    if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]));
+    __syncwarp();
+    // one copy per lane (the barrier's tx-count may dip below zero meanwhile)
+    const unsigned rbase = smem_u32(P.R), ubar = smem_u32(bar);
+    for (int i = lane; i < ncopy; i += 32) {
+        const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
+        const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                rbase + smem * (kTile * 8u)),
+            "l"(P.tape[c & 3] + size_t(slot) * (kTile * 8)), "r"(rows * (kTile * 8u)), "r"(ubar)
+            : "memory");
     }
     return 3 + 2 * ncopy;
 }
@@ -329,11 +335,11 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
 template <bool FS>
-__global__ void __launch_bounds__(32) lu_walk_kernel(DevView v, WalkView w) {
-    const int tile = blockIdx.x, lane = threadIdx.x;
+__global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
+    const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
-    prog_begin(v, w, P, tile, lane);
+    prog_begin(v, w, P, tile, warp, lane);
     double* lu_t = v.LU + size_t(tile) * v.nnzLU * kTile + lane;
     double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
     const double stol = v.singular_tol;
@@ -373,9 +379,19 @@ __global__ void __launch_bounds__(32) lu_walk_kernel(DevView v, WalkView w) {
                     x[d2 * kTile] = a2;
                     x[d3 * kTile] = a3;
                 }
-                for (; q < nrows; ++q) {
-                    const int32_t wq = dw[q >> 1];
-                    const int d0 = (q & 1) ? int(unsigned(wq) >> 16) : (wq & 0xffff);
+                if (q + 2 <= nrows) {  // q even here: one packed pair
+                    const int32_t w0 = dw[q >> 1];
+                    const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
+                    const double l0 = src[q * kTile], l1 = src[(q + 1) * kTile];
+                    double a0 = x[d0 * kTile], a1 = x[d1 * kTile];
+                    a0 = fma(-mult, l0, a0);
+                    a1 = fma(-mult, l1, a1);
+                    x[d0 * kTile] = a0;
+                    x[d1 * kTile] = a1;
+                    q += 2;
+                }
+                if (q < nrows) {
+                    const int d0 = dw[q >> 1] & 0xffff;
                     x[d0 * kTile] = fma(-mult, src[q * kTile], x[d0 * kTile]);
                 }
             }
@@ -398,18 +414,45 @@ __global__ void __launch_bounds__(32) lu_walk_kernel(DevView v, WalkView w) {
         } else if (type == kRecEnd) {
             // pivot check and normalization L = x * (1 / pivot)
             const double piv = x[dp * kTile];
-            double cmax = 0.0;
-            for (int z = 0; z < len; ++z) cmax = fmax(cmax, fabs(x[z * kTile]));
+            // max |x| is exact in any order: four independent chains
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+            int z = 0;
+            for (; z + 4 <= len; z += 4) {
+                c0 = fmax(c0, fabs(x[z * kTile]));
+                c1 = fmax(c1, fabs(x[(z + 1) * kTile]));
+                c2 = fmax(c2, fabs(x[(z + 2) * kTile]));
+                c3 = fmax(c3, fabs(x[(z + 3) * kTile]));
+            }
+            for (; z < len; ++z) c0 = fmax(c0, fabs(x[z * kTile]));
+            const double cmax = fmax(fmax(c0, c1), fmax(c2, c3));
             flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
             const double inv = 1.0 / piv;
             double* lcol = lu_t + size_t(lslot) * kTile;  // diagonal, then L rows
             lcol[0] = piv;
-            for (int z = dp + 1; z < len; ++z) {
-                const double lv = x[z * kTile] * inv;
-                x[z * kTile] = lv;
-                lcol[size_t(z - dp) * kTile] = lv;
+            z = dp + 1;
+            for (; z + 2 <= len; z += 2) {
+                const double l0 = x[z * kTile] * inv, l1 = x[(z + 1) * kTile] * inv;
+                x[z * kTile] = l0;
+                x[(z + 1) * kTile] = l1;
+                lcol[size_t(z - dp) * kTile] = l0;
+                lcol[size_t(z + 1 - dp) * kTile] = l1;
             }
-            for (int z = 0; z < dp; ++z) lu_t[size_t(r[1 + z]) * kTile] = x[z * kTile];
+            if (z < len) {
+                const double l0 = x[z * kTile] * inv;
+                x[z * kTile] = l0;
+                lcol[size_t(z - dp) * kTile] = l0;
+            }
+            z = 0;
+            for (; z + 4 <= dp; z += 4) {  // U part -> its row-major slots
+                const int32_t s0 = r[1 + z], s1 = r[2 + z], s2 = r[3 + z], s3 = r[4 + z];
+                const double u0 = x[z * kTile], u1 = x[(z + 1) * kTile], u2 = x[(z + 2) * kTile],
+                             u3 = x[(z + 3) * kTile];
+                lu_t[size_t(s0) * kTile] = u0;
+                lu_t[size_t(s1) * kTile] = u1;
+                lu_t[size_t(s2) * kTile] = u2;
+                lu_t[size_t(s3) * kTile] = u3;
+            }
+            for (; z < dp; ++z) lu_t[size_t(r[1 + z]) * kTile] = x[z * kTile];
             if (FS) {
                 x[len * kTile] = acc_y;
                 b_t[size_t(brow) * kTile] = acc_y;
@@ -418,6 +461,9 @@ __global__ void __launch_bounds__(32) lu_walk_kernel(DevView v, WalkView w) {
             P.cur += 1 + dp;
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
+        } else if (type == kRecSync) {
+            __syncthreads();  // phase boundary: every walker's columns are written and fenced
+            P.cur += 1;
         } else {
             break;
         }
@@ -426,11 +472,11 @@ __global__ void __launch_bounds__(32) lu_walk_kernel(DevView v, WalkView w) {
 }
 
 // Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
-__global__ void __launch_bounds__(32) bs_walk_kernel(DevView v, WalkView w) {
-    const int tile = blockIdx.x, lane = threadIdx.x;
+__global__ void __launch_bounds__(256) bs_walk_kernel(DevView v, WalkView w) {
+    const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
-    prog_begin(v, w, P, tile, lane);
+    prog_begin(v, w, P, tile, warp, lane);
     double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
     double* blk = P.R;
     int ne = 0, e = 0, brow = 0;
@@ -466,6 +512,9 @@ __global__ void __launch_bounds__(32) bs_walk_kernel(DevView v, WalkView w) {
             P.cur += 1;
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
+        } else if (type == kRecSync) {
+            __syncthreads();  // phase boundary: every walker's columns are written and fenced
+            P.cur += 1;
         } else {
             break;
         }
@@ -518,8 +567,8 @@ unsigned n_super(const DevView& v) { return unsigned((v.n_tiles + kSuper - 1) / 
 }  // namespace
 
 size_t walk_smem_bytes(const WalkView& w) {
-    return size_t(w.ring_rows + w.stage_rows) * kTile * 8 + size_t(kWalkPages) * w.page_words * 4 +
-           size_t(kWalkBars + kWalkPages) * 8;
+    return size_t(w.rows) * kTile * 8 +
+           size_t(w.walkers) * (size_t(kWalkPages) * w.page_words * 4 + size_t(kWalkBars + kWalkPages) * 8);
 }
 
 void configure_kernels() {
@@ -548,14 +597,15 @@ void launch_jacobian(const DevView& v, cudaStream_t st) {
 
 void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {
     const size_t smem = walk_smem_bytes(w);
+    const unsigned threads = unsigned(kTile * w.walkers);
     if (fs)
-        lu_walk_kernel<true><<<unsigned(v.n_tiles), kTile, smem, st>>>(v, w);
+        lu_walk_kernel<true><<<unsigned(v.n_tiles), threads, smem, st>>>(v, w);
     else
-        lu_walk_kernel<false><<<unsigned(v.n_tiles), kTile, smem, st>>>(v, w);
+        lu_walk_kernel<false><<<unsigned(v.n_tiles), threads, smem, st>>>(v, w);
 }
 
 void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st) {
-    bs_walk_kernel<<<unsigned(v.n_tiles), kTile, walk_smem_bytes(w), st>>>(v, w);
+    bs_walk_kernel<<<unsigned(v.n_tiles), unsigned(kTile * w.walkers), walk_smem_bytes(w), st>>>(v, w);
 }
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {

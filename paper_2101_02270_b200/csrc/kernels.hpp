@@ -44,8 +44,9 @@ struct DevView {
 
 // Device copy of a Walk (walk.hpp).
 struct WalkView {
-    const int32_t* stream;  // program words (walk.hpp kRec*)
-    int32_t n_pages, page_words, pages, ring_rows, stage_rows, barriers;
+    const int32_t* stream;  // program words (walk.hpp kRec*), walker-major pages
+    int32_t walkers, page_words, rows;
+    int32_t wpage0[9];      // first page of each walker's program
 };
 
 size_t walk_smem_bytes(const WalkView& w);

@@ -67,7 +67,7 @@ enum Phase { kNpm = 0, kJac, kLu, kFsbs, kVupd, kPhases };
 struct gbnr_plan {
     gbnr::Symbolic sym;
     gbnr::LuLayout lay;
-    gbnr::Walk wf, wl, wb;           // forward LU+FS, LU-only, backward walks
+    gbnr::WalkSet wf, wl, wb;        // forward LU+FS, LU-only, backward walks
     gbnr::WalkView vf{}, vl{}, vb{};
     gbnr_options opt{};
     bool on_device = false;
@@ -135,16 +135,16 @@ struct gbnr_plan {
         v.max_iter = opt.max_iter;
     }
 
-    gbnr::WalkView upload_walk(const gbnr::Walk& w) {
+    gbnr::WalkView upload_walk(const gbnr::WalkSet& w) {
         gbnr::WalkView x{};
         x.stream = dev_upload(owned, w.stream);
-        x.n_pages = w.n_pages;
+        x.walkers = w.walkers;
         x.page_words = w.page_words;
-        x.pages = w.pages;
-        x.ring_rows = w.ring_rows;
-        x.stage_rows = w.stage_rows;
-        x.barriers = w.barriers;
+        x.rows = w.rows;
+        if (w.walkers < 1 || w.walkers > 8) throw Error(GBNR_ECONFIG, "1..8 walkers per tile");
+        for (int32_t i = 0; i <= w.walkers; ++i) x.wpage0[i] = w.wpage0[i];
         if (w.barriers != 32 || w.pages != 4) throw Error(GBNR_ECONFIG, "walk kernels use 32 barriers, 4 pages");
+        if (gbnr::walk_smem_bytes(x) != w.smem_bytes()) throw Error(GBNR_ECONFIG, "walk smem layout mismatch");
         if (gbnr::walk_smem_bytes(x) > 227 * 1024)
             throw Error(GBNR_ECONFIG, "walk needs more shared memory than a B200 CTA has");
         return x;
@@ -382,11 +382,12 @@ void gbnr_default_options(gbnr_options* o) {
     o->pivot_tol = 1e-3;
     o->singular_tol = 1e-14;
     o->device = 0;
-    o->ring_rows = 176;
+    o->ring_rows = 0;
     o->profile = 0;
-    o->stage_rows = 80;
+    o->stage_rows = 0;
     o->prefetch = 8;
     o->headroom = 2;
+    o->walkers = 4;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -434,7 +435,8 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             gbnr_default_options(&p->opt);
         if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 30)
             throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 30");
-        if (p->opt.ring_rows < 0 || p->opt.stage_rows < 0 || p->opt.prefetch < 0 || p->opt.headroom < 0)
+        if (p->opt.ring_rows < 0 || p->opt.stage_rows < 0 || p->opt.prefetch < 0 || p->opt.headroom < 0 ||
+            p->opt.walkers < 0 || p->opt.walkers > 8)
             throw Error(GBNR_ECONFIG, "negative walk parameter");
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
@@ -444,6 +446,7 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (p->opt.stage_rows) wc.stage_rows = p->opt.stage_rows;
         if (p->opt.prefetch) wc.prefetch = p->opt.prefetch;
         if (p->opt.headroom) wc.headroom = p->opt.headroom;
+        if (p->opt.walkers) wc.walkers = p->opt.walkers;
         p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
         p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
         p->wb = gbnr::build_backward_walk(p->sym, p->lay, wc);
@@ -532,7 +535,7 @@ int gbnr_last_timing(const gbnr_plan* p, double* out) {
     return guarded([&] { std::memcpy(out, p->timing, sizeof p->timing); });
 }
 
-static const gbnr::Walk& pick_walk(const gbnr_plan* p, int32_t which) {
+static const gbnr::WalkSet& pick_walk(const gbnr_plan* p, int32_t which) {
     if (which == 0) return p->wf;
     if (which == 1) return p->wl;
     if (which == 2) return p->wb;
@@ -541,35 +544,30 @@ static const gbnr::Walk& pick_walk(const gbnr_plan* p, int32_t which) {
 
 int gbnr_walk_info(const gbnr_plan* p, int32_t which, int64_t* o) {
     return guarded([&] {
-        const gbnr::Walk& w = pick_walk(p, which);
-        const int64_t vals[17] = {w.n_steps, int64_t(w.dep.size()), int64_t(w.dst.size()),
-                                  int64_t(w.op.size()), int64_t(w.ut.size()), w.ring_rows,
-                                  w.stage_rows, w.barriers, w.events, w.ring_dep_rows,
-                                  w.fetched_rows, int64_t(w.smem_bytes()),
-                                  int64_t(w.stream.size()), w.page_words, w.pages, w.n_pages,
-                                  int64_t(w.copies.size())};
+        const gbnr::WalkSet& w = pick_walk(p, which);
+        const int64_t vals[16] = {w.steps, w.walkers, w.phases, w.rows, w.page_words, w.pages,
+                                  w.barriers, int64_t(w.stream.size()), w.events, w.ring_dep_rows,
+                                  w.fetched_rows, w.n_ops, w.n_copies, int64_t(w.smem_bytes()),
+                                  w.parts.empty() ? 0 : w.parts[0].ring_rows,
+                                  w.parts.empty() ? 0 : w.parts[0].stage_rows};
         std::memcpy(o, vals, sizeof vals);
     });
 }
 
 int gbnr_walk_export(const gbnr_plan* p, int32_t which, int32_t part, void* dst) {
     return guarded([&] {
-        const gbnr::Walk& w = pick_walk(p, which);
+        const gbnr::WalkSet& w = pick_walk(p, which);
         auto put = [&](const auto& vec) {
             if (!vec.empty()) std::memcpy(dst, vec.data(), vec.size() * sizeof(vec[0]));
         };
         switch (part) {
-            case 0: put(w.step); break;
-            case 1: put(w.dep); break;
-            case 2: put(w.dst); break;
-            case 3: put(w.op); break;
-            case 4: put(w.ut); break;
-            case 5: put(p->lay.tape_of_ccs); break;
-            case 6: put(p->lay.lslot); break;
-            case 7: put(p->lay.ucrs0); break;
-            case 8: put(w.stream); break;
-            case 9: put(w.copies); break;
-            default: throw Error(GBNR_ECONFIG, "walk part must be 0..9");
+            case 0: put(w.stream); break;
+            case 1: put(w.wpage0); break;
+            case 2: put(w.owner); break;
+            case 3: put(p->lay.tape_of_ccs); break;
+            case 4: put(p->lay.lslot); break;
+            case 5: put(p->lay.ucrs0); break;
+            default: throw Error(GBNR_ECONFIG, "walk part must be 0..5");
         }
     });
 }

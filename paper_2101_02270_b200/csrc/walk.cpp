@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <deque>
 #include <limits>
+#include <queue>
 #include <string>
 
 namespace gbnr {
@@ -19,7 +20,8 @@ int32_t copy_rows(const WCopy& c) { return c.tape_rows >> 8; }
 
 // What a step loads into its own ring block, and what each dependency needs.
 struct DepIn {
-    int32_t producer;        // producing step
+    int32_t producer;        // producing step of the same program, -1 = external
+                             // (an earlier phase / another walker: always re-fetched)
     int32_t ring_src = -1;   // rows relative to the producer's block
     int32_t ring_ysrc = -1;
     std::vector<WCopy> fetch;  // copies relative to a staging allocation
@@ -33,6 +35,16 @@ struct StepIn {
     std::vector<DepIn> deps;
     WStep rec{};                // payload fields (len_dp, lslot, ut0, brow)
 };
+// A walker's program before planning: its steps and their payload arrays.
+struct Program {
+    std::vector<StepIn> steps;
+    std::vector<uint16_t> dst;
+    std::vector<int32_t> ut;
+};
+
+struct PlanCfg {
+    int32_t ring_base, ring_rows, stage_rows, barriers, prefetch, headroom, max_copies;
+};
 
 // Allocate rows [cur, cur+n) in a ring of `cap` rows; skip to the start when
 // the request does not fit before the end (TMA copies must be contiguous).
@@ -43,19 +55,21 @@ int32_t ring_alloc(int32_t& cur, int32_t n, int32_t cap) {
     return at;
 }
 
-Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
+// Plan one walker's program over its shared-memory share; op indices local.
+Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
     const int32_t T = static_cast<int32_t>(steps.size());
     Walk w;
-    int32_t max_blk = 0, max_fetch = 0;
-    for (const StepIn& s : steps) {
-        max_blk = std::max(max_blk, s.blk_rows);
-        for (const DepIn& d : s.deps) max_fetch = std::max(max_fetch, d.fetch_rows);
-    }
-    w.ring_rows = std::max(cfg.ring_rows, max_blk);
-    w.stage_rows = std::max(cfg.stage_rows, max_fetch);
+    w.ring_base = cfg.ring_base;
+    w.ring_rows = cfg.ring_rows;
+    w.stage_rows = cfg.stage_rows;
     w.barriers = cfg.barriers;
     w.n_steps = T;
-    const int32_t XR = w.ring_rows, SR = w.stage_rows, NB = w.barriers;
+    const int32_t XR = w.ring_rows, SR = w.stage_rows, NB = w.barriers, RB = cfg.ring_base;
+    for (const StepIn& s : steps) {
+        if (s.blk_rows > XR) throw Error(3, "walk block larger than the walker's ring");
+        for (const DepIn& d : s.deps)
+            if (d.fetch_rows > SR) throw Error(3, "walk fetch larger than the walker's staging ring");
+    }
 
     // 1. ring placement and first overwriter of every block
     std::vector<int32_t> ring(T), ovw(T, kInf);
@@ -89,7 +103,8 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
         for (size_t d = 0; d < steps[t].deps.size(); ++d) {
             const DepIn& di = steps[t].deps[d];
             if (di.producer >= t) throw Error(3, "walk dependency is not earlier in the walk");
-            const bool res = ovw[di.producer] == kInf || t + cfg.headroom < ovw[di.producer];
+            const bool res = di.producer >= 0 &&
+                             (ovw[di.producer] == kInf || t + cfg.headroom < ovw[di.producer]);
             resident[t][d] = res;
             if (res) lastuser[di.producer] = std::max(lastuser[di.producer], t);
         }
@@ -110,21 +125,20 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
     // 4. ops in consumption order with their issue events.  One op per step
     //    carries the step's block AND every re-fetched dependency whose staging
     //    region fits beside the others (a "chunk"); a step whose fetches exceed
-    //    the staging ring continues in further chunks, each waited on at its
-    //    first dependency.
+    //    the staging ring (or a page's copy limit) continues in further chunks,
+    //    each waited on at its first dependency.
     struct Live {
         int32_t a, b, release;
     };
     std::deque<Live> stage_live;
     int32_t scur = 0;
-    std::vector<int32_t> release;  // per op: event after which its mbarrier may be re-armed
+    std::vector<int32_t> release;      // per op: event after which its mbarrier may be re-armed
     std::vector<int32_t> tag_of_copy;  // content tag per copy (verification)
     std::vector<int32_t> dep_tag0(T + 1, 0);  // tag of dependency (t, d) = T + dep_tag0[t] + d
     for (int32_t t = 0; t < T; ++t) dep_tag0[t + 1] = dep_tag0[t] + int32_t(steps[t].deps.size());
     std::vector<int32_t> tag_producer(dep_tag0[T], -1), op_of_tag(dep_tag0[T], kInf);
     for (int32_t t = 0; t < T; ++t)
         for (size_t d = 0; d < steps[t].deps.size(); ++d) tag_producer[dep_tag0[t] + d] = steps[t].deps[d].producer;
-
     struct Chunk {
         std::vector<WCopy> cps;
         std::vector<int32_t> tags;
@@ -153,7 +167,7 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
     for (int32_t t = 0; t < T; ++t) {
         StepIn& si = steps[t];
         WStep rec = si.rec;
-        rec.ring = ring[t];
+        rec.ring = RB + ring[t];
         rec.dep0 = static_cast<int32_t>(w.dep.size());
         rec.ndep = static_cast<int32_t>(si.deps.size());
         w.block_rows += si.blk_rows;
@@ -163,7 +177,7 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
         ch.consume = ev_done(t - 1);
         ch.rel = int32_t(ev0[t]);  // barrier free once the step-start wait has passed
         for (WCopy c : si.copies) {
-            c.smem += ring[t];
+            c.smem += RB + ring[t];
             ch.cps.push_back(c);
             ch.tags.push_back(t);
         }
@@ -183,8 +197,8 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
             WDep dr = di.rec;
             dr.op = -1;
             if (resident[t][d]) {
-                dr.src = di.ring_src >= 0 ? ring[di.producer] + di.ring_src : -1;
-                dr.ysrc = di.ring_ysrc >= 0 ? ring[di.producer] + di.ring_ysrc : -1;
+                dr.src = di.ring_src >= 0 ? RB + ring[di.producer] + di.ring_src : -1;
+                dr.ysrc = di.ring_ysrc >= 0 ? RB + ring[di.producer] + di.ring_ysrc : -1;
                 w.ring_dep_rows += di.fetch_rows;
                 w.dep.push_back(dr);
                 continue;
@@ -192,8 +206,10 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
             if (di.fetch_rows <= 0) throw Error(3, "walk dependency with nothing to fetch");
             int32_t cur = scur;
             const int32_t at = XR + ring_alloc(cur, di.fetch_rows, SR);
-            // a region overlapping this chunk's own staging span starts a new chunk
-            if (!ch.tags.empty() && at < ch.hi && ch.lo < at + di.fetch_rows) {
+            // a region overlapping this chunk's own staging span, or too many
+            // copies for one program record, starts a new chunk
+            const bool clash = ch.hi >= 0 && at < ch.hi && ch.lo < at + di.fetch_rows;
+            if (clash || int32_t(ch.cps.size() + di.fetch.size()) > cfg.max_copies) {
                 close_chunk();
                 ch = Chunk{};
                 ch.after = ev_done(t - cfg.prefetch - 1);
@@ -214,12 +230,12 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
             keep.push_back(Live{at, at + di.fetch_rows, ev_dep(t, d)});
             stage_live.swap(keep);
             for (WCopy c : di.fetch) {
-                c.smem += at;
+                c.smem += RB + at;
                 ch.cps.push_back(c);
                 ch.tags.push_back(T + dep_tag0[t] + int32_t(d));
             }
-            dr.src = di.stage_src >= 0 ? at + di.stage_src : -1;
-            dr.ysrc = di.stage_ysrc >= 0 ? at + di.stage_ysrc : -1;
+            dr.src = di.stage_src >= 0 ? RB + at + di.stage_src : -1;
+            dr.ysrc = di.stage_ysrc >= 0 ? RB + at + di.stage_ysrc : -1;
             w.fetched_rows += di.fetch_rows;
             chunk_deps.push_back(w.dep.size());
             w.dep.push_back(dr);
@@ -252,8 +268,8 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
                 const WOp& o = w.op[next];
                 for (int32_t i = 0; i < o.ncopy; ++i) {
                     const WCopy& c = w.copies[o.c0 + i];
-                    const int32_t a = c.smem, n = copy_rows(c), g = tag_of_copy[o.c0 + i];
-                    if (a < 0 || a + n > rows) throw Error(3, "walk copy outside shared memory");
+                    const int32_t a = c.smem - RB, n = copy_rows(c), g = tag_of_copy[o.c0 + i];
+                    if (a < 0 || a + n > rows) throw Error(3, "walk copy outside the walker's shared memory");
                     for (int32_t r = a; r < a + n; ++r) {
                         if (row_tag[r] >= 0 && need[row_tag[r]] > ev)
                             throw Error(3, "walk plan overwrites live shared memory (row " +
@@ -270,7 +286,7 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
             }
         };
         auto expect = [&](int32_t row, int32_t g) {
-            if (row >= 0 && row_tag[row] != g) throw Error(3, "walk reads content that is not there");
+            if (row >= 0 && row_tag[row - RB] != g) throw Error(3, "walk reads content that is not there");
         };
         issue_upto(-1);
         int32_t waited = -1;
@@ -300,35 +316,36 @@ Walk plan(std::vector<StepIn>& steps, const WalkConfig& cfg) {
     return w;
 }
 
-// Serialise a verified walk into the word stream the kernels interpret:
-// prologue issues, then per step: STEP, (DEP, ISSUE*) per dependency, END,
-// ISSUE* -- each ISSUE placed right after the consumer event it waits for.
-void encode_stream(Walk& w, bool forward, const WalkConfig& cfg) {
+// Program-stream writer of one walker: pads to the next page whenever a record
+// would straddle one.
+struct Emitter {
     std::vector<int32_t> st;
-    int32_t W = cfg.page_words;
-    // longest record decides the page size
-    int32_t longest = 4;
-    for (const WOp& o : w.op) longest = std::max(longest, 3 + 2 * o.ncopy);
-    for (const WStep& s : w.step) {
-        const int32_t dp = forward ? (s.len_dp >> 16) : 0;
-        longest = std::max(longest, 1 + dp);
-        for (int32_t d = 0; d < s.ndep; ++d)
-            longest = std::max(longest, 4 + (w.dep[s.dep0 + d].nrows + 1) / 2);
-    }
-    W = std::max(W, (longest + 1 + 3) / 4 * 4);
-    auto emit = [&](const std::vector<int32_t>& rec) {
+    int32_t W;
+    void emit(const std::vector<int32_t>& rec) {
+        if (int32_t(rec.size()) > W - 1) throw Error(3, "walk record longer than a program page");
         const int32_t used = int32_t(st.size() % size_t(W));
         if (used + int32_t(rec.size()) > W - 1) {
             st.push_back(kRecPage);
             while (st.size() % size_t(W)) st.push_back(0);
         }
         st.insert(st.end(), rec.begin(), rec.end());
-    };
+    }
+    void finish() {
+        emit({kRecDone});
+        while (st.size() % size_t(W)) st.push_back(0);
+    }
+};
+
+// Serialise one verified program: prologue issues, then per step: STEP,
+// (DEP, ISSUE*) per dependency, END, ISSUE* -- each ISSUE right after the
+// consumer event it waits for.  Op numbers continue at op_base (barrier parity
+// runs on across phases).
+void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
     size_t next = 0;
     auto issue_upto = [&](int64_t ev) {
         while (next < w.op.size() && w.op[next].after <= ev) {
             const WOp& o = w.op[next];
-            std::vector<int32_t> rec{kRecIssue | (o.ncopy << 4), int32_t(next), o.bytes};
+            std::vector<int32_t> rec{kRecIssue | (o.ncopy << 4), op_base + int32_t(next), o.bytes};
             for (int32_t i = 0; i < o.ncopy; ++i) {
                 const WCopy& c = w.copies[o.c0 + i];
                 const int32_t tape = c.tape_rows & 0xff, rows = c.tape_rows >> 8;
@@ -336,51 +353,182 @@ void encode_stream(Walk& w, bool forward, const WalkConfig& cfg) {
                 rec.push_back(tape | (rows << 2) | (c.smem << 12));
                 rec.push_back(c.slot);
             }
-            emit(rec);
+            em.emit(rec);
             ++next;
         }
     };
+    auto opn = [&](int32_t op) { return op >= 0 ? op_base + op : -1; };
     issue_upto(-1);
     int64_t ev = 0;
     for (const WStep& s : w.step) {
         if (forward) {
             const int32_t len = s.len_dp & 0xffff, dp = s.len_dp >> 16;
-            emit({kRecStep | (s.ndep << 4), s.ring | (len << 16), dp, s.lslot, s.brow, s.op});
+            em.emit({kRecStep | (s.ndep << 4), s.ring | (len << 16), dp, s.lslot, s.brow, opn(s.op)});
             for (int32_t d = 0; d < s.ndep; ++d) {
                 const WDep& e = w.dep[s.dep0 + d];
                 if (e.src >= 65536 || e.nrows >= 65536) throw Error(3, "walk dependency too large to encode");
-                std::vector<int32_t> rec{kRecDep | ((e.op + 1) << 4), e.kpos_fs,
+                std::vector<int32_t> rec{kRecDep | ((opn(e.op) + 1) << 4), e.kpos_fs,
                                          e.nrows | (std::max(e.src, 0) << 16), e.ysrc};
                 for (int32_t r = 0; r < e.nrows; r += 2) {
                     const int32_t lo = w.dst[e.u0 + r];
                     const int32_t hi = r + 1 < e.nrows ? w.dst[e.u0 + r + 1] : 0;
                     rec.push_back(lo | (hi << 16));
                 }
-                emit(rec);
+                em.emit(rec);
                 issue_upto(ev++);
             }
             std::vector<int32_t> end{kRecEnd | (dp << 4)};
             for (int32_t z = 0; z < dp; ++z) end.push_back(w.ut[s.ut0 + z]);
-            emit(end);
+            em.emit(end);
             issue_upto(ev++);
         } else {
-            emit({kRecStep | (s.ndep << 4), s.ring | (s.len_dp << 16), 0, s.lslot, s.brow, s.op});
+            em.emit({kRecStep | (s.ndep << 4), s.ring | (s.len_dp << 16), 0, s.lslot, s.brow, opn(s.op)});
             for (int32_t d = 0; d < s.ndep; ++d) {
                 const WDep& e = w.dep[s.dep0 + d];
-                emit({kRecDep | ((e.op + 1) << 4), e.ysrc});
+                em.emit({kRecDep | ((opn(e.op) + 1) << 4), e.ysrc});
                 issue_upto(ev++);
             }
-            emit({kRecEnd});
+            em.emit({kRecEnd});
             issue_upto(ev++);
         }
     }
     if (next != w.op.size()) throw Error(3, "walk stream left ops unissued");
-    emit({kRecDone});
-    while (st.size() % size_t(W)) st.push_back(0);
-    w.stream = std::move(st);
-    w.page_words = W;
-    w.pages = cfg.pages;
-    w.n_pages = int32_t(w.stream.size() / size_t(W));
+}
+
+// Elimination tree of the frozen pattern: parent(k) = first L row of column k.
+std::vector<int32_t> etree_parent(const Symbolic& s) {
+    std::vector<int32_t> parent(s.nJ, -1);
+    for (int32_t k = 0; k < s.nJ; ++k)
+        if (s.dpos[k] + 1 < s.cp[k + 1]) parent[k] = s.ri[s.dpos[k] + 1];
+    return parent;
+}
+
+// Shared-memory geometry of a launch: page size from the longest possible
+// record, then the rows left in the CTA budget.
+struct Geometry {
+    int32_t W = 0, rows = 0;
+};
+Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
+    int32_t longest = 8;
+    for (int32_t k = 0; k < s.nJ; ++k) {
+        longest = std::max(longest, 2 + (s.dpos[k] - s.cp[k]));           // END
+        longest = std::max(longest, 5 + (s.cp[k + 1] - s.dpos[k]) / 2);  // DEP
+    }
+    const int32_t W = std::max(cfg.page_words, 4 * ((longest + 1 + 3) / 4));
+    const int64_t fixed = int64_t(walkers) * (int64_t(cfg.pages) * W * 4 + int64_t(cfg.barriers + cfg.pages) * 8);
+    const int64_t rows = (int64_t(cfg.smem_budget) - fixed) / 256;
+    return Geometry{W, int32_t(std::max<int64_t>(rows, 0))};
+}
+
+// Per-walker ring / staging split of a share of rows.
+void split_share(const WalkConfig& cfg, int32_t share, int32_t& ring, int32_t& stage) {
+    stage = cfg.stage_rows ? cfg.stage_rows : share * 3 / 10;
+    ring = cfg.ring_rows ? cfg.ring_rows : share - stage;
+}
+
+struct Phase {
+    std::vector<std::vector<int32_t>> lists;  // per walker: steps (column / row ids) in walk order
+};
+
+// Plan and encode every (phase, walker) program of a walk set.
+template <class MakeProgram>
+WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, const std::vector<Phase>& phases,
+                 bool forward, MakeProgram&& make_program) {
+    WalkSet ws;
+    ws.walkers = walkers;
+    ws.phases = static_cast<int32_t>(phases.size());
+    ws.page_words = g.W;
+    ws.pages = cfg.pages;
+    ws.barriers = cfg.barriers;
+    ws.rows = g.rows;
+    std::vector<Emitter> em(walkers, Emitter{{}, g.W});
+    std::vector<int32_t> op_base(walkers, 0);
+    for (size_t ph = 0; ph < phases.size(); ++ph) {
+        int32_t active = 0;
+        for (const auto& l : phases[ph].lists) active += !l.empty();
+        const int32_t share = active > 0 ? g.rows / active : g.rows;
+        int32_t slot = 0;
+        for (int32_t w = 0; w < walkers; ++w) {
+            const std::vector<int32_t>& list = phases[ph].lists[w];
+            Walk part;
+            if (!list.empty()) {
+                PlanCfg pc{};
+                pc.ring_base = slot * share;
+                split_share(cfg, share, pc.ring_rows, pc.stage_rows);
+                if (pc.ring_rows + pc.stage_rows > share) throw Error(3, "walk ring overrides exceed the CTA budget");
+                pc.barriers = cfg.barriers;
+                pc.prefetch = cfg.prefetch;
+                pc.headroom = cfg.headroom;
+                pc.max_copies = (g.W - 5) / 2;
+                Program pr = make_program(list);
+                part = plan(pr.steps, pc);
+                part.dst = std::move(pr.dst);
+                part.ut = std::move(pr.ut);
+                encode(em[w], part, forward, op_base[w]);
+                op_base[w] += static_cast<int32_t>(part.op.size());
+                ++slot;
+            }
+            ws.steps += part.n_steps;
+            ws.events += part.events;
+            ws.ring_dep_rows += part.ring_dep_rows;
+            ws.fetched_rows += part.fetched_rows;
+            ws.n_ops += int64_t(part.op.size());
+            ws.n_copies += int64_t(part.copies.size());
+            ws.parts.push_back(std::move(part));
+        }
+        if (ph + 1 < phases.size())
+            for (auto& e : em) e.emit({kRecSync});
+    }
+    ws.wpage0.assign(walkers + 1, 0);
+    for (int32_t w = 0; w < walkers; ++w) {
+        em[w].finish();
+        ws.wpage0[w + 1] = ws.wpage0[w] + int32_t(em[w].st.size() / size_t(g.W));
+        ws.stream.insert(ws.stream.end(), em[w].st.begin(), em[w].st.end());
+    }
+    if (ws.smem_bytes() > size_t(cfg.smem_budget)) throw Error(3, "walk exceeds its shared-memory budget");
+    return ws;
+}
+
+// Phase lists: forward = bins in parallel, then the top by walker 0;
+// backward = the top first (descending), then the bins (descending).
+std::vector<Phase> make_phases(const std::vector<int32_t>& owner, int32_t K, bool forward) {
+    const int32_t n = static_cast<int32_t>(owner.size());
+    Phase bins, top;
+    bins.lists.resize(K);
+    top.lists.resize(K);
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t c = forward ? i : n - 1 - i;
+        if (owner[c] >= 0)
+            bins.lists[owner[c]].push_back(c);
+        else
+            top.lists[0].push_back(c);
+    }
+    std::vector<Phase> ph;
+    const bool any_top = !top.lists[0].empty();
+    if (forward) {
+        ph.push_back(std::move(bins));
+        if (any_top) ph.push_back(std::move(top));
+    } else {
+        if (any_top) ph.push_back(std::move(top));
+        ph.push_back(std::move(bins));
+    }
+    return ph;
+}
+
+// Walker count and column ownership for a launch (falls back to one walker).
+std::vector<int32_t> choose_owner(const Symbolic& s, const WalkConfig& cfg, int32_t& K, Geometry& g) {
+    K = std::max(1, std::min(cfg.walkers, 8));
+    for (;;) {
+        g = geometry(s, cfg, K);
+        int32_t ring = 0, stage = 0;
+        split_share(cfg, g.rows / K, ring, stage);
+        WalkConfig c = cfg;
+        c.walkers = K;
+        std::vector<int32_t> owner = partition_walkers(s, c, ring, stage);
+        if (!owner.empty()) return owner;
+        if (K == 1) return std::vector<int32_t>(s.nJ, 0);
+        K = 1;  // dependencies cross subtrees: one walker
+    }
 }
 
 }  // namespace
@@ -414,119 +562,209 @@ LuLayout build_lu_layout(const Symbolic& s) {
     return lay;
 }
 
+// Subtree-to-walker mapping (proportional mapping on the elimination tree):
+// peel the heaviest subtrees (and any subtree holding a column too big for a
+// walker's share) into the serial "top", then deal the remaining whole
+// subtrees to the walkers, heaviest first onto the lightest walker.
+std::vector<int32_t> partition_walkers(const Symbolic& s, const WalkConfig& cfg, int32_t ring_w,
+                                       int32_t stage_w) {
+    const int32_t nJ = s.nJ, K = cfg.walkers;
+    std::vector<int32_t> owner(nJ, -1);
+    if (K <= 1 || nJ == 0) {
+        std::fill(owner.begin(), owner.end(), 0);
+        return owner;
+    }
+    const std::vector<int32_t> parent = etree_parent(s);
+    std::vector<double> work(nJ), sub(nJ);
+    std::vector<int32_t> smax_blk(nJ), smax_fetch(nJ);
+    std::vector<std::vector<int32_t>> children(nJ);
+    for (int32_t k = 0; k < nJ; ++k) {
+        double wk = 60.0 + (s.cp[k + 1] - s.cp[k]);
+        for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) {
+            const int32_t j = s.ri[z];
+            wk += 12.0 + (s.cp[j + 1] - s.dpos[j] - 1);
+        }
+        work[k] = sub[k] = wk;
+        smax_blk[k] = s.cp[k + 1] - s.cp[k] + 1;
+        smax_fetch[k] = s.cp[k + 1] - s.dpos[k];
+        if (parent[k] >= 0) children[parent[k]].push_back(k);
+    }
+    for (int32_t k = 0; k < nJ; ++k)  // parent > k, so children are final first
+        if (parent[k] >= 0) {
+            if (parent[k] <= k) return {};
+            sub[parent[k]] += sub[k];
+            smax_blk[parent[k]] = std::max(smax_blk[parent[k]], smax_blk[k]);
+            smax_fetch[parent[k]] = std::max(smax_fetch[parent[k]], smax_fetch[k]);
+        }
+    double total = 0.0;
+    for (double x : work) total += x;
+    const double thr = total / (K * cfg.balance);
+    std::priority_queue<std::pair<double, int32_t>> heap;
+    for (int32_t k = 0; k < nJ; ++k)
+        if (parent[k] < 0) heap.emplace(sub[k], k);
+    std::vector<std::pair<double, int32_t>> keep;
+    while (!heap.empty()) {
+        const auto [wt, r] = heap.top();
+        heap.pop();
+        if (wt > thr || smax_blk[r] > ring_w || smax_fetch[r] > stage_w) {
+            for (int32_t c : children[r]) heap.emplace(sub[c], c);  // r stays in the top
+        } else {
+            keep.emplace_back(wt, r);
+        }
+    }
+    std::sort(keep.begin(), keep.end(), std::greater<>());
+    std::vector<double> load(K, 0.0);
+    for (const auto& [wt, r] : keep) {
+        const int32_t b = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
+        load[b] += wt;
+        std::vector<int32_t> st{r};
+        while (!st.empty()) {
+            const int32_t u = st.back();
+            st.pop_back();
+            owner[u] = b;
+            for (int32_t c : children[u]) st.push_back(c);
+        }
+    }
+    // every dependency must stay inside its walker: a column of a subtree may
+    // only touch columns of the same subtree, or later top columns (which the
+    // forward walk runs after the subtrees and the backward walk before them)
+    for (int32_t j = 0; j < nJ; ++j) {
+        if (owner[j] < 0) continue;
+        for (int32_t z = s.cp[j]; z < s.cp[j + 1]; ++z) {
+            const int32_t k = s.ri[z];
+            if (k != j && owner[k] != owner[j] && !(k > j && owner[k] < 0)) return {};
+        }
+    }
+    return owner;
+}
+
 // Forward walk: column m of Alg. 2 (+ row m of the forward substitution).
 // Block of column m: its A rows (len) [+ the b row, replaced by y_m].
 // Dependencies, ascending k: the union of the U pattern of column m (LU
 // updates) and the L pattern of row m (FS terms).
-Walk build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg) {
+WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg) {
     const int32_t nJ = s.nJ;
     std::vector<std::vector<int32_t>> lrow(nJ);  // k with L(m,k) != 0, ascending
     if (with_fs)
         for (int32_t k = 0; k < nJ; ++k)
             for (int32_t z = s.dpos[k] + 1; z < s.cp[k + 1]; ++z) lrow[s.ri[z]].push_back(k);
-    std::vector<StepIn> steps(nJ);
-    std::vector<int32_t> posmap(nJ, -1);
-    std::vector<uint16_t> dst;
-    std::vector<int32_t> ut;
-    for (int32_t m = 0; m < nJ; ++m) {
-        const int32_t c0 = s.cp[m], len = s.cp[m + 1] - c0, dp = s.dpos[m] - c0;
-        StepIn& si = steps[m];
-        si.blk_rows = len + (with_fs ? 1 : 0);
-        si.copies.push_back(copy(kTapeA, c0, len, 0));
-        if (with_fs) si.copies.push_back(copy(kTapeB, m, 1, len));
-        si.rec.len_dp = len | (dp << 16);
-        si.rec.lslot = lay.lslot[m];
-        si.rec.ut0 = static_cast<int32_t>(ut.size());
-        si.rec.brow = m;
-        for (int32_t z = c0; z < s.dpos[m]; ++z) ut.push_back(lay.tape_of_ccs[z]);
-        for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = z - c0;
-        // merge U deps (rows < m of column m) with the L row of m
-        std::vector<int32_t> ks;
-        for (int32_t z = c0; z < s.dpos[m]; ++z) ks.push_back(s.ri[z]);
-        ks.insert(ks.end(), lrow[m].begin(), lrow[m].end());
-        std::sort(ks.begin(), ks.end());
-        ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
-        for (int32_t k : ks) {
-            DepIn di;
-            di.producer = k;
-            const int32_t lk0 = s.dpos[k] + 1, nl = s.cp[k + 1] - lk0;  // L(:,k) rows
-            const int32_t kpos = posmap[k];
-            const bool upd = kpos >= 0 && kpos < dp;
-            int32_t fspos = 0xffff;
-            if (with_fs) {
-                const int32_t* b = s.ri.data() + lk0;
-                const int32_t* f = std::lower_bound(b, b + nl, m);
-                if (f != b + nl && *f == m) fspos = int32_t(f - b);
-            }
-            if (!upd && fspos == 0xffff) throw Error(2, "walk dependency without a role");
-            di.rec.kpos_fs = (upd ? kpos : 0xffff) | (fspos << 16);
-            di.rec.nrows = upd ? nl : 0;
-            di.rec.u0 = static_cast<int32_t>(dst.size());
-            if (upd)
-                for (int32_t zz = lk0; zz < lk0 + nl; ++zz) {
-                    const int32_t d = posmap[s.ri[zz]];
-                    if (d < 0) throw Error(2, "frozen LU pattern is not closed");
-                    dst.push_back(static_cast<uint16_t>(d));
+    int32_t K = 1;
+    Geometry g;
+    std::vector<int32_t> owner = choose_owner(s, cfg, K, g);
+    const std::vector<Phase> phases = make_phases(owner, K, true);
+    std::vector<int32_t> posmap(nJ, -1), local(nJ, -1);
+    auto make_program = [&](const std::vector<int32_t>& list) {
+        for (size_t i = 0; i < list.size(); ++i) local[list[i]] = int32_t(i);
+        Program pr;
+        pr.steps.resize(list.size());
+        for (size_t i = 0; i < list.size(); ++i) {
+            const int32_t m = list[i];
+            const int32_t c0 = s.cp[m], len = s.cp[m + 1] - c0, dp = s.dpos[m] - c0;
+            StepIn& si = pr.steps[i];
+            si.blk_rows = len + (with_fs ? 1 : 0);
+            si.copies.push_back(copy(kTapeA, c0, len, 0));
+            if (with_fs) si.copies.push_back(copy(kTapeB, m, 1, len));
+            si.rec.len_dp = len | (dp << 16);
+            si.rec.lslot = lay.lslot[m];
+            si.rec.ut0 = static_cast<int32_t>(pr.ut.size());
+            si.rec.brow = m;
+            for (int32_t z = c0; z < s.dpos[m]; ++z) pr.ut.push_back(lay.tape_of_ccs[z]);
+            for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = z - c0;
+            std::vector<int32_t> ks;
+            for (int32_t z = c0; z < s.dpos[m]; ++z) ks.push_back(s.ri[z]);
+            ks.insert(ks.end(), lrow[m].begin(), lrow[m].end());
+            std::sort(ks.begin(), ks.end());
+            ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+            for (int32_t k : ks) {
+                DepIn di;
+                di.producer = local[k] >= 0 && local[k] < int32_t(i) ? local[k] : -1;
+                const int32_t lk0 = s.dpos[k] + 1, nl = s.cp[k + 1] - lk0;  // L(:,k) rows
+                if (nl == 0) throw Error(2, "walk dependency on an empty L column");
+                const int32_t kpos = posmap[k];
+                const bool upd = kpos >= 0 && kpos < dp;
+                int32_t fspos = 0xffff;
+                if (with_fs) {
+                    const int32_t* b = s.ri.data() + lk0;
+                    const int32_t* f = std::lower_bound(b, b + nl, m);
+                    if (f != b + nl && *f == m) fspos = int32_t(f - b);
                 }
-            const int32_t klen = s.cp[k + 1] - s.cp[k], kdp = s.dpos[k] - s.cp[k];
-            di.ring_src = kdp + 1;
-            di.ring_ysrc = with_fs ? klen : -1;
-            di.fetch.push_back(copy(kTapeLU, lay.lslot[k] + 1, nl, 0));
-            di.stage_src = 0;
-            di.fetch_rows = nl;
-            if (with_fs) {
-                di.fetch.push_back(copy(kTapeB, k, 1, nl));
-                di.stage_ysrc = nl;
-                di.fetch_rows = nl + 1;
+                if (!upd && fspos == 0xffff) throw Error(2, "walk dependency without a role");
+                di.rec.kpos_fs = (upd ? kpos : 0xffff) | (fspos << 16);
+                di.rec.nrows = upd ? nl : 0;
+                di.rec.u0 = static_cast<int32_t>(pr.dst.size());
+                if (upd)
+                    for (int32_t zz = lk0; zz < lk0 + nl; ++zz) {
+                        const int32_t d = posmap[s.ri[zz]];
+                        if (d < 0) throw Error(2, "frozen LU pattern is not closed");
+                        pr.dst.push_back(static_cast<uint16_t>(d));
+                    }
+                const int32_t klen = s.cp[k + 1] - s.cp[k], kdp = s.dpos[k] - s.cp[k];
+                di.ring_src = kdp + 1;
+                di.ring_ysrc = with_fs ? klen : -1;
+                di.fetch.push_back(copy(kTapeLU, lay.lslot[k] + 1, nl, 0));
+                di.stage_src = 0;
+                di.fetch_rows = nl;
+                if (with_fs) {
+                    di.fetch.push_back(copy(kTapeB, k, 1, nl));
+                    di.stage_ysrc = nl;
+                    di.fetch_rows = nl + 1;
+                }
+                si.deps.push_back(std::move(di));
             }
-            if (nl == 0) {  // nothing below the diagonal: never a dependency
-                throw Error(2, "walk dependency on an empty L column");
-            }
-            si.deps.push_back(std::move(di));
+            for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = -1;
         }
-        for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = -1;
-    }
-    Walk w = plan(steps, cfg);
-    w.dst = std::move(dst);
-    w.ut = std::move(ut);
-    encode_stream(w, true, cfg);
-    return w;
+        for (int32_t c : list) local[c] = -1;
+        return pr;
+    };
+    WalkSet ws = assemble(cfg, K, g, phases, true, make_program);
+    ws.owner = std::move(owner);
+    return ws;
 }
 
 // Backward walk: rows i = nJ-1 .. 0.  Block of row i: its U entries (CRS,
 // descending k), the y_i row (replaced by x_i) and the diagonal U(i,i).
 // Dependencies: x_k for every U(i,k), descending k.
-Walk build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg) {
+WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg) {
     const int32_t nJ = s.nJ;
     std::vector<std::vector<int32_t>> urow(nJ);  // k descending
     for (int32_t k = nJ - 1; k >= 0; --k)
         for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) urow[s.ri[z]].push_back(k);
-    std::vector<StepIn> steps(nJ);
-    for (int32_t t = 0; t < nJ; ++t) {
-        const int32_t i = nJ - 1 - t;
-        const int32_t ne = static_cast<int32_t>(urow[i].size());
-        StepIn& si = steps[t];
-        si.blk_rows = ne + 2;
-        if (ne > 0) si.copies.push_back(copy(kTapeLU, lay.ucrs0[i], ne, 0));
-        si.copies.push_back(copy(kTapeB, i, 1, ne));
-        si.copies.push_back(copy(kTapeLU, lay.lslot[i], 1, ne + 1));
-        si.rec.len_dp = ne;
-        si.rec.lslot = lay.lslot[i];
-        si.rec.brow = i;
-        for (int32_t k : urow[i]) {
-            DepIn di;
-            di.producer = nJ - 1 - k;
-            const int32_t kne = static_cast<int32_t>(urow[k].size());
-            di.ring_ysrc = kne;
-            di.fetch.push_back(copy(kTapeB, k, 1, 0));
-            di.stage_ysrc = 0;
-            di.fetch_rows = 1;
-            si.deps.push_back(std::move(di));
+    int32_t K = 1;
+    Geometry g;
+    std::vector<int32_t> owner = choose_owner(s, cfg, K, g);
+    const std::vector<Phase> phases = make_phases(owner, K, false);
+    std::vector<int32_t> local(nJ, -1);
+    auto make_program = [&](const std::vector<int32_t>& list) {
+        for (size_t t = 0; t < list.size(); ++t) local[list[t]] = int32_t(t);
+        Program pr;
+        pr.steps.resize(list.size());
+        for (size_t t = 0; t < list.size(); ++t) {
+            const int32_t i = list[t];
+            const int32_t ne = static_cast<int32_t>(urow[i].size());
+            StepIn& si = pr.steps[t];
+            si.blk_rows = ne + 2;
+            if (ne > 0) si.copies.push_back(copy(kTapeLU, lay.ucrs0[i], ne, 0));
+            si.copies.push_back(copy(kTapeB, i, 1, ne));
+            si.copies.push_back(copy(kTapeLU, lay.lslot[i], 1, ne + 1));
+            si.rec.len_dp = ne;
+            si.rec.lslot = lay.lslot[i];
+            si.rec.brow = i;
+            for (int32_t k : urow[i]) {
+                DepIn di;
+                di.producer = local[k] >= 0 && local[k] < int32_t(t) ? local[k] : -1;
+                di.ring_ysrc = static_cast<int32_t>(urow[k].size());
+                di.fetch.push_back(copy(kTapeB, k, 1, 0));
+                di.stage_ysrc = 0;
+                di.fetch_rows = 1;
+                si.deps.push_back(std::move(di));
+            }
         }
-    }
-    Walk w = plan(steps, cfg);
-    encode_stream(w, false, cfg);
-    return w;
+        for (int32_t c : list) local[c] = -1;
+        return pr;
+    };
+    WalkSet ws = assemble(cfg, K, g, phases, false, make_program);
+    ws.owner = std::move(owner);
+    return ws;
 }
 
 }  // namespace gbnr

@@ -70,18 +70,22 @@ struct WOp {
 };
 
 struct WalkConfig {
-    int32_t ring_rows = 176;    // XR
-    int32_t stage_rows = 80;    // SR (grown to the largest single fetch if needed)
-    int32_t barriers = 32;      // mbarriers (op i uses barrier i % 32)
-    int32_t prefetch = 8;       // steps an op may run ahead of its consumer
-    int32_t headroom = 2;       // ring residency margin (steps) before an overwrite
-    int32_t page_words = 512;   // program-stream page (grown to the longest record)
-    int32_t pages = 4;          // program-stream pages resident in shared memory
+    int32_t walkers = 4;          // K: warps per tile walking disjoint etree subtrees
+    int32_t smem_budget = 75776;  // bytes per CTA (three tiles per SM)
+    int32_t ring_rows = 0;        // per-walker ring override (0 = from the budget)
+    int32_t stage_rows = 0;       // per-walker staging override (0 = from the budget)
+    int32_t barriers = 32;        // mbarriers per walker (op i uses barrier i % 32)
+    int32_t prefetch = 8;         // steps an op may run ahead of its consumer
+    int32_t headroom = 2;         // ring residency margin (steps) before an overwrite
+    int32_t page_words = 128;     // program-stream page (grown to the longest record)
+    int32_t pages = 4;            // program-stream pages resident per walker
+    double balance = 2.0;         // split subtrees heavier than total / (walkers * balance)
 };
 
-// The device program of a walk: one int32 word stream the warp interprets in
-// order, streamed through shared memory in pages by TMA.  Records (word 0 low
-// 4 bits = type) never straddle a page; kRecPage moves to the next page.
+// The device program of a walk: per walker one int32 word stream the warp
+// interprets in order, streamed through shared memory in pages by TMA.
+// Records (word 0 low 4 bits = type) never straddle a page; kRecPage moves to
+// the next page, kRecSync is a CTA barrier between phases.
 enum : int32_t {
     kRecIssue = 1,  // 1 | ncopy << 4, op, bytes, {tape | rows << 2 | smem << 12, slot} x ncopy
     kRecStep = 2,   // 2 | ndep << 4, ring | len << 16 (fwd) / ring | ne << 16 (bwd), dp, lslot, brow, op
@@ -90,10 +94,12 @@ enum : int32_t {
     kRecEnd = 4,    // 4 | dp << 4, U-CRS tape slots [dp] (fwd)
     kRecPage = 5,
     kRecDone = 6,
+    kRecSync = 7,
 };
 
+// One verified single-walker program (one walker in one phase).
 struct Walk {
-    int32_t ring_rows = 0, stage_rows = 0, barriers = 0, n_steps = 0;
+    int32_t ring_base = 0, ring_rows = 0, stage_rows = 0, barriers = 0, n_steps = 0;
     std::vector<WStep> step;
     std::vector<WDep> dep;
     std::vector<uint16_t> dst;  // forward: destination position per applied L row
@@ -101,12 +107,18 @@ struct Walk {
     std::vector<WCopy> copies;
     std::vector<int32_t> ut;    // forward: U-part CCS slot -> U-CRS tape slot (by step)
     int64_t events = 0, ring_dep_rows = 0, fetched_rows = 0, block_rows = 0;
-    // device program (encode_stream)
-    std::vector<int32_t> stream;
-    int32_t page_words = 0, pages = 0, n_pages = 0;
+};
+
+// All walkers of one tile, all phases: what a kernel launch runs.
+struct WalkSet {
+    int32_t walkers = 1, phases = 1, rows = 0, page_words = 0, pages = 0, barriers = 0;
+    std::vector<Walk> parts;        // [phase * walkers + w]
+    std::vector<int32_t> stream;    // every walker's pages, walker-major
+    std::vector<int32_t> wpage0;    // [walkers + 1] first page of each walker
+    std::vector<int32_t> owner;     // column / row -> phase-0 walker (-1 = the serial top)
+    int64_t steps = 0, events = 0, ring_dep_rows = 0, fetched_rows = 0, n_ops = 0, n_copies = 0;
     size_t smem_bytes() const {
-        return size_t(ring_rows + stage_rows) * 256 + size_t(pages) * page_words * 4 +
-               size_t(barriers + pages) * 8;
+        return size_t(rows) * 256 + size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages) * 8);
     }
 };
 
@@ -120,7 +132,12 @@ struct LuLayout {
 };
 
 LuLayout build_lu_layout(const Symbolic& s);
-Walk build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg);
-Walk build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg);
+// Columns -> phase-0 walker (-1 = top) by splitting the elimination tree into
+// whole subtrees that fit a walker's shared-memory share; {} if dependencies
+// would cross walkers (unsymmetric pivoting), in which case one walker is used.
+std::vector<int32_t> partition_walkers(const Symbolic& s, const WalkConfig& cfg, int32_t ring_w,
+                                       int32_t stage_w);
+WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg);
+WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg);
 
 }  // namespace gbnr

@@ -46,7 +46,8 @@ class Options(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("pivot_tol", C.c_double),
                 ("singular_tol", C.c_double), ("device", C.c_int32), ("ring_rows", C.c_int32),
                 ("profile", C.c_int32), ("stage_rows", C.c_int32),
-                ("prefetch", C.c_int32), ("headroom", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("prefetch", C.c_int32), ("headroom", C.c_int32), ("walkers", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 _lib = None
@@ -253,20 +254,9 @@ class NrPlan:
         d["kernels"] = int(out[19])
         return d
 
-    WALK_KEYS = ("n_steps", "n_deps", "n_dst", "n_ops", "n_ut", "ring_rows", "stage_rows",
-                 "barriers", "events", "ring_dep_rows", "fetched_rows", "smem_bytes",
-                 "stream_words", "page_words", "pages", "n_pages", "n_copies")
-    WALK_DT = {
-        0: np.dtype([(k, np.int32) for k in ("ring", "len_dp", "dep0", "ndep", "lslot", "ut0", "op",
-                                             "brow")]),
-        1: np.dtype([(k, np.int32) for k in ("kpos_fs", "nrows", "src", "ysrc", "u0", "op", "pad0",
-                                             "pad1")]),
-        2: np.dtype(np.uint16),
-        3: np.dtype([(k, np.int32) for k in ("after", "ncopy", "bytes", "c0")]),
-        4: np.dtype(np.int32), 5: np.dtype(np.int32), 6: np.dtype(np.int32), 7: np.dtype(np.int32),
-        8: np.dtype(np.int32),
-        9: np.dtype([(k, np.int32) for k in ("tape_rows", "slot", "smem", "pad")]),
-    }
+    WALK_KEYS = ("steps", "walkers", "phases", "rows", "page_words", "pages", "barriers",
+                 "stream_words", "events", "ring_dep_rows", "fetched_rows", "n_ops", "n_copies",
+                 "smem_bytes", "ring_rows", "stage_rows")
 
     def walk_info(self, which: int) -> dict:
         out = np.zeros(17, np.int64)
@@ -274,16 +264,15 @@ class NrPlan:
         return {k: int(out[i]) for i, k in enumerate(self.WALK_KEYS)}
 
     def walk_export(self, which: int) -> dict:
-        """The static copy program of a tile walk (walk.hpp) as numpy arrays."""
+        """The device program of a tile walk (walk.hpp) as numpy arrays."""
         info = self.walk_info(which)
         st = self.stats()
-        sizes = {0: info["n_steps"], 1: info["n_deps"], 2: info["n_dst"], 3: info["n_ops"],
-                 4: info["n_ut"], 5: st["nnzLU"], 6: st["nJ"], 7: st["nJ"] + 1,
-                 8: info["stream_words"], 9: info["n_copies"]}
-        names = ("step", "dep", "dst", "op", "ut", "tape_of_ccs", "lslot", "ucrs0", "stream", "copies")
+        sizes = (info["stream_words"], info["walkers"] + 1, st["nJ"], st["nnzLU"], st["nJ"],
+                 st["nJ"] + 1)
+        names = ("stream", "wpage0", "owner", "tape_of_ccs", "lslot", "ucrs0")
         d = dict(info=info)
         for part, nm in enumerate(names):
-            a = np.zeros(sizes[part], self.WALK_DT[part])
+            a = np.zeros(sizes[part], np.int32)
             _check(lib().gbnr_walk_export(self.h, int(which), part, a.ctypes.data_as(C.c_void_p)))
             d[nm] = a
         return d

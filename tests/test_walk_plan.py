@@ -82,26 +82,27 @@ def sequential(ex, A, b):
     return lu, y, x
 
 
-REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE = 1, 2, 3, 4, 5, 6
+REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC = 1, 2, 3, 4, 5, 6, 7
 
 
 class Machine:
-    """The kernels' view of a walk: paged program words, smem rows, op barriers."""
+    """One walker as the kernels see it: its paged program words, its op barriers,
+    and the CTA's shared rows R (shared with the other walkers of the tile)."""
 
-    def __init__(self, w, tapes):
+    def __init__(self, w, walker, R, tapes):
         info = w["info"]
-        self.tapes = tapes
-        self.R = np.full((info["ring_rows"] + info["stage_rows"], 32), np.nan)
+        self.tapes, self.R = tapes, R
         self.W, self.NP, self.NB = info["page_words"], info["pages"], info["barriers"]
-        self.gs = w["stream"].astype(np.int64)
-        self.n_pages = info["n_pages"]
-        assert len(self.gs) == self.n_pages * self.W
+        p0, p1 = w["wpage0"][walker], w["wpage0"][walker + 1]
+        self.gs = w["stream"][p0 * self.W:p1 * self.W].astype(np.int64)
+        self.n_pages = p1 - p0
         self.pages = np.zeros((self.NP, self.W), np.int64)
         for p in range(min(self.NP, self.n_pages)):
             self.pages[p] = self.gs[p * self.W:(p + 1) * self.W]
         self.page, self.off = 0, 0
         self.issued = set()
         self.n_issued = 0
+        self.done = False
 
     def rec(self):
         return self.pages[self.page % self.NP, self.off:]
@@ -130,28 +131,49 @@ class Machine:
 
     def wait(self, op):
         assert op in self.issued, f"waits on unissued op {op}"
-        # the barrier of op may be re-armed only after this wait
         assert self.n_issued <= op + self.NB, "barrier re-armed before its wait"
+
+
+def run_phases(w, tapes, step_fn):
+    """Run every walker's program phase by phase (walkers of a phase are
+    independent, so running them one after another is a valid interleaving)."""
+    info = w["info"]
+    R = np.full((info["rows"], 32), np.nan)
+    ms = [Machine(w, k, R, tapes) for k in range(info["walkers"])]
+    while not all(m.done for m in ms):
+        for m in ms:
+            state = {}
+            while True:
+                r = m.rec()
+                t = int(r[0]) & 15
+                if t == REC_ISSUE:
+                    m.off += m.issue(r)
+                elif t == REC_PAGE:
+                    m.next_page()
+                elif t == REC_SYNC:
+                    m.off += 1
+                    break
+                elif t == REC_DONE:
+                    m.done = True
+                    break
+                else:
+                    m.off += step_fn(m, r, t, state)
+    return R
 
 
 def replay_forward(w, A, b_tape, nnz, fs=True):
     LU = np.full((nnz, 32), np.nan)
-    M = Machine(w, {TAPE_A: A, TAPE_LU: LU, TAPE_B: b_tape})
-    assert w["info"]["barriers"] == 32 and w["info"]["pages"] == 4
-    R = M.R
-    x = acc = None
-    ln = dp = lslot = brow = 0
-    while True:
-        r = M.rec()
+    tapes = {TAPE_A: A, TAPE_LU: LU, TAPE_B: b_tape}
+
+    def step(M, r, t, S):
+        R = M.R
         h = int(r[0])
-        t = h & 15
-        if t == REC_ISSUE:
-            M.off += M.issue(r)
-        elif t == REC_DEP:
+        if t == REC_DEP:
             op = (h >> 4) - 1
             kpos_fs, nrows, src, ysrc = int(r[1]), int(r[2]) & 0xFFFF, (int(r[2]) >> 16) & 0xFFFF, int(r[3])
             if op >= 0:
                 M.wait(op)
+            x = S["x"]
             if nrows > 0:
                 mult = x[kpos_fs & 0xFFFF].copy()
                 for q in range(nrows):
@@ -160,80 +182,69 @@ def replay_forward(w, A, b_tape, nnz, fs=True):
                     x[d] = x[d] - mult * R[src + q]
             fsp = (kpos_fs >> 16) & 0xFFFF
             if fs and fsp != 0xFFFF:
-                acc = acc - R[src + fsp] * R[ysrc]
-            M.off += 4 + (nrows + 1) // 2
-        elif t == REC_STEP:
+                S["acc"] = S["acc"] - R[src + fsp] * R[ysrc]
+            return 4 + (nrows + 1) // 2
+        if t == REC_STEP:
             ring, ln = int(r[1]) & 0xFFFF, int(r[1]) >> 16
-            dp, lslot, brow, op = int(r[2]), int(r[3]), int(r[4]), int(r[5])
-            M.off += 6
-            M.wait(op)
-            x = R[ring:ring + ln]
-            acc = R[ring + ln].copy() if fs else None
-        elif t == REC_END:
-            piv = x[dp].copy()
-            inv = 1.0 / piv
-            LU[lslot] = piv
-            for z in range(dp + 1, ln):
-                x[z] = x[z] * inv
-                LU[lslot + z - dp] = x[z]
-            for z in range(dp):
-                LU[int(r[1 + z])] = x[z]
-            if fs:
-                R[ring + ln] = acc
-                b_tape[brow] = acc
-            M.off += 1 + dp
-        elif t == REC_PAGE:
-            M.next_page()
-        else:
-            assert t == REC_DONE
-            break
-    assert M.n_issued == w["info"]["n_ops"]
+            S.update(ring=ring, ln=ln, dp=int(r[2]), lslot=int(r[3]), brow=int(r[4]))
+            M.wait(int(r[5]))
+            S["x"] = R[ring:ring + ln]
+            S["acc"] = R[ring + ln].copy() if fs else None
+            return 6
+        assert t == REC_END
+        x, dp, ln, lslot = S["x"], S["dp"], S["ln"], S["lslot"]
+        piv = x[dp].copy()
+        inv = 1.0 / piv
+        LU[lslot] = piv
+        for z in range(dp + 1, ln):
+            x[z] = x[z] * inv
+            LU[lslot + z - dp] = x[z]
+        for z in range(dp):
+            LU[int(r[1 + z])] = x[z]
+        if fs:
+            R[S["ring"] + ln] = S["acc"]
+            b_tape[S["brow"]] = S["acc"]
+        return 1 + dp
+
+    run_phases(w, tapes, step)
     return LU
 
 
 def replay_backward(w, LU, b_tape):
-    M = Machine(w, {TAPE_A: None, TAPE_LU: LU, TAPE_B: b_tape})
-    R = M.R
-    blk = acc = None
-    ne = e = brow = ring = 0
-    while True:
-        r = M.rec()
+    tapes = {TAPE_A: None, TAPE_LU: LU, TAPE_B: b_tape}
+
+    def step(M, r, t, S):
+        R = M.R
         h = int(r[0])
-        t = h & 15
-        if t == REC_ISSUE:
-            M.off += M.issue(r)
-        elif t == REC_DEP:
+        if t == REC_DEP:
             op = (h >> 4) - 1
             if op >= 0:
                 M.wait(op)
-            acc = acc - R[ring + e] * R[int(r[1])]
-            e += 1
-            M.off += 2
-        elif t == REC_STEP:
+            S["acc"] = S["acc"] - R[S["ring"] + S["e"]] * R[int(r[1])]
+            S["e"] += 1
+            return 2
+        if t == REC_STEP:
             ring, ne = int(r[1]) & 0xFFFF, int(r[1]) >> 16
-            brow, op = int(r[4]), int(r[5])
-            M.off += 6
-            M.wait(op)
-            acc = R[ring + ne].copy()
-            e = 0
-        elif t == REC_END:
-            xi = acc / R[ring + ne + 1]
-            R[ring + ne] = xi
-            b_tape[brow] = xi
-            M.off += 1
-        elif t == REC_PAGE:
-            M.next_page()
-        else:
-            assert t == REC_DONE
-            break
-    assert M.n_issued == w["info"]["n_ops"]
+            S.update(ring=ring, ne=ne, brow=int(r[4]), e=0)
+            M.wait(int(r[5]))
+            S["acc"] = R[ring + ne].copy()
+            return 6
+        assert t == REC_END
+        ring, ne = S["ring"], S["ne"]
+        xi = S["acc"] / R[ring + ne + 1]
+        R[ring + ne] = xi
+        b_tape[S["brow"]] = xi
+        return 1
+
+    run_phases(w, tapes, step)
 
 
 @pytest.mark.parametrize("name,opts", [("case14", {}), ("synth118", {}), ("synth300", {}),
-                                       ("synth300", dict(ring_rows=40, stage_rows=24, prefetch=3)),
-                                       ("synth300", dict(ring_rows=400, stage_rows=200, prefetch=20)),
-                                       ("synth2383", dict(ring_rows=64, stage_rows=40, prefetch=5,
-                                                          headroom=1))])
+                                       ("synth300", dict(walkers=1)),
+                                       ("synth300", dict(walkers=8)),
+                                       ("synth300", dict(walkers=2, ring_rows=40, stage_rows=24, prefetch=3)),
+                                       ("synth300", dict(walkers=1, ring_rows=200, stage_rows=80, prefetch=20)),
+                                       ("synth2383", dict(walkers=3, prefetch=5, headroom=1))])
 def test_walk_replay_bitwise(name, opts):
     gc = load_case(util.case_path(name))
     plan = S.NrPlan.from_case(gc, device=-1, **opts)
@@ -254,18 +265,20 @@ def test_walk_replay_bitwise(name, opts):
 
 
 def test_walk_stats_and_layout():
-    gc = load_case(util.case_path("synth300"))
+    gc = load_case(util.case_path("synth2383"))
     plan = S.NrPlan.from_case(gc, device=-1)
     st = plan.stats()
     for which in (0, 1, 2):
         info = plan.walk_info(which)
-        assert info["n_steps"] == st["nJ"]
-        assert info["smem_bytes"] + 1024 <= 228 * 1024 // 3  # three tile walkers per SM
+        assert info["steps"] == st["nJ"]
+        assert info["walkers"] == 4 and info["phases"] == 2
+        assert info["smem_bytes"] + 1024 <= 228 * 1024 // 3  # three tiles per SM
     w = plan.walk_export(0)
     toc = w["tape_of_ccs"]
     assert sorted(toc.tolist()) == list(range(st["nnzLU"]))  # a permutation of the slots
-    # LU-only walk fetches no right-hand side rows
-    wl = plan.walk_export(1)
-    assert not ((wl["copies"]["tape_rows"] & 0xFF) == TAPE_B).any()
-    assert wl["op"]["ncopy"].sum() == len(wl["copies"])
+    own = w["owner"]
+    assert (own >= -1).all() and (own < 4).all()
+    # most columns are walked in parallel subtrees; the serial top is small
+    assert (own >= 0).mean() > 0.8
+    np.testing.assert_array_equal(plan.walk_export(2)["owner"], own)
     plan.close()
