@@ -285,15 +285,18 @@ def main():
     h2d = 2 * n * T * 8 + 2 * n * 8
     d2h = 2 * n * T * 8 + T * (4 + 1 + 4 + 8)
 
-    # roofline of the dominant kernel (batched LU refactorization)
-    b_lu_task = 8 * (2 * st["nnzLU"] + st["D"])
+    # roofline of the dominant kernel: the LU walk (frozen-pattern G-P
+    # refactorization fused with the forward substitution), DESIGN.md §5:
+    # 8(2 zLU + D) bytes of Alg. 2 + 16 nJ of right-hand side in / y out
+    b_lu_task = 8 * (2 * st["nnzLU"] + st["D"]) + 16 * st["nJ"]
     peak, peak_kind = measured_peaks()
     achieved = b_lu_task * lu_tasks / (lu_ms / 1e3) / 1e9 if lu_ms > 0 else None
     tr = lu_traffic_per_task()
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
             "traffic": tr * (lu_tasks / max(lu_launches, 1)) if tr else None,
-            "kernel": "lu_kernel (batched frozen-pattern G-P refactorization)",
+            "kernel": "lu_walk_kernel<FS> (batched frozen-pattern G-P refactorization + forward "
+                      "substitution, tile walks)",
             "algorithmic_bytes_per_task": b_lu_task, "peak_kind": peak_kind,
             "lu_ms_per_launch": lu_ms / max(lu_launches, 1),
             "lu_share_of_step": lu_ms / dev_ms if dev_ms else None}

@@ -462,9 +462,19 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
         } else if (type == kRecSync) {
+            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                printf("[walk] tile %d warp %d reached sync at %llu ns\n", tile, warp, t);
+            }
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             P.cur += 1;
         } else {
+            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                printf("[walk] tile %d warp %d done at %llu ns\n", tile, warp, t);
+            }
             break;
         }
     }
@@ -513,9 +523,19 @@ __global__ void __launch_bounds__(256) bs_walk_kernel(DevView v, WalkView w) {
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
         } else if (type == kRecSync) {
+            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                printf("[walk] tile %d warp %d reached sync at %llu ns\n", tile, warp, t);
+            }
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             P.cur += 1;
         } else {
+            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                printf("[walk] tile %d warp %d done at %llu ns\n", tile, warp, t);
+            }
             break;
         }
     }

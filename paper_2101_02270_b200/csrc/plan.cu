@@ -387,7 +387,7 @@ void gbnr_default_options(gbnr_options* o) {
     o->stage_rows = 0;
     o->prefetch = 8;
     o->headroom = 2;
-    o->walkers = 4;
+    o->walkers = 8;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }

@@ -489,45 +489,47 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
     return ws;
 }
 
-// Phase lists: forward = bins in parallel, then the top by walker 0;
-// backward = the top first (descending), then the bins (descending).
-std::vector<Phase> make_phases(const std::vector<int32_t>& owner, int32_t K, bool forward) {
-    const int32_t n = static_cast<int32_t>(owner.size());
-    Phase bins, top;
-    bins.lists.resize(K);
-    top.lists.resize(K);
+// Phase lists from the level / bin assignment: forward = level 0 (most
+// walkers) first, backward = the last level (the serial top) first.
+std::vector<Phase> make_phases(const std::vector<int32_t>& level, const std::vector<int32_t>& bin, int32_t K,
+                               int32_t levels, bool forward) {
+    const int32_t n = static_cast<int32_t>(level.size());
+    std::vector<Phase> by_level(levels);
+    for (auto& p : by_level) p.lists.resize(K);
     for (int32_t i = 0; i < n; ++i) {
         const int32_t c = forward ? i : n - 1 - i;
-        if (owner[c] >= 0)
-            bins.lists[owner[c]].push_back(c);
-        else
-            top.lists[0].push_back(c);
+        by_level[level[c]].lists[bin[c]].push_back(c);
     }
     std::vector<Phase> ph;
-    const bool any_top = !top.lists[0].empty();
-    if (forward) {
-        ph.push_back(std::move(bins));
-        if (any_top) ph.push_back(std::move(top));
-    } else {
-        if (any_top) ph.push_back(std::move(top));
-        ph.push_back(std::move(bins));
+    for (int32_t l = 0; l < levels; ++l) {
+        Phase& p = by_level[forward ? l : levels - 1 - l];
+        bool any = false;
+        for (const auto& x : p.lists) any |= !x.empty();
+        if (any) ph.push_back(std::move(p));
     }
     return ph;
 }
 
-// Walker count and column ownership for a launch (falls back to one walker).
-std::vector<int32_t> choose_owner(const Symbolic& s, const WalkConfig& cfg, int32_t& K, Geometry& g) {
-    K = std::max(1, std::min(cfg.walkers, 8));
+struct Schedule {
+    int32_t K = 1, levels = 1;
+    std::vector<int32_t> lvl_walkers, level, bin;
+};
+
+// Walkers per level halve until one walks the remaining top alone.
+Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g) {
+    Schedule sc;
+    sc.K = std::max(1, std::min(cfg.walkers, 8));
     for (;;) {
-        g = geometry(s, cfg, K);
-        int32_t ring = 0, stage = 0;
-        split_share(cfg, g.rows / K, ring, stage);
-        WalkConfig c = cfg;
-        c.walkers = K;
-        std::vector<int32_t> owner = partition_walkers(s, c, ring, stage);
-        if (!owner.empty()) return owner;
-        if (K == 1) return std::vector<int32_t>(s.nJ, 0);
-        K = 1;  // dependencies cross subtrees: one walker
+        g = geometry(s, cfg, sc.K);
+        sc.lvl_walkers.clear();
+        for (int32_t k = sc.K; k > 1; k /= 2) sc.lvl_walkers.push_back(k);
+        sc.lvl_walkers.push_back(1);
+        sc.levels = static_cast<int32_t>(sc.lvl_walkers.size());
+        std::vector<int32_t> ring(sc.levels), stage(sc.levels);
+        for (int32_t l = 0; l < sc.levels; ++l) split_share(cfg, g.rows / sc.lvl_walkers[l], ring[l], stage[l]);
+        if (partition_levels(s, cfg, sc.lvl_walkers, ring, stage, sc.level, sc.bin)) return sc;
+        if (sc.K == 1) throw Error(3, "walk schedule failed with one walker");
+        sc.K = 1;  // dependencies cross subtrees: one walker
     }
 }
 
@@ -562,80 +564,102 @@ LuLayout build_lu_layout(const Symbolic& s) {
     return lay;
 }
 
-// Subtree-to-walker mapping (proportional mapping on the elimination tree):
-// peel the heaviest subtrees (and any subtree holding a column too big for a
-// walker's share) into the serial "top", then deal the remaining whole
-// subtrees to the walkers, heaviest first onto the lightest walker.
-std::vector<int32_t> partition_walkers(const Symbolic& s, const WalkConfig& cfg, int32_t ring_w,
-                                       int32_t stage_w) {
-    const int32_t nJ = s.nJ, K = cfg.walkers;
-    std::vector<int32_t> owner(nJ, -1);
-    if (K <= 1 || nJ == 0) {
-        std::fill(owner.begin(), owner.end(), 0);
-        return owner;
-    }
+// Subtree-to-walker mapping (proportional mapping on the elimination tree),
+// level by level: at level l, peel the heaviest subtrees of the still
+// unassigned (top) forest -- and any subtree holding a column too big for a
+// walker's share at that level -- back into the top, then deal the remaining
+// whole subtrees to that level's walkers, heaviest first onto the lightest.
+// The last level (one walker) takes whatever is left.  Returns false if some
+// dependency would cross walkers (possible only with unsymmetric pivoting).
+bool partition_levels(const Symbolic& s, const WalkConfig& cfg, const std::vector<int32_t>& lvl_walkers,
+                      const std::vector<int32_t>& ring_w, const std::vector<int32_t>& stage_w,
+                      std::vector<int32_t>& level, std::vector<int32_t>& bin) {
+    const int32_t nJ = s.nJ, L = static_cast<int32_t>(lvl_walkers.size());
+    level.assign(nJ, -1);
+    bin.assign(nJ, 0);
     const std::vector<int32_t> parent = etree_parent(s);
-    std::vector<double> work(nJ), sub(nJ);
-    std::vector<int32_t> smax_blk(nJ), smax_fetch(nJ);
+    std::vector<double> work(nJ);
+    std::vector<int32_t> blk(nJ), fetch(nJ);
     std::vector<std::vector<int32_t>> children(nJ);
     for (int32_t k = 0; k < nJ; ++k) {
+        if (parent[k] >= 0 && parent[k] <= k) return false;
         double wk = 60.0 + (s.cp[k + 1] - s.cp[k]);
         for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) {
             const int32_t j = s.ri[z];
             wk += 12.0 + (s.cp[j + 1] - s.dpos[j] - 1);
         }
-        work[k] = sub[k] = wk;
-        smax_blk[k] = s.cp[k + 1] - s.cp[k] + 1;
-        smax_fetch[k] = s.cp[k + 1] - s.dpos[k];
+        work[k] = wk;
+        blk[k] = s.cp[k + 1] - s.cp[k] + 1;
+        fetch[k] = s.cp[k + 1] - s.dpos[k];
         if (parent[k] >= 0) children[parent[k]].push_back(k);
     }
-    for (int32_t k = 0; k < nJ; ++k)  // parent > k, so children are final first
-        if (parent[k] >= 0) {
-            if (parent[k] <= k) return {};
-            sub[parent[k]] += sub[k];
-            smax_blk[parent[k]] = std::max(smax_blk[parent[k]], smax_blk[k]);
-            smax_fetch[parent[k]] = std::max(smax_fetch[parent[k]], smax_fetch[k]);
+    for (int32_t l = 0; l < L; ++l) {
+        const int32_t K = lvl_walkers[l];
+        if (l == L - 1 || K == 1) {
+            for (int32_t k = 0; k < nJ; ++k)
+                if (level[k] < 0) level[k] = l, bin[k] = 0;
+            break;
         }
-    double total = 0.0;
-    for (double x : work) total += x;
-    const double thr = total / (K * cfg.balance);
-    std::priority_queue<std::pair<double, int32_t>> heap;
-    for (int32_t k = 0; k < nJ; ++k)
-        if (parent[k] < 0) heap.emplace(sub[k], k);
-    std::vector<std::pair<double, int32_t>> keep;
-    while (!heap.empty()) {
-        const auto [wt, r] = heap.top();
-        heap.pop();
-        if (wt > thr || smax_blk[r] > ring_w || smax_fetch[r] > stage_w) {
-            for (int32_t c : children[r]) heap.emplace(sub[c], c);  // r stays in the top
-        } else {
-            keep.emplace_back(wt, r);
+        // subtree sums over the unassigned forest (parent > child: one pass)
+        std::vector<double> sub(nJ, 0.0);
+        std::vector<int32_t> smax_blk(nJ, 0), smax_fetch(nJ, 0);
+        double total = 0.0;
+        for (int32_t k = 0; k < nJ; ++k) {
+            if (level[k] >= 0) continue;
+            sub[k] += work[k];
+            smax_blk[k] = std::max(smax_blk[k], blk[k]);
+            smax_fetch[k] = std::max(smax_fetch[k], fetch[k]);
+            total += work[k];
+            const int32_t p = parent[k];
+            if (p >= 0 && level[p] < 0) {
+                sub[p] += sub[k];
+                smax_blk[p] = std::max(smax_blk[p], smax_blk[k]);
+                smax_fetch[p] = std::max(smax_fetch[p], smax_fetch[k]);
+            }
+        }
+        const double thr = total / (K * cfg.balance);
+        std::priority_queue<std::pair<double, int32_t>> heap;
+        for (int32_t k = 0; k < nJ; ++k)
+            if (level[k] < 0 && (parent[k] < 0 || level[parent[k]] >= 0)) heap.emplace(sub[k], k);
+        std::vector<std::pair<double, int32_t>> keep;
+        while (!heap.empty()) {
+            const auto [wt, r] = heap.top();
+            heap.pop();
+            if (wt > thr || smax_blk[r] > ring_w[l] || smax_fetch[r] > stage_w[l]) {
+                for (int32_t c : children[r])
+                    if (level[c] < 0) heap.emplace(sub[c], c);  // r stays in the top
+            } else {
+                keep.emplace_back(wt, r);
+            }
+        }
+        std::sort(keep.begin(), keep.end(), std::greater<>());
+        std::vector<double> load(K, 0.0);
+        for (const auto& [wt, r] : keep) {
+            const int32_t b = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
+            load[b] += wt;
+            std::vector<int32_t> st{r};
+            while (!st.empty()) {
+                const int32_t u = st.back();
+                st.pop_back();
+                level[u] = l;
+                bin[u] = b;
+                for (int32_t c : children[u])
+                    if (level[c] < 0) st.push_back(c);
+            }
         }
     }
-    std::sort(keep.begin(), keep.end(), std::greater<>());
-    std::vector<double> load(K, 0.0);
-    for (const auto& [wt, r] : keep) {
-        const int32_t b = int32_t(std::min_element(load.begin(), load.end()) - load.begin());
-        load[b] += wt;
-        std::vector<int32_t> st{r};
-        while (!st.empty()) {
-            const int32_t u = st.back();
-            st.pop_back();
-            owner[u] = b;
-            for (int32_t c : children[u]) st.push_back(c);
-        }
-    }
-    // every dependency must stay inside its walker: a column of a subtree may
-    // only touch columns of the same subtree, or later top columns (which the
-    // forward walk runs after the subtrees and the backward walk before them)
-    for (int32_t j = 0; j < nJ; ++j) {
-        if (owner[j] < 0) continue;
+    // every dependency must be finished before its consumer runs: a column's U
+    // rows (its dependencies) lie in an earlier level or in the same (level,
+    // bin); its L rows (its consumers) in a later level or the same (level, bin)
+    for (int32_t j = 0; j < nJ; ++j)
         for (int32_t z = s.cp[j]; z < s.cp[j + 1]; ++z) {
             const int32_t k = s.ri[z];
-            if (k != j && owner[k] != owner[j] && !(k > j && owner[k] < 0)) return {};
+            if (k == j) continue;
+            const bool same = level[k] == level[j] && bin[k] == bin[j];
+            if (k < j && !(same || level[k] < level[j])) return false;
+            if (k > j && !(same || level[k] > level[j])) return false;
         }
-    }
-    return owner;
+    return true;
 }
 
 // Forward walk: column m of Alg. 2 (+ row m of the forward substitution).
@@ -648,10 +672,9 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
     if (with_fs)
         for (int32_t k = 0; k < nJ; ++k)
             for (int32_t z = s.dpos[k] + 1; z < s.cp[k + 1]; ++z) lrow[s.ri[z]].push_back(k);
-    int32_t K = 1;
     Geometry g;
-    std::vector<int32_t> owner = choose_owner(s, cfg, K, g);
-    const std::vector<Phase> phases = make_phases(owner, K, true);
+    const Schedule sc = choose_schedule(s, cfg, g);
+    const std::vector<Phase> phases = make_phases(sc.level, sc.bin, sc.K, sc.levels, true);
     std::vector<int32_t> posmap(nJ, -1), local(nJ, -1);
     auto make_program = [&](const std::vector<int32_t>& list) {
         for (size_t i = 0; i < list.size(); ++i) local[list[i]] = int32_t(i);
@@ -716,8 +739,9 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
         for (int32_t c : list) local[c] = -1;
         return pr;
     };
-    WalkSet ws = assemble(cfg, K, g, phases, true, make_program);
-    ws.owner = std::move(owner);
+    WalkSet ws = assemble(cfg, sc.K, g, phases, true, make_program);
+    ws.owner.resize(nJ);
+    for (int32_t c = 0; c < nJ; ++c) ws.owner[c] = sc.level[c] * 16 + sc.bin[c];
     return ws;
 }
 
@@ -729,10 +753,9 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
     std::vector<std::vector<int32_t>> urow(nJ);  // k descending
     for (int32_t k = nJ - 1; k >= 0; --k)
         for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) urow[s.ri[z]].push_back(k);
-    int32_t K = 1;
     Geometry g;
-    std::vector<int32_t> owner = choose_owner(s, cfg, K, g);
-    const std::vector<Phase> phases = make_phases(owner, K, false);
+    const Schedule sc = choose_schedule(s, cfg, g);
+    const std::vector<Phase> phases = make_phases(sc.level, sc.bin, sc.K, sc.levels, false);
     std::vector<int32_t> local(nJ, -1);
     auto make_program = [&](const std::vector<int32_t>& list) {
         for (size_t t = 0; t < list.size(); ++t) local[list[t]] = int32_t(t);
@@ -762,8 +785,9 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
         for (int32_t c : list) local[c] = -1;
         return pr;
     };
-    WalkSet ws = assemble(cfg, K, g, phases, false, make_program);
-    ws.owner = std::move(owner);
+    WalkSet ws = assemble(cfg, sc.K, g, phases, false, make_program);
+    ws.owner.resize(nJ);
+    for (int32_t c = 0; c < nJ; ++c) ws.owner[c] = sc.level[c] * 16 + sc.bin[c];
     return ws;
 }
 

@@ -70,7 +70,7 @@ struct WOp {
 };
 
 struct WalkConfig {
-    int32_t walkers = 4;          // K: warps per tile walking disjoint etree subtrees
+    int32_t walkers = 8;          // K: warps per tile walking disjoint etree subtrees
     int32_t smem_budget = 75776;  // bytes per CTA (three tiles per SM)
     int32_t ring_rows = 0;        // per-walker ring override (0 = from the budget)
     int32_t stage_rows = 0;       // per-walker staging override (0 = from the budget)
@@ -115,7 +115,7 @@ struct WalkSet {
     std::vector<Walk> parts;        // [phase * walkers + w]
     std::vector<int32_t> stream;    // every walker's pages, walker-major
     std::vector<int32_t> wpage0;    // [walkers + 1] first page of each walker
-    std::vector<int32_t> owner;     // column / row -> phase-0 walker (-1 = the serial top)
+    std::vector<int32_t> owner;     // column / row -> level * 16 + walker
     int64_t steps = 0, events = 0, ring_dep_rows = 0, fetched_rows = 0, n_ops = 0, n_copies = 0;
     size_t smem_bytes() const {
         return size_t(rows) * 256 + size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages) * 8);
@@ -132,11 +132,13 @@ struct LuLayout {
 };
 
 LuLayout build_lu_layout(const Symbolic& s);
-// Columns -> phase-0 walker (-1 = top) by splitting the elimination tree into
-// whole subtrees that fit a walker's shared-memory share; {} if dependencies
-// would cross walkers (unsymmetric pivoting), in which case one walker is used.
-std::vector<int32_t> partition_walkers(const Symbolic& s, const WalkConfig& cfg, int32_t ring_w,
-                                       int32_t stage_w);
+// Columns -> (level, walker) by splitting the elimination tree into whole
+// subtrees that fit a walker's shared-memory share, level by level with
+// halving walker counts; false if dependencies would cross walkers
+// (unsymmetric pivoting), in which case one walker is used.
+bool partition_levels(const Symbolic& s, const WalkConfig& cfg, const std::vector<int32_t>& lvl_walkers,
+                      const std::vector<int32_t>& ring_w, const std::vector<int32_t>& stage_w,
+                      std::vector<int32_t>& level, std::vector<int32_t>& bin);
 WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg);
 WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg);
 
