@@ -247,7 +247,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // The walk's program is a word stream (walk.hpp kRec*) paged through shared
 // memory by TMA; every lane reads the same words (smem broadcast).
 constexpr int kWalkBars = 32;   // op i completes on barrier i % 32
-constexpr int kWalkPages = 4;   // resident program pages
+constexpr int kWalkPages = 2;   // resident program pages
 
 struct Prog {
     double* R;                  // smem rows [ring_rows + stage_rows][32]
@@ -599,6 +599,13 @@ void configure_kernels() {
     cudaFuncSetAttribute(lu_walk_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(lu_walk_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(bs_walk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+int walk_ctas_per_sm(size_t smem, int threads) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lu_walk_kernel<true>, threads, smem) != cudaSuccess)
+        return 0;
+    return n;
 }
 
 void launch_init(const DevView& v, cudaStream_t st) {

@@ -51,6 +51,7 @@ struct WalkView {
 
 size_t walk_smem_bytes(const WalkView& w);
 void configure_kernels();
+int walk_ctas_per_sm(size_t smem, int threads);  // resident LU-walk CTAs per SM
 void launch_init(const DevView& v, cudaStream_t st);
 void launch_npm(const DevView& v, cudaStream_t st);  // NPM + convergence + iteration bump
 void launch_jacobian(const DevView& v, cudaStream_t st);

@@ -143,7 +143,7 @@ struct gbnr_plan {
         x.rows = w.rows;
         if (w.walkers < 1 || w.walkers > 8) throw Error(GBNR_ECONFIG, "1..8 walkers per tile");
         for (int32_t i = 0; i <= w.walkers; ++i) x.wpage0[i] = w.wpage0[i];
-        if (w.barriers != 32 || w.pages != 4) throw Error(GBNR_ECONFIG, "walk kernels use 32 barriers, 4 pages");
+        if (w.barriers != 32 || w.pages != 2) throw Error(GBNR_ECONFIG, "walk kernels use 32 barriers, 2 pages");
         if (gbnr::walk_smem_bytes(x) != w.smem_bytes()) throw Error(GBNR_ECONFIG, "walk smem layout mismatch");
         if (gbnr::walk_smem_bytes(x) > 227 * 1024)
             throw Error(GBNR_ECONFIG, "walk needs more shared memory than a B200 CTA has");
@@ -447,13 +447,27 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (p->opt.prefetch) wc.prefetch = p->opt.prefetch;
         if (p->opt.headroom) wc.headroom = p->opt.headroom;
         if (p->opt.walkers) wc.walkers = p->opt.walkers;
-        p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
-        p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
-        p->wb = gbnr::build_backward_walk(p->sym, p->lay, wc);
+        if (const char* e = std::getenv("GBNR_STAGE_FRAC")) wc.stage_frac = std::atof(e);
+        if (const char* e = std::getenv("GBNR_SMEM_BUDGET")) wc.smem_budget = std::atoi(e);
+        if (const char* e = std::getenv("GBNR_BALANCE")) wc.balance = std::atof(e);
+        auto build_walks = [&] {
+            p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
+            p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
+            p->wb = gbnr::build_backward_walk(p->sym, p->lay, wc);
+        };
+        build_walks();
         if (p->opt.device >= 0) {
             int ndev = 0;
             CK(cudaGetDeviceCount(&ndev));
             if (p->opt.device >= ndev) throw Error(GBNR_ECUDA, "CUDA device ordinal out of range");
+            CK(cudaSetDevice(p->opt.device));
+            gbnr::configure_kernels();
+            // three tiles per SM: shrink the shared-memory budget until the
+            // device really co-schedules three walk CTAs
+            while (gbnr::walk_ctas_per_sm(p->wf.smem_bytes(), 32 * p->wf.walkers) < 3 && wc.smem_budget > 65536) {
+                wc.smem_budget -= 1024;
+                build_walks();
+            }
             p->on_device = true;
             p->upload_structure();
             p->set_ybus(y_re, y_im);

@@ -422,7 +422,7 @@ Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
 
 // Per-walker ring / staging split of a share of rows.
 void split_share(const WalkConfig& cfg, int32_t share, int32_t& ring, int32_t& stage) {
-    stage = cfg.stage_rows ? cfg.stage_rows : share * 3 / 10;
+    stage = cfg.stage_rows ? cfg.stage_rows : int32_t(share * cfg.stage_frac);
     ring = cfg.ring_rows ? cfg.ring_rows : share - stage;
 }
 

@@ -71,15 +71,16 @@ struct WOp {
 
 struct WalkConfig {
     int32_t walkers = 8;          // K: warps per tile walking disjoint etree subtrees
-    int32_t smem_budget = 75776;  // bytes per CTA (three tiles per SM)
+    int32_t smem_budget = 76800;  // bytes per CTA: three tiles per SM (228 KB - 3 x 1 KB reserved)
     int32_t ring_rows = 0;        // per-walker ring override (0 = from the budget)
     int32_t stage_rows = 0;       // per-walker staging override (0 = from the budget)
     int32_t barriers = 32;        // mbarriers per walker (op i uses barrier i % 32)
     int32_t prefetch = 8;         // steps an op may run ahead of its consumer
     int32_t headroom = 2;         // ring residency margin (steps) before an overwrite
     int32_t page_words = 128;     // program-stream page (grown to the longest record)
-    int32_t pages = 4;            // program-stream pages resident per walker
+    int32_t pages = 2;            // program-stream pages resident per walker
     double balance = 2.0;         // split subtrees heavier than total / (walkers * balance)
+    double stage_frac = 0.4;      // staging share of a walker's rows
 };
 
 // The device program of a walk: per walker one int32 word stream the warp

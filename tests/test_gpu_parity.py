@@ -117,7 +117,7 @@ def test_repeat_solve_is_deterministic():
     np.testing.assert_array_equal(a.iterations, b.iterations)
 
 
-@pytest.mark.parametrize("opts", [dict(walkers=4, ring_rows=40, stage_rows=24, prefetch=3),
+@pytest.mark.parametrize("opts", [dict(walkers=4, ring_rows=36, stage_rows=24, prefetch=3),
                                   dict(walkers=1, ring_rows=64, stage_rows=40, prefetch=1, headroom=1),
                                   dict(walkers=1),
                                   dict(walkers=8, prefetch=16, headroom=4)])
