@@ -256,9 +256,22 @@ struct Prog {
     unsigned long long* pbar;   // page barriers [kWalkPages]
     const int32_t* gs;          // stream in global memory
     const int32_t* cur;         // next record
-    const char* tape[3];        // this tile's A, LU and b tapes (256 B rows)
+    const char *tA, *tLU, *tB;  // this tile's A, LU and b tapes (256 B rows)
     int W, n_pages, page;
 };
+
+// Debug timeline (GBNR_DBG & 4): kernel start (-1), phase barrier (0), end (1).
+__device__ __noinline__ void walk_trace_print(int tile, int warp, int what) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    printf("[walk] tile %d warp %d %s at %llu ns\n", tile, warp,
+           what < 0 ? "start" : (what == 0 ? "reached sync" : "done"), t);
+}
+__device__ __forceinline__ void walk_trace(const DevView& v, int tile, int warp, int lane, int what) {
+#ifdef GBNR_TRACE  // make GBNR_TRACE=1: compiled out of production builds (no call frame)
+    if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) walk_trace_print(tile, warp, what);
+#endif
+}
 
 // Shared memory of a walk CTA: [rows][32] doubles shared by the walkers (each
 // phase's plan gives every walker a disjoint share), then per walker its
@@ -277,9 +290,9 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.n_pages = w.wpage0[warp + 1] - w.wpage0[warp];
     P.page = 0;
     P.cur = P.pg;
-    P.tape[kTapeA] = reinterpret_cast<const char*>(v.A + size_t(tile) * v.nnzLU * kTile);
-    P.tape[kTapeLU] = reinterpret_cast<const char*>(v.LU + size_t(tile) * v.nnzLU * kTile);
-    P.tape[kTapeB] = reinterpret_cast<const char*>(v.b + size_t(tile) * v.nJ * kTile);
+    P.tA = reinterpret_cast<const char*>(v.A + size_t(tile) * v.nnzLU * kTile);
+    P.tLU = reinterpret_cast<const char*>(v.LU + size_t(tile) * v.nnzLU * kTile);
+    P.tB = reinterpret_cast<const char*>(v.b + size_t(tile) * v.nJ * kTile);
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
     if (lane == 0) {
@@ -323,7 +336,8 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 rbase + smem * (kTile * 8u)),
-            "l"(P.tape[c & 3] + size_t(slot) * (kTile * 8)), "r"(rows * (kTile * 8u)), "r"(ubar)
+            "l"(((c & 3) == kTapeA ? P.tA : (c & 3) == kTapeLU ? P.tLU : P.tB) + size_t(slot) * (kTile * 8)),
+            "r"(rows * (kTile * 8u)), "r"(ubar)
             : "memory");
     }
     return 3 + 2 * ncopy;
@@ -339,6 +353,7 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
+    walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
     double* lu_t = v.LU + size_t(tile) * v.nnzLU * kTile + lane;
     double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
@@ -462,19 +477,11 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
         } else if (type == kRecSync) {
-            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                printf("[walk] tile %d warp %d reached sync at %llu ns\n", tile, warp, t);
-            }
+            walk_trace(v, tile, warp, lane, 0);
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             P.cur += 1;
         } else {
-            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                printf("[walk] tile %d warp %d done at %llu ns\n", tile, warp, t);
-            }
+            walk_trace(v, tile, warp, lane, 1);
             break;
         }
     }
@@ -486,6 +493,7 @@ __global__ void __launch_bounds__(256) bs_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
+    walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
     double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
     double* blk = P.R;
@@ -523,19 +531,11 @@ __global__ void __launch_bounds__(256) bs_walk_kernel(DevView v, WalkView w) {
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
         } else if (type == kRecSync) {
-            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                printf("[walk] tile %d warp %d reached sync at %llu ns\n", tile, warp, t);
-            }
+            walk_trace(v, tile, warp, lane, 0);
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             P.cur += 1;
         } else {
-            if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                printf("[walk] tile %d warp %d done at %llu ns\n", tile, warp, t);
-            }
+            walk_trace(v, tile, warp, lane, 1);
             break;
         }
     }

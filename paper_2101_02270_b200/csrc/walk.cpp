@@ -516,7 +516,7 @@ struct Schedule {
 };
 
 // Walkers per level halve until one walks the remaining top alone.
-Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g) {
+Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g, bool backward) {
     Schedule sc;
     sc.K = std::max(1, std::min(cfg.walkers, 8));
     for (;;) {
@@ -527,7 +527,7 @@ Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g) 
         sc.levels = static_cast<int32_t>(sc.lvl_walkers.size());
         std::vector<int32_t> ring(sc.levels), stage(sc.levels);
         for (int32_t l = 0; l < sc.levels; ++l) split_share(cfg, g.rows / sc.lvl_walkers[l], ring[l], stage[l]);
-        if (partition_levels(s, cfg, sc.lvl_walkers, ring, stage, sc.level, sc.bin)) return sc;
+        if (partition_levels(s, cfg, sc.lvl_walkers, ring, stage, backward, sc.level, sc.bin)) return sc;
         if (sc.K == 1) throw Error(3, "walk schedule failed with one walker");
         sc.K = 1;  // dependencies cross subtrees: one walker
     }
@@ -572,25 +572,33 @@ LuLayout build_lu_layout(const Symbolic& s) {
 // The last level (one walker) takes whatever is left.  Returns false if some
 // dependency would cross walkers (possible only with unsymmetric pivoting).
 bool partition_levels(const Symbolic& s, const WalkConfig& cfg, const std::vector<int32_t>& lvl_walkers,
-                      const std::vector<int32_t>& ring_w, const std::vector<int32_t>& stage_w,
+                      const std::vector<int32_t>& ring_w, const std::vector<int32_t>& stage_w, bool backward,
                       std::vector<int32_t>& level, std::vector<int32_t>& bin) {
     const int32_t nJ = s.nJ, L = static_cast<int32_t>(lvl_walkers.size());
     level.assign(nJ, -1);
     bin.assign(nJ, 0);
     const std::vector<int32_t> parent = etree_parent(s);
     std::vector<double> work(nJ);
-    std::vector<int32_t> blk(nJ), fetch(nJ);
+    std::vector<int32_t> blk(nJ), fetch(nJ), urow(nJ, 0);
     std::vector<std::vector<int32_t>> children(nJ);
+    for (int32_t k = 0; k < nJ; ++k)
+        for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) urow[s.ri[z]]++;
     for (int32_t k = 0; k < nJ; ++k) {
         if (parent[k] >= 0 && parent[k] <= k) return false;
-        double wk = 60.0 + (s.cp[k + 1] - s.cp[k]);
-        for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) {
-            const int32_t j = s.ri[z];
-            wk += 12.0 + (s.cp[j + 1] - s.dpos[j] - 1);
+        if (!backward) {  // column k of the LU walk: its A block, its L(:,k) + y fetch
+            double wk = 60.0 + (s.cp[k + 1] - s.cp[k]);
+            for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) {
+                const int32_t j = s.ri[z];
+                wk += 12.0 + (s.cp[j + 1] - s.dpos[j] - 1);
+            }
+            work[k] = wk;
+            blk[k] = s.cp[k + 1] - s.cp[k] + 1;
+            fetch[k] = s.cp[k + 1] - s.dpos[k];
+        } else {  // row k of the backward walk: its U row + y + diagonal, single x rows
+            work[k] = 40.0 + 10.0 * urow[k];
+            blk[k] = urow[k] + 2;
+            fetch[k] = 1;
         }
-        work[k] = wk;
-        blk[k] = s.cp[k + 1] - s.cp[k] + 1;
-        fetch[k] = s.cp[k + 1] - s.dpos[k];
         if (parent[k] >= 0) children[parent[k]].push_back(k);
     }
     for (int32_t l = 0; l < L; ++l) {
@@ -673,7 +681,7 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
         for (int32_t k = 0; k < nJ; ++k)
             for (int32_t z = s.dpos[k] + 1; z < s.cp[k + 1]; ++z) lrow[s.ri[z]].push_back(k);
     Geometry g;
-    const Schedule sc = choose_schedule(s, cfg, g);
+    const Schedule sc = choose_schedule(s, cfg, g, false);
     const std::vector<Phase> phases = make_phases(sc.level, sc.bin, sc.K, sc.levels, true);
     std::vector<int32_t> posmap(nJ, -1), local(nJ, -1);
     auto make_program = [&](const std::vector<int32_t>& list) {
@@ -754,7 +762,7 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
     for (int32_t k = nJ - 1; k >= 0; --k)
         for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) urow[s.ri[z]].push_back(k);
     Geometry g;
-    const Schedule sc = choose_schedule(s, cfg, g);
+    const Schedule sc = choose_schedule(s, cfg, g, true);
     const std::vector<Phase> phases = make_phases(sc.level, sc.bin, sc.K, sc.levels, false);
     std::vector<int32_t> local(nJ, -1);
     auto make_program = [&](const std::vector<int32_t>& list) {

@@ -138,7 +138,7 @@ LuLayout build_lu_layout(const Symbolic& s);
 // halving walker counts; false if dependencies would cross walkers
 // (unsymmetric pivoting), in which case one walker is used.
 bool partition_levels(const Symbolic& s, const WalkConfig& cfg, const std::vector<int32_t>& lvl_walkers,
-                      const std::vector<int32_t>& ring_w, const std::vector<int32_t>& stage_w,
+                      const std::vector<int32_t>& ring_w, const std::vector<int32_t>& stage_w, bool backward,
                       std::vector<int32_t>& level, std::vector<int32_t>& bin);
 WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs, const WalkConfig& cfg);
 WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkConfig& cfg);

@@ -282,5 +282,7 @@ def test_walk_stats_and_layout():
     assert (walker < np.array([8, 4, 2, 1])[level]).all()
     # most columns are walked by eight concurrent walkers; the serial top is small
     assert (level == 0).mean() > 0.7 and (level == level.max()).sum() < 0.02 * len(own)
-    np.testing.assert_array_equal(plan.walk_export(2)["owner"], own)
+    # the backward walk has its own (lighter) blocks, so more of it runs at level 0
+    bl = plan.walk_export(2)["owner"] >> 4
+    assert (bl == 0).mean() >= (level == 0).mean()
     plan.close()
