@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--tasks", type=int, default=10000, help="tasks per GPU (weak scaling)")
     ap.add_argument("--total-tasks", type=int, default=0, help="strong scaling: total tasks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=8, help="batches in the pipelined e2e call")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -255,35 +255,37 @@ def main():
     job_conv = dist.reduce_sum(rk, conv)
     value = job_conv / (job_ms / 1e3)
 
-    # end to end through the C ABI with pinned host buffers
+    # end to end through the C ABI with pinned host buffers: gbnr_solve_batches
+    # over e2e_steps batches (alternating two distinct scenario batches), every
+    # batch's H2D of Sbus and D2H of V / iterations / status inside the timed
+    # region, pipelined against the neighbouring batches' solves
     n = gc.n_bus
-    hp0 = torch.from_numpy(np.ascontiguousarray(p0)).pin_memory().numpy()
-    hq0 = torch.from_numpy(np.ascontiguousarray(q0)).pin_memory().numpy()
-    out_vm = torch.empty((n, T), dtype=torch.float64).pin_memory().numpy()
-    out_va = torch.empty((n, T), dtype=torch.float64).pin_memory().numpy()
-    out_it = np.empty(T, np.int32)
-    out_cv = np.empty(T, np.uint8)
-    out_st = np.empty(T, np.int32)
-    out_mm = np.empty(T)
     import ctypes as C
     lib = S.lib()
-    ptr = lambda x: x.ctypes.data_as(C.c_void_p)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    pb, qb = montecarlo(gc, T, task0=task0 + T)
+    ins = [(pin(p0), pin(q0)), (pin(pb), pin(qb))]
+    outs = [S.TaskResults(pin(np.empty((n, T))), pin(np.empty((n, T))), np.empty(T, np.int32),
+                          np.empty(T, np.uint8), np.empty(T, np.int32), np.empty(T)) for _ in range(2)]
+    K = max(a.e2e_steps, 1)
+    P = C.c_void_p * K
+    arr = lambda xs: P(*[x.ctypes.data for x in xs])  # noqa: E731
+    sel = [i % 2 for i in range(K)]
     def solve_e2e():
-        rc = lib.gbnr_solve(plan.h, T, None, None, 1, ptr(hp0), ptr(hq0), T, ptr(vm0), ptr(va0), 1,
-                            ptr(out_vm), ptr(out_va), ptr(out_it), ptr(out_cv), ptr(out_st),
-                            ptr(out_mm))
+        rc = lib.gbnr_solve_batches(
+            plan.h, K, T, arr([ins[j][0] for j in sel]), arr([ins[j][1] for j in sel]),
+            vm0.ctypes.data, va0.ctypes.data, arr([outs[j].vm for j in sel]), arr([outs[j].va for j in sel]),
+            arr([outs[j].iterations for j in sel]), arr([outs[j].converged for j in sel]),
+            arr([outs[j].status for j in sel]), arr([outs[j].max_mismatch for j in sel]))
         S._check(rc)
     solve_e2e()  # warm
     dist.barrier(rk)
     e0 = time.perf_counter()
-    e2e_conv = 0
-    for _ in range(a.e2e_steps):
-        solve_e2e()
-        e2e_conv += int(out_cv.sum())
+    solve_e2e()
     e2e_s = dist.reduce_max(rk, time.perf_counter() - e0)
-    e2e_conv = dist.reduce_sum(rk, e2e_conv)
-    h2d = 2 * n * T * 8 + 2 * n * 8
-    d2h = 2 * n * T * 8 + T * (4 + 1 + 4 + 8)
+    e2e_conv = dist.reduce_sum(rk, sum(int(outs[j].converged.sum()) for j in sel))
+    h2d = 2 * n * T * 8
+    d2h = 2 * n * T * 8 + T * (4 + 4 + 8)
 
     # roofline of the dominant kernel: the LU walk (frozen-pattern G-P
     # refactorization fused with the forward substitution), DESIGN.md §5:
@@ -322,7 +324,9 @@ def main():
                           "wall_s_timed": wall},
                "clocks": clk.summary(),
                "e2e": {"value": e2e_conv / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h},
+                       "d2h_bytes_per_step": d2h, "steps": K,
+                       "call": "gbnr_solve_batches (pinned host buffers, per-batch H2D/D2H pipelined "
+                               "against the neighbouring batches' solves)"},
                "gpu_launches": int(launches),
                "roofline": roof,
                "cpu_baseline": cpu}

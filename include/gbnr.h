@@ -129,6 +129,19 @@ int gbnr_run(gbnr_plan* plan);
 int gbnr_fetch(gbnr_plan* plan, double* vm_out, double* va_out, int32_t* iterations_out,
                uint8_t* converged_out, int32_t* status_out, double* max_mismatch_out);
 
+/* A sequence of batches through one call, pipelined: batch i+1's injections go
+ * host->device on a copy stream and batch i-1's voltages device->host on another
+ * while batch i solves (batch_runtime.run over mini-batches).
+ * Every batch has n_tasks tasks with per-task injections p0[i]/q0[i]
+ * [n_bus][n_tasks] and the shared start voltages vm0/va0 [n_bus]; outputs per
+ * batch as gbnr_solve (any output array pointer may be NULL).  The injection
+ * and voltage host buffers should be pinned for full overlap (the small
+ * per-task results go through the plan's own pinned staging). */
+int gbnr_solve_batches(gbnr_plan* plan, int32_t n_batches, int32_t n_tasks, const double* const* p0,
+                       const double* const* q0, const double* vm0, const double* va0, double* const* vm_out,
+                       double* const* va_out, int32_t* const* iterations_out, uint8_t* const* converged_out,
+                       int32_t* const* status_out, double* const* max_mismatch_out);
+
 /* Per-kernel device time of the last gbnr_run/gbnr_solve (CUDA events on the
  * solver stream).  out[24]: [0..4] ms of npm, jacobian, lu, fsbs, vupdate when
  * opt.profile=1 (events recorded around each launch, no host syncs); [5] ms of

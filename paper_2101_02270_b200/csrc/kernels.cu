@@ -102,12 +102,13 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
         const double vre = vmr * v.c[r * bp + t], vim = vmr * v.s[r * bp + t];
         double P, Q;
         injection(vre, vim, ire, iim, P, Q);
-        const double fp = P - v.p0[size_t(r) * v.s_ld + size_t(t) * v.s_inc];
+        const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
+        const double fp = P - v.p0[size_t(r) * v.s_ld + ts];
         b_t[size_t(__ldg(v.brow_p + r)) * kTile] = fp;
         nrm = fmax(nrm, nan_as_inf_abs(fp));
         const int bq = __ldg(v.brow_q + r);
         if (bq >= 0) {
-            const double fq = Q - v.q0[size_t(r) * v.s_ld + size_t(t) * v.s_inc];
+            const double fq = Q - v.q0[size_t(r) * v.s_ld + ts];
             b_t[size_t(bq) * kTile] = fq;
             nrm = fmax(nrm, nan_as_inf_abs(fq));
         }
@@ -149,7 +150,34 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
     }
 }
 
-__global__ void bump_kernel(DevView v) { *v.it_dev += 1; }
+// Iteration bump; publishes this iteration's counters to mapped host memory (a
+// kernel store over PCIe, not a DMA copy that would queue behind bulk D2H
+// traffic of a pipelined neighbouring batch).
+__global__ void bump_kernel(DevView v) {
+    const int it = *v.it_dev;
+    volatile int32_t* h = v.h_counts;
+    h[it] = v.active_count[it];
+    h[32 + it] = v.active_count[32 + it];
+    __threadfence_system();
+    *v.it_dev = it + 1;
+}
+
+// Final per-status task counts -> mapped host memory.
+__global__ void status_count_kernel(DevView v) {
+    __shared__ int c[3];
+    if (threadIdx.x < 3) c[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < v.n_tasks; t += blockDim.x) {
+        const int s = v.status[t];
+        atomicAdd(&c[(s >= 0 && s <= 2) ? s : 2], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        volatile int32_t* h = v.h_counts;
+        h[64 + threadIdx.x] = c[threadIdx.x];
+    }
+    __threadfence_system();
+}
 
 // ---------------------------------------------------------------------------
 // Jacobian -> A tape (LU slot order, tile-blocked; fill slots are never
@@ -261,12 +289,14 @@ struct Prog {
 };
 
 // Debug timeline (GBNR_DBG & 4): kernel start (-1), phase barrier (0), end (1).
+#ifdef GBNR_TRACE
 __device__ __noinline__ void walk_trace_print(int tile, int warp, int what) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     printf("[walk] tile %d warp %d %s at %llu ns\n", tile, warp,
            what < 0 ? "start" : (what == 0 ? "reached sync" : "done"), t);
 }
+#endif
 __device__ __forceinline__ void walk_trace(const DevView& v, int tile, int warp, int lane, int what) {
 #ifdef GBNR_TRACE  // make GBNR_TRACE=1: compiled out of production builds (no call frame)
     if ((v.dbg & 4) && lane == 0 && (tile == 0 || tile == v.n_tiles - 1)) walk_trace_print(tile, warp, what);
@@ -577,6 +607,16 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     }
 }
 
+// [n][bpad] -> [n][n_tasks] (packed for a single linear D2H copy)
+__global__ void pack_kernel(double* __restrict__ dst, const double* __restrict__ src, int32_t n, int32_t n_tasks,
+                            int32_t bpad) {
+    const size_t tot = size_t(n) * n_tasks;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < tot; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t r = i / size_t(n_tasks), t = i - r * size_t(n_tasks);
+        dst[i] = src[r * size_t(bpad) + t];
+    }
+}
+
 __global__ void broadcast_kernel(double* dst, const double* src, int32_t n, int32_t bpad) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < size_t(n) * bpad) dst[i] = src[i / bpad];
@@ -618,6 +658,8 @@ void launch_npm(const DevView& v, cudaStream_t st) {
     bump_kernel<<<1, 1, 0, st>>>(v);
 }
 
+void launch_status_count(const DevView& v, cudaStream_t st) { status_count_kernel<<<1, 1024, 0, st>>>(v); }
+
 void launch_jacobian(const DevView& v, cudaStream_t st) {
     jacobian_kernel<<<dim3(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v)), 256, 0, st>>>(v);
 }
@@ -637,6 +679,10 @@ void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st) {
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {
     vupdate_kernel<<<dim3(unsigned((v.n + 31) / 32), n_super(v)), 256, 0, st>>>(v);
+}
+
+void launch_pack(double* dst, const double* src, int32_t n, int32_t n_tasks, int32_t bpad, cudaStream_t st) {
+    pack_kernel<<<148 * 8, 256, 0, st>>>(dst, src, n, n_tasks, bpad);
 }
 
 void launch_broadcast(double* dst, const double* src, int32_t n, int32_t bpad, cudaStream_t st) {

@@ -37,6 +37,8 @@ struct DevView {
     unsigned long long* norm_bits;  // running max-norm (IEEE bits) of the current NPM
     int32_t *tile_active, *active_count;
     int32_t* it_dev;                // Newton iteration counter on the device
+    int32_t* h_counts;              // mapped host memory: [0,32) active tasks, [32,64) active
+                                    // tiles per iteration, [64,67) tasks per final status
     double tol, singular_tol;
     int32_t max_iter;
     int32_t dbg;                    // experiment switches (GBNR_DBG), 0 in production
@@ -55,9 +57,11 @@ int walk_ctas_per_sm(size_t smem, int threads);  // resident LU-walk CTAs per SM
 void launch_init(const DevView& v, cudaStream_t st);
 void launch_npm(const DevView& v, cudaStream_t st);  // NPM + convergence + iteration bump
 void launch_jacobian(const DevView& v, cudaStream_t st);
+void launch_status_count(const DevView& v, cudaStream_t st);
 void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st);
 void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st);
 void launch_vupdate(const DevView& v, cudaStream_t st);
 void launch_broadcast(double* dst, const double* src, int32_t n, int32_t bpad, cudaStream_t st);
+void launch_pack(double* dst, const double* src, int32_t n, int32_t n_tasks, int32_t bpad, cudaStream_t st);
 
 }  // namespace gbnr

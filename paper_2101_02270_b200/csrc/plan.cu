@@ -72,13 +72,26 @@ struct gbnr_plan {
     gbnr_options opt{};
     bool on_device = false;
     cudaStream_t stream = nullptr;
+    // batch pipeline (gbnr_solve_batches): copy streams, a second input set and
+    // two result sets, so batch i+1's H2D and batch i-1's D2H overlap batch i
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    std::vector<void*> pipe;
+    int32_t pipe_tiles = 0;
+    double *p0_set[2] = {nullptr, nullptr}, *q0_set[2] = {nullptr, nullptr};
+    double *out_vm[2] = {nullptr, nullptr}, *out_va[2] = {nullptr, nullptr}, *out_mm[2] = {nullptr, nullptr};
+    int32_t *out_it[2] = {nullptr, nullptr}, *out_st[2] = {nullptr, nullptr};
+    cudaEvent_t ev_in[2] = {}, ev_free_in[2] = {}, ev_res[2] = {}, ev_out[2] = {};
+    // pinned staging of the small per-task results (a D2H into pageable memory
+    // would block the host until the copy stream drains)
+    int32_t *h_it[2] = {nullptr, nullptr}, *h_st[2] = {nullptr, nullptr};
+    double* h_mm[2] = {nullptr, nullptr};
     std::vector<void*> owned;     // structure buffers
     double* d_scratch = nullptr;  // [n] staging for broadcast sets
     std::vector<void*> batch;     // per-batch tapes
     int32_t cap_tiles = 0;        // allocated tile capacity
     bool staged = false;
     gbnr::DevView v{};
-    int32_t* h_count = nullptr;   // pinned
+    int32_t* h_count = nullptr;   // pinned, mapped (device writes counters here)
     double timing[24] = {0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // profiling: an event pair per phase, recorded without host syncs and
@@ -96,13 +109,33 @@ struct gbnr_plan {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+        for (void* q : pipe) cudaFree(q);
+        for (int i = 0; i < 2; ++i) {
+            for (cudaEvent_t e : {ev_in[i], ev_free_in[i], ev_res[i], ev_out[i]})
+                if (e) cudaEventDestroy(e);
+            if (h_it[i]) cudaFreeHost(h_it[i]);
+            if (h_st[i]) cudaFreeHost(h_st[i]);
+            if (h_mm[i]) cudaFreeHost(h_mm[i]);
+        }
+        if (s_h2d) cudaStreamDestroy(s_h2d);
+        if (s_d2h) cudaStreamDestroy(s_d2h);
         if (stream) cudaStreamDestroy(stream);
     }
 
     void upload_structure() {
         CK(cudaSetDevice(opt.device));
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-        CK(cudaMallocHost(&h_count, sizeof(int32_t) * 64));
+        CK(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i)
+            for (cudaEvent_t* e : {&ev_in[i], &ev_free_in[i], &ev_res[i], &ev_out[i]})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CK(cudaHostAlloc(&h_count, sizeof(int32_t) * 128, cudaHostAllocMapped));
+        {
+            void* dp = nullptr;
+            CK(cudaHostGetDevicePointer(&dp, h_count, 0));
+            v.h_counts = static_cast<int32_t*>(dp);
+        }
         CK(cudaEventCreate(&ev0));
         CK(cudaEventCreate(&ev1));
         gbnr::configure_kernels();
@@ -214,7 +247,7 @@ struct gbnr_plan {
                const double* vm0, const double* va0, int32_t n_vsets) {
         if (!on_device) throw Error(GBNR_ECONFIG, "host-only plan (device = -1) cannot solve");
         if (n_tasks <= 0) throw Error(GBNR_ECONFIG, "n_tasks must be positive");
-        if ((n_ssets != 1 && n_ssets != n_tasks) || (n_vsets != 1 && n_vsets != n_tasks))
+        if ((n_ssets != 0 && n_ssets != 1 && n_ssets != n_tasks) || (n_vsets != 1 && n_vsets != n_tasks))
             throw Error(GBNR_ECONFIG, "set counts must be 1 or n_tasks");
         CK(cudaSetDevice(opt.device));
         const int32_t n_tiles = (n_tasks + gbnr::kTile - 1) / gbnr::kTile;
@@ -224,13 +257,23 @@ struct gbnr_plan {
         v.n_tasks = n_tasks;
         put_tape(const_cast<double*>(v.vm_in), vm0, n_vsets, n_tasks);
         put_tape(const_cast<double*>(v.va_in), va0, n_vsets, n_tasks);
-        if (n_ssets == 1 && n_tasks > 1) {
+        if (n_ssets == 0) {
+            // injections are placed by the caller (batch pipeline)
+        } else if (n_ssets == 1 && n_tasks > 1) {
             CK(cudaMemcpyAsync(const_cast<double*>(v.p0), p0, size_t(sym.n) * sizeof(double),
                                cudaMemcpyHostToDevice, stream));
             CK(cudaMemcpyAsync(const_cast<double*>(v.q0), q0, size_t(sym.n) * sizeof(double),
                                cudaMemcpyHostToDevice, stream));
             v.s_ld = 1;
             v.s_inc = 0;
+        } else if (n_ssets == n_tasks && n_tasks > 1) {
+            // the host layout [n][n_tasks] as is: one linear copy per array (a
+            // pitched copy into [n][bpad] runs the DMA engines row by row)
+            const size_t bytes = size_t(sym.n) * size_t(n_tasks) * sizeof(double);
+            CK(cudaMemcpyAsync(const_cast<double*>(v.p0), p0, bytes, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(const_cast<double*>(v.q0), q0, bytes, cudaMemcpyHostToDevice, stream));
+            v.s_ld = n_tasks;
+            v.s_inc = 1;
         } else {
             put_tape(const_cast<double*>(v.p0), p0, n_ssets, n_tasks);
             put_tape(const_cast<double*>(v.q0), q0, n_ssets, n_tasks);
@@ -286,10 +329,8 @@ struct gbnr_plan {
         timed(kNpm, [&] { gbnr::launch_npm(v, stream); });
         int it_done = 0;
         for (int it = 1; it <= opt.max_iter; ++it) {
-            CK(cudaMemcpyAsync(h_count, v.active_count + (it - 1), sizeof(int32_t),
-                               cudaMemcpyDeviceToHost, stream));
-            CK(cudaStreamSynchronize(stream));
-            if (*h_count == 0) break;
+            CK(cudaStreamSynchronize(stream));  // the bump kernel published active_count[it-1]
+            if (reinterpret_cast<volatile int32_t*>(h_count)[it - 1] == 0) break;
             timed(kJac, [&] { gbnr::launch_jacobian(v, stream); });
             timed(kLu, [&] { launch_lu_all(); });
             timed(kFsbs, [&] { launch_fsbs_all(); });
@@ -299,8 +340,7 @@ struct gbnr_plan {
             it_done = it;
         }
         CK(cudaEventRecord(ev1, stream));
-        CK(cudaMemcpyAsync(h_count, v.active_count, 64 * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                           stream));
+        gbnr::launch_status_count(v, stream);
         CK(cudaStreamSynchronize(stream));
         double tiles = 0, tasks = 0;
         for (int it = 1; it <= it_done; ++it) {
@@ -309,9 +349,7 @@ struct gbnr_plan {
         }
         timing[14] = tiles;
         timing[15] = tasks;
-        std::vector<int32_t> st(size_t(v.n_tasks));
-        CK(cudaMemcpy(st.data(), v.status, st.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        for (int32_t x : st) timing[16 + (x >= 0 && x <= 2 ? x : 2)] += 1.0;
+        for (int x = 0; x < 3; ++x) timing[16 + x] = h_count[64 + x];
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
         resolve_profile();
@@ -321,17 +359,118 @@ struct gbnr_plan {
         timing[19] = double(launches_per_iteration()) * it_done + 4;  // kernels launched
     }
 
+    void ensure_pipe(int32_t n_tiles) {
+        if (n_tiles <= pipe_tiles) return;
+        CK(cudaDeviceSynchronize());
+        for (void* q : pipe) cudaFree(q);
+        pipe.clear();
+        const size_t nb = size_t(sym.n) * size_t(n_tiles) * gbnr::kTile * sizeof(double);
+        const size_t tb = size_t(n_tiles) * gbnr::kTile;
+        auto alloc = [&](size_t bytes) {
+            void* q = nullptr;
+            CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+            pipe.push_back(q);
+            return q;
+        };
+        for (int i = 0; i < 2; ++i) {
+            if (h_it[i]) cudaFreeHost(h_it[i]);
+            if (h_st[i]) cudaFreeHost(h_st[i]);
+            if (h_mm[i]) cudaFreeHost(h_mm[i]);
+            CK(cudaMallocHost(&h_it[i], tb * sizeof(int32_t)));
+            CK(cudaMallocHost(&h_st[i], tb * sizeof(int32_t)));
+            CK(cudaMallocHost(&h_mm[i], tb * sizeof(double)));
+            p0_set[i] = static_cast<double*>(alloc(nb));
+            q0_set[i] = static_cast<double*>(alloc(nb));
+            out_vm[i] = static_cast<double*>(alloc(nb));
+            out_va[i] = static_cast<double*>(alloc(nb));
+            out_mm[i] = static_cast<double*>(alloc(tb * sizeof(double)));
+            out_it[i] = static_cast<int32_t*>(alloc(tb * sizeof(int32_t)));
+            out_st[i] = static_cast<int32_t*>(alloc(tb * sizeof(int32_t)));
+        }
+        pipe_tiles = n_tiles;
+    }
+
+    // Pipelined sequence of batches (all of n_tasks tasks, injections per task,
+    // start voltages shared): H2D of batch i+1 (copy stream) and D2H of batch
+    // i-1 (second copy stream) run while batch i solves.  Results per batch as
+    // in gbnr_solve.
+    void solve_batches(int32_t n_batches, int32_t n_tasks, const double* const* p0s, const double* const* q0s,
+                       const double* vm0, const double* va0, double* const* vms, double* const* vas,
+                       int32_t* const* its, uint8_t* const* convs, int32_t* const* sts, double* const* mms) {
+        if (n_batches <= 0) return;
+        const size_t ntt = size_t(n_tasks);
+        // batch j's small results: pinned staging -> the caller's arrays
+        auto unstage_small = [&](int32_t j) {
+            const int set = j & 1;
+            CK(cudaEventSynchronize(ev_out[set]));
+            if (its && its[j]) std::memcpy(its[j], h_it[set], ntt * 4);
+            if (sts && sts[j]) std::memcpy(sts[j], h_st[set], ntt * 4);
+            if (mms && mms[j]) std::memcpy(mms[j], h_mm[set], ntt * 8);
+            if (convs && convs[j])
+                for (size_t t = 0; t < ntt; ++t) convs[j][t] = h_st[set][t] == GBNR_CONVERGED;
+        };
+        // geometry and the shared start voltages (injections come per batch below)
+        stage(n_tasks, nullptr, nullptr, 0, vm0, va0, 1);
+        CK(cudaStreamSynchronize(stream));
+        ensure_pipe(v.n_tiles);
+        const size_t nt = size_t(n_tasks), row = nt * sizeof(double);
+        const size_t bytes = size_t(sym.n) * row;  // host layout [n][n_tasks], copied linearly
+        auto issue_h2d = [&](int32_t j) {
+            const int set = j & 1;
+            if (j >= 2) CK(cudaStreamWaitEvent(s_h2d, ev_free_in[set], 0));
+            CK(cudaMemcpyAsync(p0_set[set], p0s[j], bytes, cudaMemcpyHostToDevice, s_h2d));
+            CK(cudaMemcpyAsync(q0_set[set], q0s[j], bytes, cudaMemcpyHostToDevice, s_h2d));
+            CK(cudaEventRecord(ev_in[set], s_h2d));
+        };
+        issue_h2d(0);
+        for (int32_t i = 0; i < n_batches; ++i) {
+            const int set = i & 1;
+            if (i + 1 < n_batches) issue_h2d(i + 1);
+            CK(cudaStreamWaitEvent(stream, ev_in[set], 0));
+            v.p0 = p0_set[set];
+            v.q0 = q0_set[set];
+            v.s_ld = n_tasks;
+            v.s_inc = 1;
+            run();
+            CK(cudaEventRecord(ev_free_in[set], stream));
+            if (i >= 2) CK(cudaStreamWaitEvent(stream, ev_out[set], 0));
+            // pack [n][bpad] -> [n][n_tasks] on the device so the D2H is one linear copy
+            gbnr::launch_pack(out_vm[set], v.vm, sym.n, n_tasks, v.bpad, stream);
+            gbnr::launch_pack(out_va[set], v.va, sym.n, n_tasks, v.bpad, stream);
+            CK(cudaMemcpyAsync(out_it[set], v.iters, nt * 4, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemcpyAsync(out_st[set], v.status, nt * 4, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemcpyAsync(out_mm[set], v.maxmis, nt * 8, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaEventRecord(ev_res[set], stream));
+            CK(cudaStreamWaitEvent(s_d2h, ev_res[set], 0));
+            if (vms[i]) CK(cudaMemcpyAsync(vms[i], out_vm[set], bytes, cudaMemcpyDeviceToHost, s_d2h));
+            if (vas[i]) CK(cudaMemcpyAsync(vas[i], out_va[set], bytes, cudaMemcpyDeviceToHost, s_d2h));
+            if (i >= 2) unstage_small(i - 2);  // its pinned staging set is reused now
+            CK(cudaMemcpyAsync(h_it[set], out_it[set], nt * 4, cudaMemcpyDeviceToHost, s_d2h));
+            CK(cudaMemcpyAsync(h_st[set], out_st[set], nt * 4, cudaMemcpyDeviceToHost, s_d2h));
+            CK(cudaMemcpyAsync(h_mm[set], out_mm[set], nt * 8, cudaMemcpyDeviceToHost, s_d2h));
+            CK(cudaEventRecord(ev_out[set], s_d2h));
+        }
+        CK(cudaStreamSynchronize(s_d2h));
+        CK(cudaStreamSynchronize(s_h2d));
+        for (int32_t i = std::max(0, n_batches - 2); i < n_batches; ++i) unstage_small(i);
+        staged = false;  // the device tapes no longer hold a staged batch
+    }
+
     void fetch(double* vm, double* va, int32_t* iters, uint8_t* conv, int32_t* status,
                double* maxmis) {
         CK(cudaSetDevice(opt.device));
         const int32_t nt = v.n_tasks;
-        const size_t bpad = size_t(v.bpad);
-        if (vm)
-            CK(cudaMemcpy2DAsync(vm, size_t(nt) * 8, v.vm, bpad * 8, size_t(nt) * 8, sym.n,
-                                 cudaMemcpyDeviceToHost, stream));
-        if (va)
-            CK(cudaMemcpy2DAsync(va, size_t(nt) * 8, v.va, bpad * 8, size_t(nt) * 8, sym.n,
-                                 cudaMemcpyDeviceToHost, stream));
+        const size_t row = size_t(nt) * 8, bytes = size_t(sym.n) * row;
+        if (vm || va) ensure_pipe(v.n_tiles);
+        // pack [n][bpad] -> [n][n_tasks] on the device, then one linear D2H each
+        if (vm) {
+            gbnr::launch_pack(out_vm[0], v.vm, sym.n, nt, v.bpad, stream);
+            CK(cudaMemcpyAsync(vm, out_vm[0], bytes, cudaMemcpyDeviceToHost, stream));
+        }
+        if (va) {
+            gbnr::launch_pack(out_va[0], v.va, sym.n, nt, v.bpad, stream);
+            CK(cudaMemcpyAsync(va, out_va[0], bytes, cudaMemcpyDeviceToHost, stream));
+        }
         std::vector<int32_t> st(nt);
         CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
         if (iters) CK(cudaMemcpyAsync(iters, v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
@@ -508,7 +647,10 @@ int gbnr_plan_export(const gbnr_plan* p, int32_t* row_fwd, int32_t* col_fwd, int
 
 int gbnr_stage(gbnr_plan* p, int32_t n_tasks, const double* p0, const double* q0, int32_t n_ssets,
                const double* vm0, const double* va0, int32_t n_vsets) {
-    return guarded([&] { p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets); });
+    return guarded([&] {
+        if (n_ssets < 1) throw Error(GBNR_ECONFIG, "n_ssets must be 1 or n_tasks");
+        p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
+    });
 }
 
 int gbnr_run(gbnr_plan* p) {
@@ -531,6 +673,7 @@ int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* 
     return guarded([&] {
         if (n_ysets != 1)
             throw Error(GBNR_ECONFIG, "per-task Ybus value sets (N-1 mode) are not supported yet");
+        if (n_ssets < 1) throw Error(GBNR_ECONFIG, "n_ssets must be 1 or n_tasks");
         if (y_re && y_im) {
             // a different shared value set than the plan's: refresh it on the device
             CK(cudaSetDevice(p->opt.device));
@@ -542,6 +685,18 @@ int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* 
         p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
         p->run();
         p->fetch(vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out);
+    });
+}
+
+int gbnr_solve_batches(gbnr_plan* p, int32_t n_batches, int32_t n_tasks, const double* const* p0,
+                       const double* const* q0, const double* vm0, const double* va0, double* const* vm_out,
+                       double* const* va_out, int32_t* const* iterations_out, uint8_t* const* converged_out,
+                       int32_t* const* status_out, double* const* max_mismatch_out) {
+    return guarded([&] {
+        for (int32_t i = 0; i < n_batches; ++i)
+            if (!p0 || !q0 || !p0[i] || !q0[i]) throw Error(GBNR_ECONFIG, "every batch needs p0 and q0");
+        p->solve_batches(n_batches, n_tasks, p0, q0, vm0, va0, vm_out, va_out, iterations_out, converged_out,
+                         status_out, max_mismatch_out);
     });
 }
 

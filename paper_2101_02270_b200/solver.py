@@ -33,7 +33,8 @@ STAT_KEYS = ("nJ", "nnzJ", "nnzLU", "nnzL", "nnzU", "D", "flops_lu", "levels_lu"
 EXPORTS = ("gbnr_default_options", "gbnr_last_error", "gbnr_version", "gbnr_build_ybus",
            "gbnr_amd_order", "gbnr_plan_create", "gbnr_plan_destroy", "gbnr_plan_stats",
            "gbnr_plan_export", "gbnr_solve", "gbnr_stage", "gbnr_run", "gbnr_fetch",
-           "gbnr_last_timing", "gbnr_refactor", "gbnr_walk_info", "gbnr_walk_export")
+           "gbnr_last_timing", "gbnr_refactor", "gbnr_walk_info", "gbnr_walk_export",
+           "gbnr_solve_batches")
 
 
 class GbnrError(RuntimeError):
@@ -87,6 +88,7 @@ def lib() -> C.CDLL:
     L.gbnr_refactor.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                 C.POINTER(C.c_double)]
     L.gbnr_walk_info.argtypes = [C.c_void_p, C.c_int32, _i64p]
+    L.gbnr_solve_batches.argtypes = [C.c_void_p, C.c_int32, C.c_int32] + [C.c_void_p] * 10
     L.gbnr_walk_export.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     _lib = L
     return L
@@ -237,6 +239,29 @@ class NrPlan:
         self.stage(p0, q0, vm0, va0, n_tasks)
         self.run()
         return self.fetch()
+
+    def solve_batches(self, p0s, q0s, vm0, va0, outs=None):
+        """Pipelined sequence of batches (gbnr_solve_batches): per-task injections
+        p0s[i]/q0s[i] [n][T], shared start voltages; returns a list of TaskResults
+        (or fills the preallocated `outs`)."""
+        nb = len(p0s)
+        T = p0s[0].shape[1]
+        n = self.n_bus
+        p0s = [_f64(a) for a in p0s]
+        q0s = [_f64(a) for a in q0s]
+        if outs is None:
+            outs = [TaskResults(np.empty((n, T)), np.empty((n, T)), np.empty(T, np.int32),
+                                np.empty(T, np.uint8), np.empty(T, np.int32), np.empty(T))
+                    for _ in range(nb)]
+        P = C.c_void_p * nb
+        arr = lambda xs: P(*[x.ctypes.data for x in xs])  # noqa: E731
+        self._keep = (p0s, q0s)
+        _check(lib().gbnr_solve_batches(
+            self.h, nb, T, arr(p0s), arr(q0s), _ptr(_f64(vm0)), _ptr(_f64(va0)),
+            arr([o.vm for o in outs]), arr([o.va for o in outs]), arr([o.iterations for o in outs]),
+            arr([o.converged for o in outs]), arr([o.status for o in outs]),
+            arr([o.max_mismatch for o in outs])))
+        return outs
 
     def timing(self) -> dict:
         out = np.zeros(24)

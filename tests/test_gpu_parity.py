@@ -132,3 +132,17 @@ def test_walk_plan_invariance(opts):
     plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, **opts)
     p0, q0 = montecarlo(gc, 100)
     _compare(plan2.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
+
+
+def test_solve_batches_pipeline_matches_single_solves():
+    """gbnr_solve_batches (H2D / D2H overlapped with neighbouring solves) returns
+    exactly what one gbnr_solve per batch returns."""
+    gc, plan, oplan, vm0, va0 = _setup("synth300")
+    T = 160
+    batches = [montecarlo(gc, T, task0=i * T) for i in range(3)]
+    outs = plan.solve_batches([b[0] for b in batches], [b[1] for b in batches], vm0, va0)
+    for (p0, q0), r in zip(batches, outs):
+        s = plan.solve(p0, q0, vm0, va0)
+        for k in ("vm", "va", "iterations", "converged", "status", "max_mismatch"):
+            np.testing.assert_array_equal(getattr(r, k), getattr(s, k))
+        _compare(r, oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
