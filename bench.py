@@ -215,7 +215,7 @@ def main():
     from paper_2101_02270_b200.case import load_case
     from paper_2101_02270_b200.scenarios import montecarlo
 
-    dev = rk.local_rank if rk.world > 1 else 0
+    dev = dist.device_of(rk)
     gc = load_case(os.path.join(ROOT, "cases", a.case + ".m"))
     if a.total_tasks:
         task0, T = dist.shard(a.total_tasks, rk.world, rk.rank)

@@ -38,18 +38,28 @@ def shard(n_total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def init(backend: str | None = None) -> Rank:
+    """Join the job.  Backend: nccl when GPUs are visible, else gloo;
+    GBNR_DIST_BACKEND overrides (gloo lets several ranks share one GPU in tests)."""
     r = from_env()
     if r.world > 1:
         import torch.distributed as td
         if not td.is_initialized():
+            backend = backend or os.environ.get("GBNR_DIST_BACKEND")
             if backend is None:
                 import torch
                 backend = "nccl" if torch.cuda.is_available() else "gloo"
             if backend == "nccl":
                 import torch
-                torch.cuda.set_device(r.local_rank)
+                torch.cuda.set_device(device_of(r))
             td.init_process_group(backend=backend)
     return r
+
+
+def device_of(r: Rank) -> int:
+    """CUDA ordinal of a rank: one GPU per rank (wrapping when ranks outnumber GPUs)."""
+    import torch
+    n = torch.cuda.device_count()
+    return r.local_rank % n if n else 0
 
 
 def _device():
