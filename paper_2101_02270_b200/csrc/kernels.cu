@@ -408,7 +408,36 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
                 const double mult = x[(kpos_fs & 0xffff) * kTile];
                 const int32_t* dw = r + 4;
                 int q = 0;
-                for (; q + 4 <= nrows; q += 4) {
+                for (; q + 8 <= nrows; q += 8) {  // eight independent rows in flight
+                    const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1], w2 = dw[(q >> 1) + 2],
+                                  w3 = dw[(q >> 1) + 3];
+                    const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
+                    const int d2 = w1 & 0xffff, d3 = int(unsigned(w1) >> 16);
+                    const int d4 = w2 & 0xffff, d5 = int(unsigned(w2) >> 16);
+                    const int d6 = w3 & 0xffff, d7 = int(unsigned(w3) >> 16);
+                    double l[8], a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) l[u] = src[(q + u) * kTile];
+                    a[0] = x[d0 * kTile];
+                    a[1] = x[d1 * kTile];
+                    a[2] = x[d2 * kTile];
+                    a[3] = x[d3 * kTile];
+                    a[4] = x[d4 * kTile];
+                    a[5] = x[d5 * kTile];
+                    a[6] = x[d6 * kTile];
+                    a[7] = x[d7 * kTile];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = fma(-mult, l[u], a[u]);
+                    x[d0 * kTile] = a[0];
+                    x[d1 * kTile] = a[1];
+                    x[d2 * kTile] = a[2];
+                    x[d3 * kTile] = a[3];
+                    x[d4 * kTile] = a[4];
+                    x[d5 * kTile] = a[5];
+                    x[d6 * kTile] = a[6];
+                    x[d7 * kTile] = a[7];
+                }
+                if (q + 4 <= nrows) {
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1];
                     const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
                     const int d2 = w1 & 0xffff, d3 = int(unsigned(w1) >> 16);
@@ -423,6 +452,7 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
                     x[d1 * kTile] = a1;
                     x[d2 * kTile] = a2;
                     x[d3 * kTile] = a3;
+                    q += 4;
                 }
                 if (q + 2 <= nrows) {  // q even here: one packed pair
                     const int32_t w0 = dw[q >> 1];
@@ -457,33 +487,29 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
             x = P.R + size_t(ring) * kTile + lane;
             acc_y = FS ? x[len * kTile] : 0.0;
         } else if (type == kRecEnd) {
-            // pivot check and normalization L = x * (1 / pivot)
+            // normalization L = x * (1 / pivot) and the U scatter, with the
+            // pivot check's column maximum folded into the same
+            // passes over x (max |x| is exact in any order)
             const double piv = x[dp * kTile];
-            // max |x| is exact in any order: four independent chains
-            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-            int z = 0;
-            for (; z + 4 <= len; z += 4) {
-                c0 = fmax(c0, fabs(x[z * kTile]));
-                c1 = fmax(c1, fabs(x[(z + 1) * kTile]));
-                c2 = fmax(c2, fabs(x[(z + 2) * kTile]));
-                c3 = fmax(c3, fabs(x[(z + 3) * kTile]));
-            }
-            for (; z < len; ++z) c0 = fmax(c0, fabs(x[z * kTile]));
-            const double cmax = fmax(fmax(c0, c1), fmax(c2, c3));
-            flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
             const double inv = 1.0 / piv;
+            double c0 = fabs(piv), c1 = 0.0;
             double* lcol = lu_t + size_t(lslot) * kTile;  // diagonal, then L rows
             lcol[0] = piv;
-            z = dp + 1;
+            int z = dp + 1;
             for (; z + 2 <= len; z += 2) {
-                const double l0 = x[z * kTile] * inv, l1 = x[(z + 1) * kTile] * inv;
+                const double x0 = x[z * kTile], x1 = x[(z + 1) * kTile];
+                c0 = fmax(c0, fabs(x0));
+                c1 = fmax(c1, fabs(x1));
+                const double l0 = x0 * inv, l1 = x1 * inv;
                 x[z * kTile] = l0;
                 x[(z + 1) * kTile] = l1;
                 lcol[size_t(z - dp) * kTile] = l0;
                 lcol[size_t(z + 1 - dp) * kTile] = l1;
             }
             if (z < len) {
-                const double l0 = x[z * kTile] * inv;
+                const double x0 = x[z * kTile];
+                c0 = fmax(c0, fabs(x0));
+                const double l0 = x0 * inv;
                 x[z * kTile] = l0;
                 lcol[size_t(z - dp) * kTile] = l0;
             }
@@ -492,12 +518,22 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
                 const int32_t s0 = r[1 + z], s1 = r[2 + z], s2 = r[3 + z], s3 = r[4 + z];
                 const double u0 = x[z * kTile], u1 = x[(z + 1) * kTile], u2 = x[(z + 2) * kTile],
                              u3 = x[(z + 3) * kTile];
+                c0 = fmax(c0, fabs(u0));
+                c1 = fmax(c1, fabs(u1));
+                c0 = fmax(c0, fabs(u2));
+                c1 = fmax(c1, fabs(u3));
                 lu_t[size_t(s0) * kTile] = u0;
                 lu_t[size_t(s1) * kTile] = u1;
                 lu_t[size_t(s2) * kTile] = u2;
                 lu_t[size_t(s3) * kTile] = u3;
             }
-            for (; z < dp; ++z) lu_t[size_t(r[1 + z]) * kTile] = x[z * kTile];
+            for (; z < dp; ++z) {
+                const double u0 = x[z * kTile];
+                c0 = fmax(c0, fabs(u0));
+                lu_t[size_t(r[1 + z]) * kTile] = u0;
+            }
+            const double cmax = fmax(c0, c1);
+            flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
             if (FS) {
                 x[len * kTile] = acc_y;
                 b_t[size_t(brow) * kTile] = acc_y;
