@@ -379,7 +379,7 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
 template <bool FS>
-__global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
+__global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(256) lu_walk_kernel(DevView v, WalkView w) {
 }
 
 // Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
-__global__ void __launch_bounds__(256) bs_walk_kernel(DevView v, WalkView w) {
+__global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
