@@ -87,6 +87,17 @@ int gbnr_build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* from, const 
                     const double* bs, double base_mva, int32_t* indptr, int32_t* indices,
                     int32_t* diag, double* y_re, double* y_im, int32_t* nnz_out);
 
+/* N-1 contingency value sets on the base pattern (ybus_values_with_outage,
+ * grid.hpp:245-255): task t removes branch outage_branch[t] (-1 = base case);
+ * y_re/y_im [nnzY][n_tasks] element-major in gbnr_build_ybus slot order, ready
+ * for gbnr_solve with n_ysets = n_tasks.  islanded [n_tasks] (may be NULL) =
+ * the outage splits the grid (outage_islands_grid, grid.hpp:257-261). */
+int gbnr_contingency_values(int32_t n_bus, int32_t n_branch, const int32_t* from, const int32_t* to,
+                            const double* r, const double* x, const double* b, const double* tap,
+                            const double* shift_deg, const uint8_t* in_service, const double* gs,
+                            const double* bs, double base_mva, const int32_t* outage_branch, int32_t n_tasks,
+                            double* y_re, double* y_im, uint8_t* islanded);
+
 /* Fill-reducing ordering on a square CCS pattern (amd.hpp:29-157); fwd[old] = new. */
 int gbnr_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd);
 
@@ -109,7 +120,8 @@ int gbnr_plan_export(const gbnr_plan* plan, int32_t* row_fwd, int32_t* col_fwd, 
                      int32_t* row_ix, int32_t* level);
 
 /* Batched Newton-Raphson, host buffers in and out (H2D, solve, D2H).
- *   y_re/y_im [nnzY][n_ysets] (n_ysets must be 1 in this version),
+ *   y_re/y_im [nnzY][n_ysets] (NULL = the plan's set; n_ysets = n_tasks for
+ *   per-task sets, e.g. N-1 contingencies from gbnr_contingency_values),
  *   p0/q0 [n_bus][n_ssets], vm0/va0 [n_bus][n_vsets],
  *   vm_out/va_out [n_bus][n_tasks], iterations/converged/status/max_mismatch [n_tasks].
  * iterations follow MATPOWER: 0 if V0 already converged, else the number of

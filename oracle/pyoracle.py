@@ -187,6 +187,7 @@ class Reference:
         L.ref_profiles.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _f64p, _f64p, _f64p, _f64p,
                                    _f64p, _f64p, _f64p]
         L.ref_case_loads.argtypes = [C.c_void_p, _f64p, _f64p]
+        L.ref_ybus_outage.argtypes = [C.c_void_p, C.c_int32, _f64p, _f64p, C.POINTER(C.c_int32)]
         L.ref_amd_order.argtypes = [C.c_int32, _i32p, _i32p, _i32p]
         L.ref_crs_from_coords.argtypes = [C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, C.c_int32,
                                           _i32p, _i32p, _i32p, C.POINTER(C.c_int32)]
@@ -234,6 +235,13 @@ class RefCase:
         yr = np.zeros(z); yi = np.zeros(z)
         self.r.lib.ref_build_ybus(self.h, ip, ix, dg, yr, yi)
         return ip, ix, dg, yr, yi
+
+    def outage(self, branch):
+        """(y_re, y_im, islands) of ybus_values_with_outage / outage_islands_grid."""
+        yr = np.zeros(self.nnzY); yi = np.zeros(self.nnzY); isl = C.c_int32()
+        if self.r.lib.ref_ybus_outage(self.h, int(branch), yr, yi, C.byref(isl)) != 0:
+            raise OracleError(self.r.err())
+        return yr, yi, bool(isl.value)
 
     def loads(self):
         p = np.zeros(self.n_bus); q = np.zeros(self.n_bus)

@@ -136,6 +136,21 @@ int ref_case_loads(void* h, double* p_mw, double* q_mvar) {
     });
 }
 
+// ybus_values_with_outage (grid.hpp:245-255) for one branch, and the islanding
+// pre-check outage_islands_grid (grid.hpp:257-261).
+int ref_ybus_outage(void* h, int32_t branch, double* yre, double* yim, int32_t* islands) {
+    return guarded([&] {
+        const GridCase& gc = *static_cast<GridCase*>(h);
+        const YbusModel y = build_ybus(gc);
+        const std::vector<cplx> v = ybus_values_with_outage(y, branch);
+        for (size_t s = 0; s < v.size(); ++s) {
+            yre[s] = v[s].real();
+            yim[s] = v[s].imag();
+        }
+        *islands = outage_islands_grid(gc, branch) ? 1 : 0;
+    });
+}
+
 // amd_order on a square CCS pattern; writes forward[old] = new.
 int ref_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd) {
     return guarded([&] {

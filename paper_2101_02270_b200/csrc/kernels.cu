@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
     const int t = tile * kTile + lane;
     const size_t bp = v.bpad;
     double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;  // tile-blocked b tape
+    const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
     double nrm = 0.0;
     const int r1 = min(v.n_rows, int(blockIdx.x + 1) * kRowChunk);
     for (int ri = blockIdx.x * kRowChunk; ri < r1; ++ri) {
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
         for (int q = __ldg(v.yp + r); q < q1; ++q) {
             const int k = __ldg(v.yi + q);
             const double vmk = v.vm[k * bp + t];
-            acc_current(__ldg(v.yre + q), __ldg(v.yim + q), vmk * v.c[k * bp + t],
+            acc_current(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vmk * v.c[k * bp + t],
                         vmk * v.s[k * bp + t], ire, iim);
         }
         const double vmr = v.vm[r * bp + t];
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
     if (blockIdx.x == 0) v.flag[t] = 0;  // pivot flags of this iteration's refactorization
     const size_t bp = v.bpad;
     double* a_t = v.A + size_t(tile) * v.nnzLU * kTile + lane;  // tile-blocked A tape
+    const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
     const int r1 = min(v.n_rows, int(blockIdx.x + 1) * kRowChunk);
     for (int ri = blockIdx.x * kRowChunk; ri < r1; ++ri) {
         const int r = __ldg(v.rows + ri);
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
         for (int q = q0; q < q1; ++q) {
             const int k = __ldg(v.yi + q);
             const double vmk = v.vm[k * bp + t];
-            acc_current(__ldg(v.yre + q), __ldg(v.yim + q), vmk * v.c[k * bp + t],
+            acc_current(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vmk * v.c[k * bp + t],
                         vmk * v.s[k * bp + t], ire, iim);
         }
         const double vmr = v.vm[r * bp + t];
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
             const int k = __ldg(v.yi + q);
             const double ck = v.c[k * bp + t], sk = v.s[k * bp + t], vmk = v.vm[k * bp + t];
             double zre, zim, j[4];
-            jac_z(__ldg(v.yre + q), __ldg(v.yim + q), vre, vim, ck, sk, zre, zim);
+            jac_z(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vre, vim, ck, sk, zre, zim);
             jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
             const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
             if (act) {

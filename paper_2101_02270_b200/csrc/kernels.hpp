@@ -20,7 +20,8 @@ struct DevView {
     int32_t n, nJ, nnzY, n_rows, nnzLU, bpad, n_tiles, n_tasks;
     // shared structure (read-only, L2-resident)
     const int32_t *yp, *yi;
-    const double *yre, *yim;
+    const double *yre, *yim;      // Ybus values: slot q of task t at q * y_ld + t * y_inc
+    int32_t y_ld, y_inc;          // (1, 0): one shared set; (n_tasks, 1): per task (N-1)
     const int32_t *rows, *brow_p, *brow_q, *zcol_t, *zcol_v;
     const int32_t* lk;
     // per-task tapes [elem][bpad]

@@ -110,6 +110,8 @@ struct gbnr_plan {
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
         for (void* q : pipe) cudaFree(q);
+        if (y_task_re) cudaFree(y_task_re);
+        if (y_task_im) cudaFree(y_task_im);
         for (int i = 0; i < 2; ++i) {
             for (cudaEvent_t e : {ev_in[i], ev_free_in[i], ev_res[i], ev_out[i]})
                 if (e) cudaEventDestroy(e);
@@ -183,10 +185,59 @@ struct gbnr_plan {
         return x;
     }
 
+    // the plan's shared Ybus value set (one for every task)
+    const double *y_shared_re = nullptr, *y_shared_im = nullptr;
+    // per-task value sets (N-1 contingencies), [nnzY][n_tasks] as the caller lays them out
+    double *y_task_re = nullptr, *y_task_im = nullptr;
+    size_t y_task_cap = 0;
+
     void set_ybus(const double* re, const double* im) {
         std::vector<double> a(re, re + sym.nnzY), b(im, im + sym.nnzY);
-        v.yre = dev_upload(owned, a);
-        v.yim = dev_upload(owned, b);
+        v.yre = y_shared_re = dev_upload(owned, a);
+        v.yim = y_shared_im = dev_upload(owned, b);
+        v.y_ld = 1;
+        v.y_inc = 0;
+    }
+
+    // Ybus values for the next solve: n_ysets = 1 refreshes the shared set, n_tasks
+    // stages one set per task (linear copies of the caller's [nnzY][n_tasks]).
+    void stage_ybus(const double* y_re, const double* y_im, int32_t n_ysets, int32_t n_tasks) {
+        if (!y_re || !y_im) {
+            if (n_ysets != 1) throw Error(GBNR_ECONFIG, "per-task Ybus sets need y_re and y_im");
+            v.yre = y_shared_re;
+            v.yim = y_shared_im;
+            v.y_ld = 1;
+            v.y_inc = 0;
+            return;
+        }
+        if (n_ysets == 1 || n_tasks == 1) {
+            CK(cudaMemcpyAsync(const_cast<double*>(y_shared_re), y_re, size_t(sym.nnzY) * 8,
+                               cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(const_cast<double*>(y_shared_im), y_im, size_t(sym.nnzY) * 8,
+                               cudaMemcpyHostToDevice, stream));
+            v.yre = y_shared_re;
+            v.yim = y_shared_im;
+            v.y_ld = 1;
+            v.y_inc = 0;
+            return;
+        }
+        if (n_ysets != n_tasks) throw Error(GBNR_ECONFIG, "n_ysets must be 1 or n_tasks");
+        const size_t bytes = size_t(sym.nnzY) * size_t(n_tasks) * 8;
+        if (bytes > y_task_cap) {
+            CK(cudaStreamSynchronize(stream));
+            if (y_task_re) cudaFree(y_task_re);
+            if (y_task_im) cudaFree(y_task_im);
+            y_task_re = y_task_im = nullptr;
+            CK(cudaMalloc(&y_task_re, bytes));
+            CK(cudaMalloc(&y_task_im, bytes));
+            y_task_cap = bytes;
+        }
+        CK(cudaMemcpyAsync(y_task_re, y_re, bytes, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(y_task_im, y_im, bytes, cudaMemcpyHostToDevice, stream));
+        v.yre = y_task_re;
+        v.yim = y_task_im;
+        v.y_ld = n_tasks;
+        v.y_inc = 1;
     }
 
     void ensure_capacity(int32_t n_tiles) {
@@ -409,7 +460,8 @@ struct gbnr_plan {
             if (convs && convs[j])
                 for (size_t t = 0; t < ntt; ++t) convs[j][t] = h_st[set][t] == GBNR_CONVERGED;
         };
-        // geometry and the shared start voltages (injections come per batch below)
+        // geometry, the plan's Ybus and the shared start voltages (injections come per batch below)
+        stage_ybus(nullptr, nullptr, 1, n_tasks);
         stage(n_tasks, nullptr, nullptr, 0, vm0, va0, 1);
         CK(cudaStreamSynchronize(stream));
         ensure_pipe(v.n_tiles);
@@ -550,6 +602,20 @@ int gbnr_build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* from, const 
     });
 }
 
+int gbnr_contingency_values(int32_t n_bus, int32_t n_branch, const int32_t* from, const int32_t* to,
+                            const double* r, const double* x, const double* b, const double* tap,
+                            const double* shift_deg, const uint8_t* in_service, const double* gs,
+                            const double* bs, double base_mva, const int32_t* outage_branch, int32_t n_tasks,
+                            double* y_re, double* y_im, uint8_t* islanded) {
+    return guarded([&] {
+        if (n_tasks <= 0) throw Error(GBNR_ECONFIG, "n_tasks must be positive");
+        const gbnr::YbusCsr y = gbnr::build_ybus(n_bus, n_branch, from, to, r, x, b, tap, shift_deg,
+                                                 in_service, gs, bs, base_mva);
+        gbnr::contingency_values(y, n_branch, from, to, in_service, outage_branch, n_tasks, y_re, y_im,
+                                 islanded);
+    });
+}
+
 int gbnr_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd) {
     return guarded([&] {
         const std::vector<int32_t> f = gbnr::amd_order(n, col_ptr, row_ix);
@@ -649,6 +715,7 @@ int gbnr_stage(gbnr_plan* p, int32_t n_tasks, const double* p0, const double* q0
                const double* vm0, const double* va0, int32_t n_vsets) {
     return guarded([&] {
         if (n_ssets < 1) throw Error(GBNR_ECONFIG, "n_ssets must be 1 or n_tasks");
+        if (p->on_device) p->stage_ybus(nullptr, nullptr, 1, n_tasks);  // the plan's shared set
         p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
     });
 }
@@ -671,17 +738,10 @@ int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* 
                double* va_out, int32_t* iterations_out, uint8_t* converged_out,
                int32_t* status_out, double* max_mismatch_out) {
     return guarded([&] {
-        if (n_ysets != 1)
-            throw Error(GBNR_ECONFIG, "per-task Ybus value sets (N-1 mode) are not supported yet");
         if (n_ssets < 1) throw Error(GBNR_ECONFIG, "n_ssets must be 1 or n_tasks");
-        if (y_re && y_im) {
-            // a different shared value set than the plan's: refresh it on the device
-            CK(cudaSetDevice(p->opt.device));
-            CK(cudaMemcpyAsync(const_cast<double*>(p->v.yre), y_re, size_t(p->sym.nnzY) * 8,
-                               cudaMemcpyHostToDevice, p->stream));
-            CK(cudaMemcpyAsync(const_cast<double*>(p->v.yim), y_im, size_t(p->sym.nnzY) * 8,
-                               cudaMemcpyHostToDevice, p->stream));
-        }
+        if (!p->on_device) throw Error(GBNR_ECONFIG, "host-only plan (device = -1) cannot solve");
+        CK(cudaSetDevice(p->opt.device));
+        p->stage_ybus(y_re, y_im, n_ysets, n_tasks);
         p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
         p->run();
         p->fetch(vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out);

@@ -63,6 +63,8 @@ YbusCsr build_ybus(int32_t n, int32_t nbr, const int32_t* f, const int32_t* t, c
     std::vector<cplx> v(nnz, cplx(0.0, 0.0));
     y.diag.resize(n);
     for (int32_t i = 0; i < n; ++i) y.diag[i] = find_sorted(y.indices, y.indptr[i], y.indptr[i + 1], i);
+    y.slot.resize(4 * static_cast<size_t>(nbr));
+    y.adm.resize(8 * static_cast<size_t>(nbr));
     for (int32_t k = 0; k < nbr; ++k) {
         cplx ff(0.0, 0.0), ft(0.0, 0.0), tf(0.0, 0.0), tt(0.0, 0.0);
         if (on[k]) {
@@ -74,10 +76,15 @@ YbusCsr build_ybus(int32_t n, int32_t nbr, const int32_t* f, const int32_t* t, c
             ft = -ys / std::conj(tc);
             tf = -ys / tc;
         }
-        v[y.diag[f[k]]] += ff;
-        v[find_sorted(y.indices, y.indptr[f[k]], y.indptr[f[k] + 1], t[k])] += ft;
-        v[find_sorted(y.indices, y.indptr[t[k]], y.indptr[t[k] + 1], f[k])] += tf;
-        v[y.diag[t[k]]] += tt;
+        const int32_t sl[4] = {y.diag[f[k]], find_sorted(y.indices, y.indptr[f[k]], y.indptr[f[k] + 1], t[k]),
+                               find_sorted(y.indices, y.indptr[t[k]], y.indptr[t[k] + 1], f[k]), y.diag[t[k]]};
+        const cplx a[4] = {ff, ft, tf, tt};
+        for (int q = 0; q < 4; ++q) {
+            v[sl[q]] += a[q];
+            y.slot[4 * size_t(k) + q] = sl[q];
+            y.adm[8 * size_t(k) + 2 * q] = a[q].real();
+            y.adm[8 * size_t(k) + 2 * q + 1] = a[q].imag();
+        }
     }
     for (int32_t i = 0; i < n; ++i) v[y.diag[i]] += cplx(gs[i], bs[i]) / base_mva;
     y.re.resize(nnz);
@@ -87,6 +94,74 @@ YbusCsr build_ybus(int32_t n, int32_t nbr, const int32_t* f, const int32_t* t, c
         y.im[s] = v[s].imag();
     }
     return y;
+}
+
+// ---------------------------------------------------------------------------
+// N-1 contingency value sets on the fixed pattern: ybus_values_with_outage
+// (grid.hpp:245-255) -- the outaged branch's four contributions subtracted from
+// the base values, complex arithmetic as the reference -- and the islanding
+// pre-check outage_islands_grid (grid.hpp:257-261): an in-service branch whose
+// removal disconnects the grid is a bridge (one Tarjan pass, parallel branches
+// counted as distinct edges).
+// ---------------------------------------------------------------------------
+void contingency_values(const YbusCsr& y, int32_t nbr, const int32_t* f, const int32_t* t, const uint8_t* on,
+                        const int32_t* outage, int32_t n_tasks, double* y_re, double* y_im, uint8_t* islanded) {
+    const int32_t n = y.n;
+    const size_t nnz = y.indices.size(), T = size_t(n_tasks);
+    // bridges of the in-service branch graph
+    std::vector<uint8_t> bridge(nbr, 0);
+    {
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> adj(n);  // (neighbour, branch)
+        for (int32_t k = 0; k < nbr; ++k)
+            if (on[k] && f[k] != t[k]) {
+                adj[f[k]].emplace_back(t[k], k);
+                adj[t[k]].emplace_back(f[k], k);
+            }
+        std::vector<int32_t> disc(n, -1), low(n, 0), it(n, 0), via(n, -1), stack;
+        int32_t timer = 0;
+        for (int32_t root = 0; root < n; ++root) {
+            if (disc[root] >= 0) continue;
+            disc[root] = low[root] = timer++;
+            stack.push_back(root);
+            while (!stack.empty()) {  // iterative DFS (grids are deep)
+                const int32_t u = stack.back();
+                if (it[u] < int32_t(adj[u].size())) {
+                    const auto [w, k] = adj[u][it[u]++];
+                    if (k == via[u]) continue;
+                    if (disc[w] < 0) {
+                        disc[w] = low[w] = timer++;
+                        via[w] = k;
+                        stack.push_back(w);
+                    } else {
+                        low[u] = std::min(low[u], disc[w]);
+                    }
+                } else {
+                    stack.pop_back();
+                    if (!stack.empty()) {
+                        const int32_t p = stack.back();
+                        low[p] = std::min(low[p], low[u]);
+                        if (low[u] > disc[p]) bridge[via[u]] = 1;
+                    }
+                }
+            }
+        }
+    }
+    for (size_t task = 0; task < T; ++task) {
+        const int32_t k = outage[task];
+        if (k >= nbr) throw Error(2, "outage branch out of range");
+        for (size_t q = 0; q < nnz; ++q) {
+            y_re[q * T + task] = y.re[q];
+            y_im[q * T + task] = y.im[q];
+        }
+        if (islanded) islanded[task] = k >= 0 && on[k] && bridge[k];
+        if (k < 0 || !on[k]) continue;  // no outage / out-of-service branch: the base values
+        for (int c = 0; c < 4; ++c) {
+            const size_t q = size_t(y.slot[4 * size_t(k) + c]);
+            const cplx v = cplx(y.re[q], y.im[q]) - cplx(y.adm[8 * size_t(k) + 2 * c], y.adm[8 * size_t(k) + 2 * c + 1]);
+            y_re[q * T + task] = v.real();
+            y_im[q * T + task] = v.imag();
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -29,6 +29,8 @@ struct YbusCsr {
     int32_t n = 0;
     std::vector<int32_t> indptr, indices, diag;
     std::vector<double> re, im;
+    std::vector<int32_t> slot;  // [4 * n_branch] slots of (ff, ft, tf, tt)
+    std::vector<double> adm;    // [8 * n_branch] (re, im) of the branch's (ff, ft, tf, tt)
 };
 
 YbusCsr build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* f, const int32_t* t,
@@ -37,6 +39,12 @@ YbusCsr build_ybus(int32_t n_bus, int32_t n_branch, const int32_t* f, const int3
                    double base_mva);
 
 std::vector<int32_t> amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix);
+
+// N-1 value sets (element-major [nnzY][n_tasks]) and islanding flags per task;
+// outage[task] = branch index, or -1 for the base case.
+void contingency_values(const YbusCsr& y, int32_t n_branch, const int32_t* from, const int32_t* to,
+                        const uint8_t* in_service, const int32_t* outage, int32_t n_tasks, double* y_re,
+                        double* y_im, uint8_t* islanded);
 
 struct Symbolic {
     // inputs

@@ -34,7 +34,7 @@ EXPORTS = ("gbnr_default_options", "gbnr_last_error", "gbnr_version", "gbnr_buil
            "gbnr_amd_order", "gbnr_plan_create", "gbnr_plan_destroy", "gbnr_plan_stats",
            "gbnr_plan_export", "gbnr_solve", "gbnr_stage", "gbnr_run", "gbnr_fetch",
            "gbnr_last_timing", "gbnr_refactor", "gbnr_walk_info", "gbnr_walk_export",
-           "gbnr_solve_batches")
+           "gbnr_solve_batches", "gbnr_contingency_values")
 
 
 class GbnrError(RuntimeError):
@@ -69,6 +69,9 @@ def lib() -> C.CDLL:
                                   _f64p, _u8p, _f64p, _f64p, C.c_double, _i32p, _i32p, _i32p,
                                   _f64p, _f64p, C.POINTER(C.c_int32)]
     L.gbnr_amd_order.argtypes = [C.c_int32, _i32p, _i32p, _i32p]
+    L.gbnr_contingency_values.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, _f64p, _f64p, _f64p, _f64p,
+                                          _f64p, _u8p, _f64p, _f64p, C.c_double, _i32p, C.c_int32,
+                                          _f64p, _f64p, _u8p]
     L.gbnr_plan_create.argtypes = [C.c_int32, _i32p, _i32p, _f64p, _f64p, C.c_int32, _i32p,
                                    C.c_int32, _i32p, C.c_int32, _f64p, _f64p, C.POINTER(Options),
                                    C.POINTER(C.c_void_p)]
@@ -136,6 +139,23 @@ def build_ybus(gc):
                                  C.byref(nnz)))
     m = nnz.value
     return indptr, indices[:m].copy(), diag, yre[:m].copy(), yim[:m].copy()
+
+
+def contingency_values(gc, outages):
+    """N-1 value sets (grid.hpp:245-261 via the C++ host): for every task the base
+    Ybus pattern's values with branch outages[t] removed (-1 = base case).
+    Returns (y_re, y_im) [nnzY][T] and islanded [T] (bool)."""
+    outages = _i32(outages)
+    T = len(outages)
+    nnz = int(build_ybus(gc)[0][-1])
+    yre = np.empty((nnz, T))
+    yim = np.empty((nnz, T))
+    isl = np.zeros(T, np.uint8)
+    _check(lib().gbnr_contingency_values(
+        gc.n_bus, gc.n_branch, _i32(gc.br_f), _i32(gc.br_t), _f64(gc.br_r), _f64(gc.br_x),
+        _f64(gc.br_b), _f64(gc.br_tap), _f64(gc.br_shift), np.ascontiguousarray(gc.br_on, np.uint8),
+        _f64(gc.gs), _f64(gc.bs), float(gc.base_mva), outages, T, yre, yim, isl))
+    return yre, yim, isl.astype(bool)
 
 
 def amd_order(n, col_ptr, row_ix) -> np.ndarray:
@@ -234,11 +254,30 @@ class NrPlan:
                                 _ptr(r.converged), _ptr(r.status), _ptr(r.max_mismatch)))
         return r
 
-    def solve(self, p0, q0, vm0, va0, n_tasks: int | None = None) -> TaskResults:
-        """``nr_solve_batch`` (SPEC.md:213-221): stage (H2D), solve, fetch (D2H)."""
-        self.stage(p0, q0, vm0, va0, n_tasks)
-        self.run()
-        return self.fetch()
+    def solve(self, p0, q0, vm0, va0, n_tasks: int | None = None, y=None) -> TaskResults:
+        """``nr_solve_batch`` through gbnr_solve: H2D, solve, D2H.
+        ``y`` = (y_re, y_im) [nnzY] (a new shared value set) or [nnzY][T] (one per
+        task, e.g. N-1 contingencies from ``contingency_values``)."""
+        p0 = _f64(p0); vm0 = _f64(vm0)
+        if n_tasks is None:
+            n_tasks = max(p0.shape[1] if p0.ndim == 2 else 1, vm0.shape[1] if vm0.ndim == 2 else 1)
+        p0, ns = self._sets(p0, n_tasks)
+        q0, _ = self._sets(q0, n_tasks)
+        vm0, nv = self._sets(vm0, n_tasks)
+        va0, _ = self._sets(va0, n_tasks)
+        yre = yim = None
+        ny = 1
+        if y is not None:
+            yre, yim = _f64(y[0]), _f64(y[1])
+            ny = yre.shape[1] if yre.ndim == 2 else 1
+        n, T = self.n_bus, n_tasks
+        r = TaskResults(np.empty((n, T)), np.empty((n, T)), np.empty(T, np.int32),
+                        np.empty(T, np.uint8), np.empty(T, np.int32), np.empty(T))
+        _check(lib().gbnr_solve(self.h, T, _ptr(yre), _ptr(yim), ny, _ptr(p0), _ptr(q0), ns,
+                                _ptr(vm0), _ptr(va0), nv, _ptr(r.vm), _ptr(r.va), _ptr(r.iterations),
+                                _ptr(r.converged), _ptr(r.status), _ptr(r.max_mismatch)))
+        self._n_tasks = T
+        return r
 
     def solve_batches(self, p0s, q0s, vm0, va0, outs=None):
         """Pipelined sequence of batches (gbnr_solve_batches): per-task injections

@@ -86,6 +86,25 @@ def test_jacobian_pattern_and_amd(name, orc):
     np.testing.assert_array_equal(S.amd_order(nJ, cp, ri), g["amd_fwd"])
 
 
+@pytest.mark.parametrize("name", CASES)
+def test_contingency_values_bitwise(name):
+    """N-1 value sets on the fixed pattern (ybus_values_with_outage, grid.hpp:245-255)
+    and the islanding pre-check (outage_islands_grid, grid.hpp:257-261) against the
+    reference's own functions."""
+    g = gold(name)
+    gc = load_case(util.case_path(name))
+    br = g["outage_branches"]
+    yre, yim, isl = S.contingency_values(gc, np.r_[br, -1])
+    np.testing.assert_array_equal(yre[:, :-1], g["outage_y_re"])
+    np.testing.assert_array_equal(yim[:, :-1], g["outage_y_im"])
+    np.testing.assert_array_equal(isl[:-1], g["outage_islands"].astype(bool))
+    np.testing.assert_array_equal(yre[:, -1], g["y_re"])  # -1 = the base case
+    np.testing.assert_array_equal(yim[:, -1], g["y_im"])
+    if len(g["islands_all"]):
+        _, _, isl_all = S.contingency_values(gc, np.arange(gc.n_branch))
+        np.testing.assert_array_equal(isl_all, g["islands_all"].astype(bool))
+
+
 def test_amd_kats():
     """SPEC.md:289 (diagonal -> identity) and :290 (arrow: zero fill; the reference
     puts the hub at n-2 because of its lowest-index tie-break)."""

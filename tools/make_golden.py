@@ -11,6 +11,9 @@ Runs the reference's own header-only substrate, compiled in place from
                     table), vm_start, va_start (the V0 rule :331-342)
   * amd_order       amd.hpp:29-157     -> forward permutation of the reduced
                     Jacobian pattern (built by tests/util.py)
+  * ybus_values_with_outage grid.hpp:245-255 -> N-1 value sets for a few branches,
+    outage_islands_grid grid.hpp:257-261 -> the islanding pre-check (every branch
+    where the case is small enough)
   * the SPEC.md known-answer examples of sparse_core
 
 /root/reference does not exist on the GPU box; the fixtures are committed and
@@ -46,10 +49,20 @@ def case_golden(ref: po.Reference, name: str) -> dict:
     p3, q3, _, _ = rc.profiles(p_mw[:, None] * scale, q_mvar[:, None] * scale)
     nJ, cp, ri = util.j_pattern_ccs(rc.n_bus, ip, ix, rc.slack, pv, pq)
     fwd = ref.amd(nJ, cp, ri)
+    # N-1: ybus_values_with_outage for some branches, islanding for every branch
+    nb = rc.n_branch
+    pick = np.arange(nb) if nb <= 64 else np.unique(np.r_[0, 1, nb // 2, nb - 1,
+                                                          np.random.default_rng(7).integers(0, nb, 4)])
+    outs = [rc.outage(int(b)) for b in pick]
+    islands = np.array([rc.outage(b)[2] for b in range(nb)], np.uint8) if nb <= 4096 else \
+        np.array([], np.uint8)
     return dict(n_bus=rc.n_bus, n_branch=rc.n_branch, slack=rc.slack, pv=pv, pq=pq,
                 indptr=ip, indices=ix, diag=dg, y_re=yr, y_im=yi, p_mw=p_mw, q_mvar=q_mvar,
                 p0=p0[:, 0], q0=q0[:, 0], p0_3=p3, q0_3=q3, scale_3=scale, vm_start=vm0,
-                va_start=va0, nJ=nJ, j_col_ptr=cp, j_row_ix=ri, amd_fwd=fwd)
+                va_start=va0, nJ=nJ, j_col_ptr=cp, j_row_ix=ri, amd_fwd=fwd,
+                outage_branches=pick.astype(np.int32),
+                outage_y_re=np.stack([o[0] for o in outs], 1), outage_y_im=np.stack([o[1] for o in outs], 1),
+                outage_islands=np.array([o[2] for o in outs], np.uint8), islands_all=islands)
 
 
 def sparse_kats(ref: po.Reference) -> dict:
