@@ -18,6 +18,9 @@
  *   gbnr_amd_order     <- amd_order (amd.hpp:29-157)
  *   gbnr_plan_stats    <- cmd_inspect counters
  *   gbnr_refactor      <- refactorize_batch, LU-only microbenchmark
+ *   gbnr_solve_batches <- batch_runtime.run over mini-batches, pipelined
+ *   gbnr_contingency_values <- ybus_values_with_outage / outage_islands_grid (grid.hpp:245-261)
+ *   gbnr_branch_flows  <- calc_branch_flows
  *
  * Conventions
  *  - Batched arrays are element-major with the task index innermost
@@ -98,6 +101,13 @@ int gbnr_contingency_values(int32_t n_bus, int32_t n_branch, const int32_t* from
                             const double* bs, double base_mva, const int32_t* outage_branch, int32_t n_tasks,
                             double* y_re, double* y_im, uint8_t* islanded);
 
+/* Per-branch admittances adm [n_branch][8]: (ff, ft, tf, tt) as (re, im),
+ * zero for out-of-service branches (branch_admittance, grid.hpp:195-206). */
+int gbnr_branch_admittances(int32_t n_bus, int32_t n_branch, const int32_t* from, const int32_t* to,
+                            const double* r, const double* x, const double* b, const double* tap,
+                            const double* shift_deg, const uint8_t* in_service, const double* gs,
+                            const double* bs, double base_mva, double* adm);
+
 /* Fill-reducing ordering on a square CCS pattern (amd.hpp:29-157); fwd[old] = new. */
 int gbnr_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd);
 
@@ -153,6 +163,16 @@ int gbnr_solve_batches(gbnr_plan* plan, int32_t n_batches, int32_t n_tasks, cons
                        const double* const* q0, const double* vm0, const double* va0, double* const* vm_out,
                        double* const* va_out, int32_t* const* iterations_out, uint8_t* const* converged_out,
                        int32_t* const* status_out, double* const* max_mismatch_out);
+
+/* calc_branch_flows on the voltages of the last solve of
+ * `plan` (still on the device): S_from = V_f conj(Yff V_f + Yft V_t), S_to =
+ * V_t conj(Ytf V_f + Ytt V_t) per branch and task, zero for the task's outaged
+ * branch (outage_branch [n_tasks] or NULL); outputs [n_branch][n_tasks]
+ * element-major (any may be NULL).  Computed for every task (diverged ones
+ * included); status_out of the solve flags them. */
+int gbnr_branch_flows(gbnr_plan* plan, int32_t n_branch, const int32_t* from, const int32_t* to,
+                      const double* adm, const int32_t* outage_branch, double* sf_re, double* sf_im,
+                      double* st_re, double* st_im);
 
 /* Per-kernel device time of the last gbnr_run/gbnr_solve (CUDA events on the
  * solver stream).  out[24]: [0..4] ms of npm, jacobian, lu, fsbs, vupdate when

@@ -1094,3 +1094,42 @@ int orc_mismatch(const orc_plan* P, int32_t n_tasks, const double* p0, const dou
     free(c); free(s); free(vmt);
     return 0;
 }
+
+/* calc_branch_flows: S_from = V_f conj(Yff V_f + Yft V_t),
+ * S_to = V_t conj(Ytf V_f + Ytt V_t), zero for the task's outaged branch; the
+ * operation sequence of the CUDA path (numerics.cuh branch_flow). */
+int orc_branch_flows(int32_t n_bus, int32_t n_branch, const int32_t* f, const int32_t* t,
+                     const double* adm, int32_t n_tasks, const double* vm, const double* va,
+                     const int32_t* outage, double* sf_re, double* sf_im, double* st_re, double* st_im) {
+    for (int32_t task = 0; task < n_tasks; ++task) {
+        for (int32_t k = 0; k < n_branch; ++k) {
+            const size_t o = (size_t)k * n_tasks + task;
+            if (outage && outage[task] == k) {
+                sf_re[o] = sf_im[o] = st_re[o] = st_im[o] = 0.0;
+                continue;
+            }
+            double sfv, cfv, stv, ctv;
+            orc_sincos(va[(size_t)f[k] * n_tasks + task], &sfv, &cfv);
+            orc_sincos(va[(size_t)t[k] * n_tasks + task], &stv, &ctv);
+            const double vmf = vm[(size_t)f[k] * n_tasks + task], vmt = vm[(size_t)t[k] * n_tasks + task];
+            const double vfr = vmf * cfv, vfi = vmf * sfv, vtr = vmt * ctv, vti = vmt * stv;
+            const double* a = adm + (size_t)8 * k;
+            double ire = 0.0, iim = 0.0;
+            ire = fma(a[0], vfr, ire); ire = fma(-a[1], vfi, ire);
+            iim = fma(a[0], vfi, iim); iim = fma(a[1], vfr, iim);
+            ire = fma(a[2], vtr, ire); ire = fma(-a[3], vti, ire);
+            iim = fma(a[2], vti, iim); iim = fma(a[3], vtr, iim);
+            sf_re[o] = fma(vfr, ire, vfi * iim);
+            sf_im[o] = fma(vfi, ire, -(vfr * iim));
+            ire = 0.0; iim = 0.0;
+            ire = fma(a[4], vfr, ire); ire = fma(-a[5], vfi, ire);
+            iim = fma(a[4], vfi, iim); iim = fma(a[5], vfr, iim);
+            ire = fma(a[6], vtr, ire); ire = fma(-a[7], vti, ire);
+            iim = fma(a[6], vti, iim); iim = fma(a[7], vtr, iim);
+            st_re[o] = fma(vtr, ire, vti * iim);
+            st_im[o] = fma(vti, ire, -(vtr * iim));
+        }
+    }
+    (void)n_bus;
+    return 0;
+}

@@ -14,6 +14,7 @@
  *   orc_solve           SPEC.md:195-230 (compute_npm, update_jacobian,
  *                       update_voltage), :213-221 (nr_solve_batch), :310-318
  *                       (refactorize_batch = PAPER.md Alg. 2), :328-336 (fs_bs_batch)
+ *   orc_branch_flows    SPEC.md:231-239 (calc_branch_flows)
  *   worker pool + mini-batches: SPEC.md:254-255, batch_tape.hpp:80-92
  *
  * Parity status: the substrate (Ybus, profiles, AMD ordering, CRS/CCS/scatter)
@@ -82,6 +83,13 @@ int orc_refactor(const orc_plan* p, int32_t n_tasks, const double* vm, const dou
  * f_out [nJ][n_tasks] in J row order [P(pv;pq); Q(pq)]. */
 int orc_mismatch(const orc_plan* p, int32_t n_tasks, const double* p0, const double* q0,
                  const double* vm, const double* va, double* f_out);
+
+/* calc_branch_flows for voltages vm/va [n_bus][n_tasks];
+ * adm [n_branch][8] = (ff, ft, tf, tt) as (re, im); outage [n_tasks] or NULL;
+ * outputs [n_branch][n_tasks]. */
+int orc_branch_flows(int32_t n_bus, int32_t n_branch, const int32_t* f, const int32_t* t,
+                     const double* adm, int32_t n_tasks, const double* vm, const double* va,
+                     const int32_t* outage, double* sf_re, double* sf_im, double* st_re, double* st_im);
 
 #ifdef __cplusplus
 }

@@ -63,6 +63,8 @@ class Oracle:
         L.orc_refactor.argtypes = [C.c_void_p, C.c_int32, _f64p, _f64p, C.c_double, _f64p, _u8p,
                                    C.c_int32]
         L.orc_mismatch.argtypes = [C.c_void_p, C.c_int32, _f64p, _f64p, _f64p, _f64p, _f64p]
+        L.orc_branch_flows.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, _f64p, C.c_int32, _f64p,
+                                       _f64p, C.c_void_p, _f64p, _f64p, _f64p, _f64p]
 
     def _check(self, rc):
         if rc != 0:
@@ -89,6 +91,18 @@ class Oracle:
             C.byref(nnz)))
         m = nnz.value
         return indptr, indices[:m].copy(), diag, yre[:m].copy(), yim[:m].copy()
+
+    def branch_flows(self, gc, adm, vm, va, outage=None):
+        """calc_branch_flows (SPEC.md:231-239): (S_from, S_to) complex [n_branch][T]."""
+        vm = _f64(vm); va = _f64(va)
+        T = vm.shape[1]
+        nb = gc.n_branch
+        out = [np.zeros((nb, T)) for _ in range(4)]
+        oa = None if outage is None else _i32(outage)
+        self._check(self.lib.orc_branch_flows(
+            gc.n_bus, nb, _i32(gc.br_f), _i32(gc.br_t), _f64(adm), T, vm, va,
+            None if oa is None else oa.ctypes.data_as(C.c_void_p), *out))
+        return out[0] + 1j * out[1], out[2] + 1j * out[3]
 
     def amd(self, n, col_ptr, row_ix):
         fwd = np.zeros(n, np.int32)
@@ -204,6 +218,18 @@ class Reference:
         if rc.value != 0:
             raise OracleError(f"ref parse error {rc.value}: {self.err()}")
         return RefCase(self, h)
+
+    def branch_flows(self, gc, adm, vm, va, outage=None):
+        """calc_branch_flows (SPEC.md:231-239): (S_from, S_to) complex [n_branch][T]."""
+        vm = _f64(vm); va = _f64(va)
+        T = vm.shape[1]
+        nb = gc.n_branch
+        out = [np.zeros((nb, T)) for _ in range(4)]
+        oa = None if outage is None else _i32(outage)
+        self._check(self.lib.orc_branch_flows(
+            gc.n_bus, nb, _i32(gc.br_f), _i32(gc.br_t), _f64(adm), T, vm, va,
+            None if oa is None else oa.ctypes.data_as(C.c_void_p), *out))
+        return out[0] + 1j * out[1], out[2] + 1j * out[3]
 
     def amd(self, n, col_ptr, row_ix):
         fwd = np.zeros(n, np.int32)

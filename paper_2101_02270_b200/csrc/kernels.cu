@@ -645,6 +645,40 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     }
 }
 
+// calc_branch_flows on the solved voltages: block (32-branch
+// chunk, super-tile), warp = tile; outputs [n_branch][n_tasks] packed.
+__global__ void __launch_bounds__(256) flows_kernel(DevView v, int32_t nb, const int32_t* bf, const int32_t* bt,
+                                                    const double* adm, const int32_t* outage, double* sfr,
+                                                    double* sfi, double* str, double* sti) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.y * kSuper + warp;
+    if (tile >= v.n_tiles) return;
+    const int t = tile * kTile + lane;
+    if (t >= v.n_tasks) return;
+    const size_t bp = v.bpad, T = size_t(v.n_tasks);
+    const int out = outage ? outage[t] : -1;
+    const int k1 = min(nb, int(blockIdx.x + 1) * 32);
+    for (int k = blockIdx.x * 32; k < k1; ++k) {
+        const size_t o = size_t(k) * T + t;
+        if (k == out) {
+            sfr[o] = sfi[o] = str[o] = sti[o] = 0.0;
+            continue;
+        }
+        const int f = __ldg(bf + k), to = __ldg(bt + k);
+        const double vmf = v.vm[f * bp + t], vmt = v.vm[to * bp + t];
+        const double vfr = vmf * v.c[f * bp + t], vfi = vmf * v.s[f * bp + t];
+        const double vtr = vmt * v.c[to * bp + t], vti = vmt * v.s[to * bp + t];
+        const double* a = adm + size_t(8) * k;
+        double P, Q;
+        branch_end_flow(__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3), vfr, vfi, vtr, vti, vfr, vfi, P, Q);
+        sfr[o] = P;
+        sfi[o] = Q;
+        branch_end_flow(__ldg(a + 4), __ldg(a + 5), __ldg(a + 6), __ldg(a + 7), vfr, vfi, vtr, vti, vtr, vti, P, Q);
+        str[o] = P;
+        sti[o] = Q;
+    }
+}
+
 // [n][bpad] -> [n][n_tasks] (packed for a single linear D2H copy)
 __global__ void pack_kernel(double* __restrict__ dst, const double* __restrict__ src, int32_t n, int32_t n_tasks,
                             int32_t bpad) {
@@ -717,6 +751,12 @@ void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st) {
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {
     vupdate_kernel<<<dim3(unsigned((v.n + 31) / 32), n_super(v)), 256, 0, st>>>(v);
+}
+
+void launch_flows(const DevView& v, int32_t nb, const int32_t* bf, const int32_t* bt, const double* adm,
+                  const int32_t* outage, double* sfr, double* sfi, double* str, double* sti, cudaStream_t st) {
+    flows_kernel<<<dim3(unsigned((nb + 31) / 32), n_super(v)), 256, 0, st>>>(v, nb, bf, bt, adm, outage, sfr, sfi,
+                                                                          str, sti);
 }
 
 void launch_pack(double* dst, const double* src, int32_t n, int32_t n_tasks, int32_t bpad, cudaStream_t st) {

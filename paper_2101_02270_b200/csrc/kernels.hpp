@@ -64,5 +64,7 @@ void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st);
 void launch_vupdate(const DevView& v, cudaStream_t st);
 void launch_broadcast(double* dst, const double* src, int32_t n, int32_t bpad, cudaStream_t st);
 void launch_pack(double* dst, const double* src, int32_t n, int32_t n_tasks, int32_t bpad, cudaStream_t st);
+void launch_flows(const DevView& v, int32_t nb, const int32_t* bf, const int32_t* bt, const double* adm,
+                  const int32_t* outage, double* sfr, double* sfi, double* str, double* sti, cudaStream_t st);
 
 }  // namespace gbnr

@@ -92,4 +92,13 @@ GB_HD void jac_entries(bool diag, double zre, double zim, double vmk, double ck,
     }
 }
 
+// Branch flow S = V_a conj(Y_a V_f + Y_b V_t) of one branch end.
+GB_HD void branch_end_flow(double ar, double ai, double br, double bi, double vfr, double vfi, double vtr,
+                           double vti, double var, double vai, double& P, double& Q) {
+    double ire = 0.0, iim = 0.0;
+    acc_current(ar, ai, vfr, vfi, ire, iim);
+    acc_current(br, bi, vtr, vti, ire, iim);
+    injection(var, vai, ire, iim, P, Q);
+}
+
 }  // namespace gbnr

@@ -90,6 +90,7 @@ struct gbnr_plan {
     std::vector<void*> batch;     // per-batch tapes
     int32_t cap_tiles = 0;        // allocated tile capacity
     bool staged = false;
+    bool solved = false;  // device voltages hold a finished solve
     gbnr::DevView v{};
     int32_t* h_count = nullptr;   // pinned, mapped (device writes counters here)
     double timing[24] = {0};
@@ -408,6 +409,7 @@ struct gbnr_plan {
         timing[12] = it_done;
         timing[13] = v.n_tasks;
         timing[19] = double(launches_per_iteration()) * it_done + 4;  // kernels launched
+        solved = true;
     }
 
     void ensure_pipe(int32_t n_tiles) {
@@ -533,6 +535,40 @@ struct gbnr_plan {
             for (int32_t t = 0; t < nt; ++t) conv[t] = st[t] == GBNR_CONVERGED;
     }
 
+    // calc_branch_flows on the voltages of the last solve (device-resident)
+    void branch_flows(int32_t nb, const int32_t* bf, const int32_t* bt, const double* adm, const int32_t* outage,
+                      double* sfr, double* sfi, double* str, double* sti) {
+        if (!solved) throw Error(GBNR_ECONFIG, "gbnr_branch_flows before a solve");
+        CK(cudaSetDevice(opt.device));
+        const size_t T = size_t(v.n_tasks), out_bytes = size_t(nb) * T * 8;
+        std::vector<void*> tmp;
+        auto up = [&](const void* h, size_t bytes) {
+            void* d = nullptr;
+            CK(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
+            tmp.push_back(d);
+            if (h) CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
+            return d;
+        };
+        try {
+            auto* dbf = static_cast<const int32_t*>(up(bf, size_t(nb) * 4));
+            auto* dbt = static_cast<const int32_t*>(up(bt, size_t(nb) * 4));
+            auto* dadm = static_cast<const double*>(up(adm, size_t(nb) * 64));
+            auto* dout = outage ? static_cast<const int32_t*>(up(outage, T * 4)) : nullptr;
+            double* o[4];
+            for (auto& q : o) q = static_cast<double*>(up(nullptr, out_bytes));
+            gbnr::launch_flows(v, nb, dbf, dbt, dadm, dout, o[0], o[1], o[2], o[3], stream);
+            CK(cudaGetLastError());
+            double* h[4] = {sfr, sfi, str, sti};
+            for (int i = 0; i < 4; ++i)
+                if (h[i]) CK(cudaMemcpyAsync(h[i], o[i], out_bytes, cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+        } catch (...) {
+            for (void* q : tmp) cudaFree(q);
+            throw;
+        }
+        for (void* q : tmp) cudaFree(q);
+    }
+
     void refactor(int32_t reps, double* lu_out, uint8_t* flags_out, double* ms_out) {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_refactor before gbnr_stage");
         CK(cudaSetDevice(opt.device));
@@ -613,6 +649,29 @@ int gbnr_contingency_values(int32_t n_bus, int32_t n_branch, const int32_t* from
                                                  in_service, gs, bs, base_mva);
         gbnr::contingency_values(y, n_branch, from, to, in_service, outage_branch, n_tasks, y_re, y_im,
                                  islanded);
+    });
+}
+
+int gbnr_branch_admittances(int32_t n_bus, int32_t n_branch, const int32_t* from, const int32_t* to,
+                            const double* r, const double* x, const double* b, const double* tap,
+                            const double* shift_deg, const uint8_t* in_service, const double* gs,
+                            const double* bs, double base_mva, double* adm) {
+    return guarded([&] {
+        const gbnr::YbusCsr y = gbnr::build_ybus(n_bus, n_branch, from, to, r, x, b, tap, shift_deg,
+                                                 in_service, gs, bs, base_mva);
+        std::memcpy(adm, y.adm.data(), y.adm.size() * sizeof(double));
+    });
+}
+
+int gbnr_branch_flows(gbnr_plan* p, int32_t n_branch, const int32_t* from, const int32_t* to,
+                      const double* adm, const int32_t* outage_branch, double* sf_re, double* sf_im,
+                      double* st_re, double* st_im) {
+    return guarded([&] {
+        if (!p->on_device) throw Error(GBNR_ECONFIG, "host-only plan (device = -1) has no voltages");
+        for (int32_t k = 0; k < n_branch; ++k)
+            if (from[k] < 0 || from[k] >= p->sym.n || to[k] < 0 || to[k] >= p->sym.n)
+                throw Error(GBNR_ESTRUCT, "branch endpoint out of range");
+        p->branch_flows(n_branch, from, to, adm, outage_branch, sf_re, sf_im, st_re, st_im);
     });
 }
 

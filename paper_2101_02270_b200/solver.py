@@ -34,7 +34,8 @@ EXPORTS = ("gbnr_default_options", "gbnr_last_error", "gbnr_version", "gbnr_buil
            "gbnr_amd_order", "gbnr_plan_create", "gbnr_plan_destroy", "gbnr_plan_stats",
            "gbnr_plan_export", "gbnr_solve", "gbnr_stage", "gbnr_run", "gbnr_fetch",
            "gbnr_last_timing", "gbnr_refactor", "gbnr_walk_info", "gbnr_walk_export",
-           "gbnr_solve_batches", "gbnr_contingency_values")
+           "gbnr_solve_batches", "gbnr_contingency_values", "gbnr_branch_admittances",
+           "gbnr_branch_flows")
 
 
 class GbnrError(RuntimeError):
@@ -69,6 +70,9 @@ def lib() -> C.CDLL:
                                   _f64p, _u8p, _f64p, _f64p, C.c_double, _i32p, _i32p, _i32p,
                                   _f64p, _f64p, C.POINTER(C.c_int32)]
     L.gbnr_amd_order.argtypes = [C.c_int32, _i32p, _i32p, _i32p]
+    L.gbnr_branch_admittances.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, _f64p, _f64p, _f64p, _f64p,
+                                          _f64p, _u8p, _f64p, _f64p, C.c_double, _f64p]
+    L.gbnr_branch_flows.argtypes = [C.c_void_p, C.c_int32, _i32p, _i32p, _f64p, C.c_void_p] + [C.c_void_p] * 4
     L.gbnr_contingency_values.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, _f64p, _f64p, _f64p, _f64p,
                                           _f64p, _u8p, _f64p, _f64p, C.c_double, _i32p, C.c_int32,
                                           _f64p, _f64p, _u8p]
@@ -156,6 +160,16 @@ def contingency_values(gc, outages):
         _f64(gc.br_b), _f64(gc.br_tap), _f64(gc.br_shift), np.ascontiguousarray(gc.br_on, np.uint8),
         _f64(gc.gs), _f64(gc.bs), float(gc.base_mva), outages, T, yre, yim, isl))
     return yre, yim, isl.astype(bool)
+
+
+def branch_admittances(gc) -> np.ndarray:
+    """[n_branch][8] (ff, ft, tf, tt) as (re, im) -- grid.hpp:195-206 via the C++ host."""
+    adm = np.zeros((gc.n_branch, 8))
+    _check(lib().gbnr_branch_admittances(
+        gc.n_bus, gc.n_branch, _i32(gc.br_f), _i32(gc.br_t), _f64(gc.br_r), _f64(gc.br_x),
+        _f64(gc.br_b), _f64(gc.br_tap), _f64(gc.br_shift), np.ascontiguousarray(gc.br_on, np.uint8),
+        _f64(gc.gs), _f64(gc.bs), float(gc.base_mva), adm))
+    return adm
 
 
 def amd_order(n, col_ptr, row_ix) -> np.ndarray:
@@ -301,6 +315,17 @@ class NrPlan:
             arr([o.converged for o in outs]), arr([o.status for o in outs]),
             arr([o.max_mismatch for o in outs])))
         return outs
+
+    def branch_flows(self, gc, outages=None):
+        """calc_branch_flows on the last solve: (S_from, S_to)
+        complex [n_branch][T]; loading percent = 100 |S| / (rateA / baseMVA)."""
+        nb, T = gc.n_branch, self._n_tasks
+        adm = branch_admittances(gc)
+        out = [np.empty((nb, T)) for _ in range(4)]
+        oa = None if outages is None else _i32(outages)
+        _check(lib().gbnr_branch_flows(self.h, nb, _i32(gc.br_f), _i32(gc.br_t), adm, _ptr(oa),
+                                       *[_ptr(o) for o in out]))
+        return out[0] + 1j * out[1], out[2] + 1j * out[3]
 
     def timing(self) -> dict:
         out = np.zeros(24)

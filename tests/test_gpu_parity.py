@@ -166,3 +166,24 @@ def test_n1_contingency_matches_oracle(name, T):
     # the shared-Ybus path is untouched afterwards
     rs = plan.solve(p0, q0, vm0, va0)
     _compare(rs, oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
+
+
+@pytest.mark.parametrize("name,n1", [("case14", False), ("synth300", False), ("synth300", True)])
+def test_branch_flows_match_oracle(name, n1):
+    """calc_branch_flows on the device voltages of the last solve, bit-identical to
+    the oracle (N-1: the outaged branch carries no flow)."""
+    gc, plan, oplan, vm0, va0 = _setup(name)
+    T = 96
+    p0, q0 = montecarlo(gc, T)
+    outages = np.random.default_rng(5).integers(0, gc.n_branch, T).astype(np.int32) if n1 else None
+    y = None
+    if n1:
+        yre, yim, _ = S.contingency_values(gc, outages)
+        y = (yre, yim)
+    r = plan.solve(p0, q0, vm0, va0, y=y)
+    sf, st = plan.branch_flows(gc, outages)
+    osf, ost = po.Oracle().branch_flows(gc, S.branch_admittances(gc), r.vm, r.va, outage=outages)
+    np.testing.assert_array_equal(sf, osf)
+    np.testing.assert_array_equal(st, ost)
+    if n1:
+        assert (sf[outages, np.arange(T)] == 0).all()

@@ -165,3 +165,30 @@ def test_case14_montecarlo_iteration_split():
     assert (r["status"] == 0).all()
     assert set(np.unique(r["iterations"])) <= {2, 3}
     assert (r["max_mismatch"] < 1e-8).all()
+
+
+def test_branch_flows_oracle_kats():
+    """calc_branch_flows in the oracle: dense restatement, lossless
+    lines conserve real power, the whole grid balances, an outaged branch carries 0."""
+    from paper_2101_02270_b200 import solver as S
+    gc, plan, Y, vm0, va0 = setup("case14")
+    p0, q0 = gc.profiles(gc.pd, gc.qd)
+    r = plan.solve(p0, q0, vm0[:, None], va0[:, None])
+    adm = S.branch_admittances(gc)
+    sf, st = po.Oracle().branch_flows(gc, adm, r["vm"], r["va"])
+    V = r["vm"][:, 0] * np.exp(1j * r["va"][:, 0])
+    a = adm[:, 0::2] + 1j * adm[:, 1::2]  # ff, ft, tf, tt
+    Vf, Vt = V[gc.br_f], V[gc.br_t]
+    np.testing.assert_allclose(sf[:, 0], Vf * np.conj(a[:, 0] * Vf + a[:, 1] * Vt), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(st[:, 0], Vt * np.conj(a[:, 2] * Vf + a[:, 3] * Vt), rtol=0, atol=1e-12)
+    lossless = (gc.br_r == 0) & (gc.br_b == 0)
+    assert lossless.any()
+    np.testing.assert_allclose(sf[lossless, 0].real, -st[lossless, 0].real, atol=1e-12)
+    Sbus = V * np.conj(Y @ V)  # injections = branch flows + shunts
+    shunt = np.conj((gc.gs + 1j * gc.bs) / gc.base_mva) * np.abs(V) ** 2
+    total = np.zeros(gc.n_bus, complex)
+    np.add.at(total, gc.br_f, sf[:, 0])
+    np.add.at(total, gc.br_t, st[:, 0])
+    np.testing.assert_allclose(total + shunt, Sbus, atol=1e-10)
+    sf2, st2 = po.Oracle().branch_flows(gc, adm, r["vm"], r["va"], outage=np.array([3], np.int32))
+    assert sf2[3, 0] == 0 and st2[3, 0] == 0 and sf2[2, 0] == sf[2, 0]
