@@ -394,16 +394,15 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     double* x = P.R;
     int len = 0, dp = 0, lslot = 0, brow = 0;
     double acc_y = 0.0;
+    int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
     for (;;) {
         const int32_t* r = P.cur;
-        const int32_t h = r[0];
         const int type = h & 15;
-        if (type == kRecIssue) {
-            P.cur += prog_issue(v, P, r, lane);
-        } else if (type == kRecDep) {
+        if (type == kRecDep) {
             const int op = (h >> 4) - 1;
             const int kpos_fs = r[1], nrows = r[2] & 0xffff, src_row = int(unsigned(r[2]) >> 16);
             const int ysrc = r[3];
+            h = r[4 + ((nrows + 1) >> 1)];
             if (op >= 0) prog_wait(P, op);
             const double* src = P.R + size_t(src_row) * kTile + lane;
             if (nrows > 0) {
@@ -477,6 +476,9 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 if (fspos != 0xffff) acc_y = fma(-src[fspos * kTile], P.R[size_t(ysrc) * kTile + lane], acc_y);
             }
             P.cur += 4 + ((nrows + 1) >> 1);
+        } else if (type == kRecIssue) {
+            P.cur += prog_issue(v, P, r, lane);
+            h = P.cur[0];
         } else if (type == kRecStep) {
             const int ring = r[1] & 0xffff;
             len = int(unsigned(r[1]) >> 16);
@@ -484,11 +486,13 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             lslot = r[3];
             brow = r[4];
             const int op = r[5];
+            h = r[6];
             P.cur += 6;
             prog_wait(P, op);
             x = P.R + size_t(ring) * kTile + lane;
             acc_y = FS ? x[len * kTile] : 0.0;
         } else if (type == kRecEnd) {
+            h = r[1 + dp];
             // normalization L = x * (1 / pivot) and the U scatter, with the
             // pivot check's column maximum folded into the same
             // passes over x (max |x| is exact in any order)
@@ -544,10 +548,12 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             P.cur += 1 + dp;
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
+            h = P.cur[0];
         } else if (type == kRecSync) {
             walk_trace(v, tile, warp, lane, 0);
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             P.cur += 1;
+            h = P.cur[0];
         } else {
             walk_trace(v, tile, warp, lane, 1);
             break;
@@ -567,30 +573,35 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     double* blk = P.R;
     int ne = 0, e = 0, brow = 0;
     double acc = 0.0;
+    int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
     for (;;) {
         const int32_t* r = P.cur;
-        const int32_t h = r[0];
         const int type = h & 15;
-        if (type == kRecIssue) {
-            P.cur += prog_issue(v, P, r, lane);
-        } else if (type == kRecDep) {
+        if (type == kRecDep) {
             const int op = (h >> 4) - 1;
             const int ysrc = r[1];
+            h = r[2];
             if (op >= 0) prog_wait(P, op);
             acc = fma(-blk[e * kTile], P.R[size_t(ysrc) * kTile + lane], acc);
             ++e;
             P.cur += 2;
+        } else if (type == kRecIssue) {
+            const int len = prog_issue(v, P, r, lane);
+            P.cur += len;
+            h = P.cur[0];
         } else if (type == kRecStep) {
             const int ring = r[1] & 0xffff;
             ne = int(unsigned(r[1]) >> 16);
             brow = r[4];
             const int op = r[5];
+            h = r[6];
             P.cur += 6;
             prog_wait(P, op);
             blk = P.R + size_t(ring) * kTile + lane;
             acc = blk[ne * kTile];
             e = 0;
         } else if (type == kRecEnd) {
+            h = r[1];
             const double xi = acc / blk[(ne + 1) * kTile];
             blk[ne * kTile] = xi;
             b_t[size_t(brow) * kTile] = xi;
@@ -598,10 +609,12 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             P.cur += 1;
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
+            h = P.cur[0];
         } else if (type == kRecSync) {
             walk_trace(v, tile, warp, lane, 0);
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             P.cur += 1;
+            h = P.cur[0];
         } else {
             walk_trace(v, tile, warp, lane, 1);
             break;

@@ -504,9 +504,43 @@ void Symbolic::analyze(int32_t n_bus, const int32_t* indptr, const int32_t* indi
     brow_q.assign(n, -1);
     zcol_t.assign(n, -1);
     zcol_v.assign(n, -1);
-    for (int32_t b = 0; b < n; ++b) {
+    // Row order of the NPM / Jacobian sweeps: reverse Cuthill-McKee on the Ybus
+    // graph, so a block's 32 consecutive rows share neighbours and the
+    // neighbours' voltage rows are re-read from L2 (results do not depend on
+    // it: rows are independent and the max-norm is order-free).
+    std::vector<int32_t> order;
+    {
+        std::vector<uint8_t> seen(n, 0);
+        std::vector<int32_t> deg(n);
+        for (int32_t i = 0; i < n; ++i) deg[i] = yp[i + 1] - yp[i];
+        std::vector<int32_t> by_deg(n);
+        for (int32_t i = 0; i < n; ++i) by_deg[i] = i;
+        std::stable_sort(by_deg.begin(), by_deg.end(), [&](int32_t a, int32_t b) { return deg[a] < deg[b]; });
+        for (int32_t start : by_deg) {
+            if (seen[start]) continue;
+            size_t head = order.size();
+            order.push_back(start);
+            seen[start] = 1;
+            while (head < order.size()) {
+                const int32_t u = order[head++];
+                const size_t first = order.size();
+                for (int32_t q = yp[u]; q < yp[u + 1]; ++q)
+                    if (!seen[yi[q]]) {
+                        seen[yi[q]] = 1;
+                        order.push_back(yi[q]);
+                    }
+                std::stable_sort(order.begin() + first, order.end(),
+                                 [&](int32_t a, int32_t b) { return deg[a] < deg[b]; });
+            }
+        }
+        std::reverse(order.begin(), order.end());
+    }
+    for (int32_t b : order) {
         if (b == ref) continue;
         rows.push_back(b);
+    }
+    for (int32_t b = 0; b < n; ++b) {
+        if (b == ref) continue;
         brow_p[b] = row_fwd[jth[b]];
         zcol_t[b] = col_fwd[jth[b]];
         if (jvm[b] >= 0) {
