@@ -327,6 +327,7 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.tB = reinterpret_cast<const char*>(v.b + size_t(tile) * v.nJ * kTile);
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
+    __syncwarp();  // every lane's barrier is initialised before lane 0 arms the page barriers
     if (lane == 0) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         for (int p = 0; p < kWalkPages && p < P.n_pages; ++p) {
