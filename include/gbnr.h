@@ -74,7 +74,11 @@ typedef struct gbnr_options {
     int32_t prefetch;      /* steps a walk copy may run ahead (0 = 8)              */
     int32_t headroom;      /* ring residency margin in steps (0 = 2)               */
     int32_t walkers;       /* warps per tile walking disjoint subtrees (0 = 8, <= 8) */
-    int32_t reserved;
+    int32_t jacobian;      /* when the next Jacobian is built: 0 = inside the mismatch
+                              sweep unless the task is predicted to converge at that
+                              check (a wrong guess adds a Jacobian-only launch);
+                              1 = always inside the sweep; 2 = always after the check
+                              (the reference's order).  Results are identical.        */
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);

@@ -8,9 +8,10 @@
 // column of one tile is one contiguous run (one TMA bulk copy).  A *tile* is the
 // 32 tasks of one warp, one lane per task.
 //
-//   npm_kernel / conv_kernel   compute_npm + convergence (Alg. 1)
-//   jacobian_kernel            update_jacobian into the A tape via the static lookup
-//                              (signs per SURVEY App. B)
+//   npm_kernel<JAC> / conv_kernel  compute_npm + convergence (
+//                              Alg. 1) fused with update_jacobian into the A tape via the
+//                              static lookup (signs per
+//                              SURVEY App. B): one sweep computes the currents for both
 //   lu_walk_kernel<FS>         refactorize_batch (Alg. 2 operation order)
 //                              fused with the forward substitution:
 //                              one warp walks one tile through every column (walk.hpp)
@@ -67,6 +68,8 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
         v.active[t] = real ? 1 : 0;
         v.flag[t] = 0;
         v.maxmis[t] = real ? INFINITY : 0.0;
+        v.mis_prev[t] = INFINITY;
+        v.jskip[t] = 0;
         v.norm_bits[t] = 0ull;
         const int cnt = __popc(__ballot_sync(kFull, real));
         if (lane == 0) v.tile_active[tile] = cnt;
@@ -79,6 +82,20 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
 // each warp sweeps the chunk's Ybus rows for its tile; partial max-norms merge
 // with an exact integer atomicMax on the (non-negative) IEEE bits.
 // ---------------------------------------------------------------------------
+// JMODE: 0 no Jacobian; 1 speculative (active tasks not predicted to converge at
+// this check); 2 the tasks mode 1 skipped that are still active; 3 every active task
+enum { kJacNone = 0, kJacSpec = 1, kJacFix = 2, kJacAll = 3 };
+
+// Predicted to converge at this check: quadratic convergence extrapolated from
+// the last two checks, |F_k| ~ |F_k-1|^3 / |F_k-2|^2 < tol.  Only decides where
+// the Jacobian is computed; a wrong guess costs a kJacFix launch, never a result.
+__device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
+    if (v.jpolicy != 0) return v.jpolicy == 2;  // never / always deferred
+    const double n1 = v.maxmis[t], n2 = v.mis_prev[t];
+    return isfinite(n2) && n1 * n1 * n1 < v.tol * n2 * n2;
+}
+
+template <bool NPM, int JMODE>
 __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = my_tile(v, blockIdx.y, warp);
@@ -86,14 +103,25 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
     const int t = tile * kTile + lane;
     const size_t bp = v.bpad;
     double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;  // tile-blocked b tape
+    double* a_t = v.A + size_t(tile) * v.nnzLU * kTile + lane;  // tile-blocked A tape
     const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
+    bool act = JMODE != kJacNone && v.active[t] != 0;
+    if (JMODE == kJacSpec) {
+        const bool skip = act && predict_converged(v, t);
+        act = act && !skip;
+        if (blockIdx.x == 0) v.jskip[t] = skip;
+    } else if (JMODE == kJacFix) {
+        act = act && v.jskip[t] != 0;
+    }
+    if (JMODE != kJacNone && blockIdx.x == 0) v.flag[t] = 0;  // pivot flags of the coming refactorization
+    if (!NPM && !__any_sync(kFull, act)) return;
     double nrm = 0.0;
     const int r1 = min(v.n_rows, int(blockIdx.x + 1) * kRowChunk);
     for (int ri = blockIdx.x * kRowChunk; ri < r1; ++ri) {
         const int r = __ldg(v.rows + ri);
+        const int q0 = __ldg(v.yp + r), q1 = __ldg(v.yp + r + 1);
         double ire = 0.0, iim = 0.0;
-        const int q1 = __ldg(v.yp + r + 1);
-        for (int q = __ldg(v.yp + r); q < q1; ++q) {
+        for (int q = q0; q < q1; ++q) {
             const int k = __ldg(v.yi + q);
             const double vmk = v.vm[k * bp + t];
             acc_current(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vmk * v.c[k * bp + t],
@@ -103,18 +131,34 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
         const double vre = vmr * v.c[r * bp + t], vim = vmr * v.s[r * bp + t];
         double P, Q;
         injection(vre, vim, ire, iim, P, Q);
-        const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
-        const double fp = P - v.p0[size_t(r) * v.s_ld + ts];
-        b_t[size_t(__ldg(v.brow_p + r)) * kTile] = fp;
-        nrm = fmax(nrm, nan_as_inf_abs(fp));
-        const int bq = __ldg(v.brow_q + r);
-        if (bq >= 0) {
-            const double fq = Q - v.q0[size_t(r) * v.s_ld + ts];
-            b_t[size_t(bq) * kTile] = fq;
-            nrm = fmax(nrm, nan_as_inf_abs(fq));
+        if (NPM) {
+            const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
+            const double fp = P - v.p0[size_t(r) * v.s_ld + ts];
+            b_t[size_t(__ldg(v.brow_p + r)) * kTile] = fp;
+            nrm = fmax(nrm, nan_as_inf_abs(fp));
+            const int bq = __ldg(v.brow_q + r);
+            if (bq >= 0) {
+                const double fq = Q - v.q0[size_t(r) * v.s_ld + ts];
+                b_t[size_t(bq) * kTile] = fq;
+                nrm = fmax(nrm, nan_as_inf_abs(fq));
+            }
+        }
+        if (JMODE != kJacNone && act) {
+            for (int q = q0; q < q1; ++q) {
+                const int k = __ldg(v.yi + q);
+                const double ck = v.c[k * bp + t], sk = v.s[k * bp + t], vmk = v.vm[k * bp + t];
+                double zre, zim, j[4];
+                jac_z(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vre, vim, ck, sk, zre, zim);
+                jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
+                const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
+                if (l.x >= 0) a_t[size_t(l.x) * kTile] = j[0];
+                if (l.y >= 0) a_t[size_t(l.y) * kTile] = j[1];
+                if (l.z >= 0) a_t[size_t(l.z) * kTile] = j[2];
+                if (l.w >= 0) a_t[size_t(l.w) * kTile] = j[3];
+            }
         }
     }
-    atomicMax(v.norm_bits + t, static_cast<unsigned long long>(__double_as_longlong(nrm)));
+    if (NPM) atomicMax(v.norm_bits + t, static_cast<unsigned long long>(__double_as_longlong(nrm)));
 }
 
 // Convergence / status per task (MATPOWER iteration convention).
@@ -128,6 +172,7 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
     v.norm_bits[t] = 0ull;
     bool act = v.tile_active[tile] != 0 && v.active[t] != 0;
     if (act) {
+        v.mis_prev[t] = v.maxmis[t];
         v.maxmis[t] = m;
         if (m < v.tol) {
             v.status[t] = GBNR_CONVERGED;
@@ -142,12 +187,14 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
         }
     }
     const int cnt = __popc(__ballot_sync(kFull, act));
+    const int nj = __popc(__ballot_sync(kFull, act && v.jskip[t] != 0));
     if (lane == 0) {
         v.tile_active[tile] = cnt;
         if (cnt) {
             atomicAdd(v.active_count + it, cnt);     // active tasks after iteration it
             atomicAdd(v.active_count + 32 + it, 1);  // tiles with work left
         }
+        if (nj) atomicAdd(v.active_count + 96 + it, nj);  // still active, Jacobian skipped
     }
 }
 
@@ -159,6 +206,7 @@ __global__ void bump_kernel(DevView v) {
     volatile int32_t* h = v.h_counts;
     h[it] = v.active_count[it];
     h[32 + it] = v.active_count[32 + it];
+    h[96 + it] = v.active_count[96 + it];
     __threadfence_system();
     *v.it_dev = it + 1;
 }
@@ -180,51 +228,6 @@ __global__ void status_count_kernel(DevView v) {
     __threadfence_system();
 }
 
-// ---------------------------------------------------------------------------
-// Jacobian -> A tape (LU slot order, tile-blocked; fill slots are never
-// written and stay 0).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) jacobian_kernel(DevView v) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = my_tile(v, blockIdx.y, warp);
-    if (tile < 0) return;
-    const int t = tile * kTile + lane;
-    const bool act = v.active[t] != 0;
-    if (blockIdx.x == 0) v.flag[t] = 0;  // pivot flags of this iteration's refactorization
-    const size_t bp = v.bpad;
-    double* a_t = v.A + size_t(tile) * v.nnzLU * kTile + lane;  // tile-blocked A tape
-    const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
-    const int r1 = min(v.n_rows, int(blockIdx.x + 1) * kRowChunk);
-    for (int ri = blockIdx.x * kRowChunk; ri < r1; ++ri) {
-        const int r = __ldg(v.rows + ri);
-        const int q0 = __ldg(v.yp + r), q1 = __ldg(v.yp + r + 1);
-        double ire = 0.0, iim = 0.0;
-        for (int q = q0; q < q1; ++q) {
-            const int k = __ldg(v.yi + q);
-            const double vmk = v.vm[k * bp + t];
-            acc_current(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vmk * v.c[k * bp + t],
-                        vmk * v.s[k * bp + t], ire, iim);
-        }
-        const double vmr = v.vm[r * bp + t];
-        const double vre = vmr * v.c[r * bp + t], vim = vmr * v.s[r * bp + t];
-        double P, Q;
-        injection(vre, vim, ire, iim, P, Q);
-        for (int q = q0; q < q1; ++q) {
-            const int k = __ldg(v.yi + q);
-            const double ck = v.c[k * bp + t], sk = v.s[k * bp + t], vmk = v.vm[k * bp + t];
-            double zre, zim, j[4];
-            jac_z(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vre, vim, ck, sk, zre, zim);
-            jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
-            const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
-            if (act) {
-                if (l.x >= 0) a_t[size_t(l.x) * kTile] = j[0];
-                if (l.y >= 0) a_t[size_t(l.y) * kTile] = j[1];
-                if (l.z >= 0) a_t[size_t(l.z) * kTile] = j[2];
-                if (l.w >= 0) a_t[size_t(l.w) * kTile] = j[3];
-            }
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Tile walks (walk.hpp).  One warp = one tile = one CTA.  Shared memory is a
@@ -403,7 +406,8 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const int op = (h >> 4) - 1;
             const int kpos_fs = r[1], nrows = r[2] & 0xffff, src_row = int(unsigned(r[2]) >> 16);
             const int ysrc = r[3];
-            h = r[4 + ((nrows + 1) >> 1)];
+            const int n4 = (nrows + 3) & ~3;  // destinations padded with the scratch row len
+            h = r[4 + (n4 >> 1)];
             if (op >= 0) prog_wait(P, op);
             const double* src = P.R + size_t(src_row) * kTile + lane;
             if (nrows > 0) {
@@ -439,12 +443,13 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                     x[d6 * kTile] = a[6];
                     x[d7 * kTile] = a[7];
                 }
-                if (q + 4 <= nrows) {
+                for (; q < nrows; q += 4) {  // whole groups of 4; padding rows re-read the last L row
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1];
                     const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
                     const int d2 = w1 & 0xffff, d3 = int(unsigned(w1) >> 16);
-                    const double l0 = src[q * kTile], l1 = src[(q + 1) * kTile];
-                    const double l2 = src[(q + 2) * kTile], l3 = src[(q + 3) * kTile];
+                    const int last = nrows - 1;
+                    const double l0 = src[q * kTile], l1 = src[min(q + 1, last) * kTile];
+                    const double l2 = src[min(q + 2, last) * kTile], l3 = src[min(q + 3, last) * kTile];
                     double a0 = x[d0 * kTile], a1 = x[d1 * kTile], a2 = x[d2 * kTile], a3 = x[d3 * kTile];
                     a0 = fma(-mult, l0, a0);
                     a1 = fma(-mult, l1, a1);
@@ -454,29 +459,13 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                     x[d1 * kTile] = a1;
                     x[d2 * kTile] = a2;
                     x[d3 * kTile] = a3;
-                    q += 4;
-                }
-                if (q + 2 <= nrows) {  // q even here: one packed pair
-                    const int32_t w0 = dw[q >> 1];
-                    const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
-                    const double l0 = src[q * kTile], l1 = src[(q + 1) * kTile];
-                    double a0 = x[d0 * kTile], a1 = x[d1 * kTile];
-                    a0 = fma(-mult, l0, a0);
-                    a1 = fma(-mult, l1, a1);
-                    x[d0 * kTile] = a0;
-                    x[d1 * kTile] = a1;
-                    q += 2;
-                }
-                if (q < nrows) {
-                    const int d0 = dw[q >> 1] & 0xffff;
-                    x[d0 * kTile] = fma(-mult, src[q * kTile], x[d0 * kTile]);
                 }
             }
             if (FS) {
                 const int fspos = int(unsigned(kpos_fs) >> 16);
                 if (fspos != 0xffff) acc_y = fma(-src[fspos * kTile], P.R[size_t(ysrc) * kTile + lane], acc_y);
             }
-            P.cur += 4 + ((nrows + 1) >> 1);
+            P.cur += 4 + (n4 >> 1);
         } else if (type == kRecIssue) {
             P.cur += prog_issue(v, P, r, lane);
             h = P.cur[0];
@@ -738,16 +727,24 @@ void launch_init(const DevView& v, cudaStream_t st) {
     init_kernel<<<dim3(unsigned((v.n + 31) / 32), n_super(v)), 256, 0, st>>>(v);
 }
 
-void launch_npm(const DevView& v, cudaStream_t st) {
-    npm_kernel<<<dim3(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v)), 256, 0, st>>>(v);
+void launch_npm(const DevView& v, bool jac, cudaStream_t st) {
+    const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v));
+    if (jac)
+        npm_kernel<true, kJacSpec><<<grid, 256, 0, st>>>(v);
+    else
+        npm_kernel<true, kJacNone><<<grid, 256, 0, st>>>(v);
     conv_kernel<<<n_super(v), 256, 0, st>>>(v);
     bump_kernel<<<1, 1, 0, st>>>(v);
 }
 
 void launch_status_count(const DevView& v, cudaStream_t st) { status_count_kernel<<<1, 1024, 0, st>>>(v); }
 
-void launch_jacobian(const DevView& v, cudaStream_t st) {
-    jacobian_kernel<<<dim3(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v)), 256, 0, st>>>(v);
+void launch_jacobian(const DevView& v, bool all, cudaStream_t st) {
+    const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v));
+    if (all)
+        npm_kernel<false, kJacAll><<<grid, 256, 0, st>>>(v);
+    else
+        npm_kernel<false, kJacFix><<<grid, 256, 0, st>>>(v);
 }
 
 void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {

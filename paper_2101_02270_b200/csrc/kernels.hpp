@@ -34,14 +34,18 @@ struct DevView {
     // per-task state
     int32_t *status, *iters;
     uint8_t *active, *flag;
-    double* maxmis;
+    double* maxmis;                 // max-norm at the last check (inf before the first)
+    double* mis_prev;               // max-norm one check earlier (inf before)
+    uint8_t* jskip;                 // the last NPM skipped this task's speculative Jacobian
     unsigned long long* norm_bits;  // running max-norm (IEEE bits) of the current NPM
     int32_t *tile_active, *active_count;
     int32_t* it_dev;                // Newton iteration counter on the device
     int32_t* h_counts;              // mapped host memory: [0,32) active tasks, [32,64) active
-                                    // tiles per iteration, [64,67) tasks per final status
+                                    // tiles per iteration, [64,67) tasks per final status,
+                                    // [96,128) active tasks whose Jacobian was not written
     double tol, singular_tol;
     int32_t max_iter;
+    int32_t jpolicy;                // gbnr_options.jacobian
     int32_t dbg;                    // experiment switches (GBNR_DBG), 0 in production
 };
 
@@ -56,8 +60,11 @@ size_t walk_smem_bytes(const WalkView& w);
 void configure_kernels();
 int walk_ctas_per_sm(size_t smem, int threads);  // resident LU-walk CTAs per SM
 void launch_init(const DevView& v, cudaStream_t st);
-void launch_npm(const DevView& v, cudaStream_t st);  // NPM + convergence + iteration bump
-void launch_jacobian(const DevView& v, cudaStream_t st);
+// NPM + convergence + iteration bump; with jac, also the next Jacobian of every
+// active task not predicted to converge at this check
+void launch_npm(const DevView& v, bool jac, cudaStream_t st);
+// Jacobian only: of every active task (all) or of those the last NPM skipped
+void launch_jacobian(const DevView& v, bool all, cudaStream_t st);
 void launch_status_count(const DevView& v, cudaStream_t st);
 void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st);
 void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st);

@@ -169,6 +169,7 @@ struct gbnr_plan {
         v.tol = opt.tol;
         v.singular_tol = opt.singular_tol;
         v.max_iter = opt.max_iter;
+        v.jpolicy = opt.jacobian;
     }
 
     gbnr::WalkView upload_walk(const gbnr::WalkSet& w) {
@@ -274,9 +275,11 @@ struct gbnr_plan {
         v.active = static_cast<uint8_t*>(alloc(bpad));
         v.flag = static_cast<uint8_t*>(alloc(bpad));
         v.maxmis = static_cast<double*>(alloc(bpad * sizeof(double)));
+        v.mis_prev = static_cast<double*>(alloc(bpad * sizeof(double)));
+        v.jskip = static_cast<uint8_t*>(alloc(bpad));
         v.norm_bits = static_cast<unsigned long long*>(alloc(bpad * sizeof(unsigned long long)));
         v.tile_active = static_cast<int32_t*>(alloc(size_t(n_tiles) * sizeof(int32_t)));
-        v.active_count = static_cast<int32_t*>(alloc(64 * sizeof(int32_t)));
+        v.active_count = static_cast<int32_t*>(alloc(128 * sizeof(int32_t)));
         cap_tiles = n_tiles;
     }
 
@@ -367,7 +370,7 @@ struct gbnr_plan {
     void launch_lu_all() { gbnr::launch_lu_walk(v, vf, true, stream); }
     void launch_fsbs_all() { gbnr::launch_bs_walk(v, vb, stream); }
 
-    static int launches_per_iteration() { return 7; }  // jac, lu+fs, bs, vupd, npm, conv, bump
+    static int launches_per_iteration() { return 6; }  // lu+fs, bs, vupd, npm+jac, conv, bump
 
     void run() {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_run before gbnr_stage");
@@ -375,19 +378,23 @@ struct gbnr_plan {
         std::memset(timing, 0, sizeof timing);
         ev_used.clear();
         CK(cudaEventRecord(ev0, stream));
-        CK(cudaMemsetAsync(v.active_count, 0, 64 * sizeof(int32_t), stream));
+        CK(cudaMemsetAsync(v.active_count, 0, 128 * sizeof(int32_t), stream));
         gbnr::launch_init(v, stream);
         CK(cudaGetLastError());
-        timed(kNpm, [&] { gbnr::launch_npm(v, stream); });
-        int it_done = 0;
+        timed(kNpm, [&] { gbnr::launch_npm(v, opt.max_iter > 0, stream); });
+        int it_done = 0, jac_fix = 0;
         for (int it = 1; it <= opt.max_iter; ++it) {
             CK(cudaStreamSynchronize(stream));  // the bump kernel published active_count[it-1]
-            if (reinterpret_cast<volatile int32_t*>(h_count)[it - 1] == 0) break;
-            timed(kJac, [&] { gbnr::launch_jacobian(v, stream); });
+            const volatile int32_t* hc = h_count;
+            if (hc[it - 1] == 0) break;
+            if (hc[96 + it - 1] > 0) {  // mispredicted convergence: those tasks' Jacobian
+                timed(kJac, [&] { gbnr::launch_jacobian(v, false, stream); });
+                ++jac_fix;
+            }
             timed(kLu, [&] { launch_lu_all(); });
             timed(kFsbs, [&] { launch_fsbs_all(); });
             timed(kVupd, [&] { gbnr::launch_vupdate(v, stream); });
-            timed(kNpm, [&] { gbnr::launch_npm(v, stream); });
+            timed(kNpm, [&] { gbnr::launch_npm(v, it < opt.max_iter, stream); });
             CK(cudaGetLastError());
             it_done = it;
         }
@@ -408,7 +415,7 @@ struct gbnr_plan {
         timing[5] = ms;
         timing[12] = it_done;
         timing[13] = v.n_tasks;
-        timing[19] = double(launches_per_iteration()) * it_done + 4;  // kernels launched
+        timing[19] = double(launches_per_iteration()) * it_done + 4 + jac_fix;  // kernels launched
         solved = true;
     }
 
@@ -573,7 +580,7 @@ struct gbnr_plan {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_refactor before gbnr_stage");
         CK(cudaSetDevice(opt.device));
         gbnr::launch_init(v, stream);
-        gbnr::launch_jacobian(v, stream);
+        gbnr::launch_jacobian(v, true, stream);
         CK(cudaGetLastError());
         gbnr::launch_lu_walk(v, vl, false, stream);  // warm-up
         CK(cudaEventRecord(ev0, stream));
@@ -702,6 +709,7 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (p->opt.ring_rows < 0 || p->opt.stage_rows < 0 || p->opt.prefetch < 0 || p->opt.headroom < 0 ||
             p->opt.walkers < 0 || p->opt.walkers > 8)
             throw Error(GBNR_ECONFIG, "negative walk parameter");
+        if (p->opt.jacobian < 0 || p->opt.jacobian > 2) throw Error(GBNR_ECONFIG, "jacobian policy must be 0, 1 or 2");
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
         p->lay = gbnr::build_lu_layout(p->sym);

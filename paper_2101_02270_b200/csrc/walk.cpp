@@ -369,11 +369,12 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
                 if (e.src >= 65536 || e.nrows >= 65536) throw Error(3, "walk dependency too large to encode");
                 std::vector<int32_t> rec{kRecDep | ((opn(e.op) + 1) << 4), e.kpos_fs,
                                          e.nrows | (std::max(e.src, 0) << 16), e.ysrc};
-                for (int32_t r = 0; r < e.nrows; r += 2) {
-                    const int32_t lo = w.dst[e.u0 + r];
-                    const int32_t hi = r + 1 < e.nrows ? w.dst[e.u0 + r + 1] : 0;
-                    rec.push_back(lo | (hi << 16));
-                }
+                // destinations padded to a multiple of 4 with the block's spare
+                // row `len` (dead between STEP and END), so the kernel runs whole
+                // 4-row groups without tails
+                const int32_t n4 = (e.nrows + 3) & ~3;
+                auto dst = [&](int32_t r) { return r < e.nrows ? int32_t(w.dst[e.u0 + r]) : len; };
+                for (int32_t r = 0; r < n4; r += 2) rec.push_back(dst(r) | (dst(r + 1) << 16));
                 em.emit(rec);
                 issue_upto(ev++);
             }
@@ -412,7 +413,7 @@ Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
     int32_t longest = 8;
     for (int32_t k = 0; k < s.nJ; ++k) {
         longest = std::max(longest, 2 + (s.dpos[k] - s.cp[k]));           // END
-        longest = std::max(longest, 5 + (s.cp[k + 1] - s.dpos[k]) / 2);  // DEP
+        longest = std::max(longest, 6 + (s.cp[k + 1] - s.dpos[k]) / 2);  // DEP (rows padded to 4)
     }
     const int32_t W = std::max(cfg.page_words, 4 * ((longest + 1 + 3) / 4));
     const int64_t fixed = int64_t(walkers) * (int64_t(cfg.pages) * W * 4 + int64_t(cfg.barriers + cfg.pages) * 8);
@@ -692,7 +693,7 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
             const int32_t m = list[i];
             const int32_t c0 = s.cp[m], len = s.cp[m + 1] - c0, dp = s.dpos[m] - c0;
             StepIn& si = pr.steps[i];
-            si.blk_rows = len + (with_fs ? 1 : 0);
+            si.blk_rows = len + 1;  // row len: b / y (FS), the update padding's scratch row
             si.copies.push_back(copy(kTapeA, c0, len, 0));
             if (with_fs) si.copies.push_back(copy(kTapeB, m, 1, len));
             si.rec.len_dp = len | (dp << 16);

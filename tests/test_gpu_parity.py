@@ -134,6 +134,21 @@ def test_walk_plan_invariance(opts):
     _compare(plan2.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
 
 
+@pytest.mark.parametrize("jacobian", [0, 1, 2])
+def test_jacobian_policy_invariance(jacobian):
+    """Where the next Jacobian is built -- speculatively inside the mismatch sweep
+    (0), always there (1), or after the convergence check as the reference orders
+    it (2, every Jacobian through the skipped-task launch) -- never changes a bit."""
+    gc, plan, oplan, vm0, va0 = _setup("synth2383")
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, jacobian=jacobian)
+    p0, q0 = montecarlo(gc, 150)
+    p0[:, 7] *= 40.0  # one task that does not converge
+    r = plan2.solve(p0, q0, vm0, va0)
+    assert r.status[7] != 0 and (r.status == 0).sum() >= 140
+    _compare(r, oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
+
+
 def test_solve_batches_pipeline_matches_single_solves():
     """gbnr_solve_batches (H2D / D2H overlapped with neighbouring solves) returns
     exactly what one gbnr_solve per batch returns."""

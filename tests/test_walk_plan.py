@@ -183,7 +183,7 @@ def replay_forward(w, A, b_tape, nnz, fs=True):
             fsp = (kpos_fs >> 16) & 0xFFFF
             if fs and fsp != 0xFFFF:
                 S["acc"] = S["acc"] - R[src + fsp] * R[ysrc]
-            return 4 + (nrows + 1) // 2
+            return 4 + ((nrows + 3) & ~3) // 2
         if t == REC_STEP:
             ring, ln = int(r[1]) & 0xFFFF, int(r[1]) >> 16
             S.update(ring=ring, ln=ln, dp=int(r[2]), lslot=int(r[3]), brow=int(r[4]))
