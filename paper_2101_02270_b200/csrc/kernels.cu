@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(256) npm_kernel(DevView v) {
     if (tile < 0) return;
     const int t = tile * kTile + lane;
     const size_t bp = v.bpad;
-    double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;  // tile-blocked b tape
-    double* a_t = v.A + size_t(tile) * v.nnzLU * kTile + lane;  // tile-blocked A tape
+    double* b_t = v.b + size_t(tile) * v.tstride + lane;  // tile-blocked b tape
+    double* a_t = v.A + size_t(tile) * v.tstride + lane;  // tile-blocked A tape
     const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
     bool act = JMODE != kJacNone && v.active[t] != 0;
     if (JMODE == kJacSpec) {
@@ -238,6 +238,15 @@ __global__ void status_count_kernel(DevView v) {
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
+// 32-bit shared-window accesses of the walk rows (no generic-address arithmetic)
+__device__ __forceinline__ double lds(unsigned a) {
+    double r;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(r) : "r"(a) : "memory");
+    return r;
+}
+__device__ __forceinline__ void sts(unsigned a, double x) {
+    asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(x) : "memory");
+}
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
 }
@@ -289,7 +298,8 @@ struct Prog {
     unsigned long long* pbar;   // page barriers [kWalkPages]
     const int32_t* gs;          // stream in global memory
     const int32_t* cur;         // next record
-    const char *tA, *tLU, *tB;  // this tile's A, LU and b tapes (256 B rows)
+    const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
+    int32_t tape_rows;          // rows per tape id step (nnzLU): tape t starts at row t * nnzLU
     int W, n_pages, page;
 };
 
@@ -325,9 +335,8 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.n_pages = w.wpage0[warp + 1] - w.wpage0[warp];
     P.page = 0;
     P.cur = P.pg;
-    P.tA = reinterpret_cast<const char*>(v.A + size_t(tile) * v.nnzLU * kTile);
-    P.tLU = reinterpret_cast<const char*>(v.LU + size_t(tile) * v.nnzLU * kTile);
-    P.tB = reinterpret_cast<const char*>(v.b + size_t(tile) * v.nJ * kTile);
+    P.tb = reinterpret_cast<const char*>(v.A + size_t(tile) * v.tstride);
+    P.tape_rows = v.nnzLU;
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
     __syncwarp();  // every lane's barrier is initialised before lane 0 arms the page barriers
@@ -359,21 +368,21 @@ __device__ __forceinline__ void prog_next_page(Prog& P, int lane) {
 // kRecIssue: lane 0 arms the op's barrier and issues its bulk copies.
 __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32_t* r, int lane) {
     const int ncopy = (r[0] >> 4) & 0xfff;
-    if (!(v.dbg & 2)) fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
+    fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
     unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
     __syncwarp();
     if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]));
-    __syncwarp();
-    // one copy per lane (the barrier's tx-count may dip below zero meanwhile)
+    // one copy per lane; a copy may complete before lane 0's arrive.expect_tx (the
+    // barrier's tx-count dips below zero, its phase cannot complete without the arrive)
     const unsigned rbase = smem_u32(P.R), ubar = smem_u32(bar);
     for (int i = lane; i < ncopy; i += 32) {
         const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
         const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
+        const char* src = P.tb + size_t(unsigned((c & 3) * P.tape_rows + slot)) * (kTile * 8);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 rbase + smem * (kTile * 8u)),
-            "l"(((c & 3) == kTapeA ? P.tA : (c & 3) == kTapeLU ? P.tLU : P.tB) + size_t(slot) * (kTile * 8)),
-            "r"(rows * (kTile * 8u)), "r"(ubar)
+            "l"(src), "r"(rows * (kTile * 8u)), "r"(ubar)
             : "memory");
     }
     return 3 + 2 * ncopy;
@@ -384,6 +393,8 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 }
 
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
+// Shared rows are addressed as 32-bit shared-window offsets: row r of this
+// lane at R0 + r * 256.
 template <bool FS>
 __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -391,11 +402,13 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    double* lu_t = v.LU + size_t(tile) * v.nnzLU * kTile + lane;
-    double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
+    double* lu_t = v.LU + size_t(tile) * v.tstride + lane;
+    double* b_t = v.b + size_t(tile) * v.tstride + lane;
     const double stol = v.singular_tol;
+    constexpr unsigned RB = kTile * 8;  // bytes per shared row
+    const unsigned R0 = smem_u32(P.R) + unsigned(lane) * 8u;
     bool flagged = false;
-    double* x = P.R;
+    unsigned xs = R0;  // this step's block
     int len = 0, dp = 0, lslot = 0, brow = 0;
     double acc_y = 0.0;
     int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
@@ -409,61 +422,63 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const int n4 = (nrows + 3) & ~3;  // destinations padded with the scratch row len
             h = r[4 + (n4 >> 1)];
             if (op >= 0) prog_wait(P, op);
-            const double* src = P.R + size_t(src_row) * kTile + lane;
+            const unsigned src = R0 + unsigned(src_row) * RB;
             if (nrows > 0) {
-                const double mult = x[(kpos_fs & 0xffff) * kTile];
+                const double mult = lds(xs + unsigned(kpos_fs & 0xffff) * RB);
                 const int32_t* dw = r + 4;
                 int q = 0;
                 for (; q + 8 <= nrows; q += 8) {  // eight independent rows in flight
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1], w2 = dw[(q >> 1) + 2],
                                   w3 = dw[(q >> 1) + 3];
-                    const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
-                    const int d2 = w1 & 0xffff, d3 = int(unsigned(w1) >> 16);
-                    const int d4 = w2 & 0xffff, d5 = int(unsigned(w2) >> 16);
-                    const int d6 = w3 & 0xffff, d7 = int(unsigned(w3) >> 16);
+                    const unsigned d0 = xs + unsigned(w0 & 0xffff) * RB, d1 = xs + (unsigned(w0) >> 16) * RB;
+                    const unsigned d2 = xs + unsigned(w1 & 0xffff) * RB, d3 = xs + (unsigned(w1) >> 16) * RB;
+                    const unsigned d4 = xs + unsigned(w2 & 0xffff) * RB, d5 = xs + (unsigned(w2) >> 16) * RB;
+                    const unsigned d6 = xs + unsigned(w3 & 0xffff) * RB, d7 = xs + (unsigned(w3) >> 16) * RB;
+                    const unsigned sq = src + unsigned(q) * RB;
                     double l[8], a[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) l[u] = src[(q + u) * kTile];
-                    a[0] = x[d0 * kTile];
-                    a[1] = x[d1 * kTile];
-                    a[2] = x[d2 * kTile];
-                    a[3] = x[d3 * kTile];
-                    a[4] = x[d4 * kTile];
-                    a[5] = x[d5 * kTile];
-                    a[6] = x[d6 * kTile];
-                    a[7] = x[d7 * kTile];
+                    for (int u = 0; u < 8; ++u) l[u] = lds(sq + unsigned(u) * RB);
+                    a[0] = lds(d0);
+                    a[1] = lds(d1);
+                    a[2] = lds(d2);
+                    a[3] = lds(d3);
+                    a[4] = lds(d4);
+                    a[5] = lds(d5);
+                    a[6] = lds(d6);
+                    a[7] = lds(d7);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) a[u] = fma(-mult, l[u], a[u]);
-                    x[d0 * kTile] = a[0];
-                    x[d1 * kTile] = a[1];
-                    x[d2 * kTile] = a[2];
-                    x[d3 * kTile] = a[3];
-                    x[d4 * kTile] = a[4];
-                    x[d5 * kTile] = a[5];
-                    x[d6 * kTile] = a[6];
-                    x[d7 * kTile] = a[7];
+                    sts(d0, a[0]);
+                    sts(d1, a[1]);
+                    sts(d2, a[2]);
+                    sts(d3, a[3]);
+                    sts(d4, a[4]);
+                    sts(d5, a[5]);
+                    sts(d6, a[6]);
+                    sts(d7, a[7]);
                 }
                 for (; q < nrows; q += 4) {  // whole groups of 4; padding rows re-read the last L row
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1];
-                    const int d0 = w0 & 0xffff, d1 = int(unsigned(w0) >> 16);
-                    const int d2 = w1 & 0xffff, d3 = int(unsigned(w1) >> 16);
+                    const unsigned d0 = xs + unsigned(w0 & 0xffff) * RB, d1 = xs + (unsigned(w0) >> 16) * RB;
+                    const unsigned d2 = xs + unsigned(w1 & 0xffff) * RB, d3 = xs + (unsigned(w1) >> 16) * RB;
                     const int last = nrows - 1;
-                    const double l0 = src[q * kTile], l1 = src[min(q + 1, last) * kTile];
-                    const double l2 = src[min(q + 2, last) * kTile], l3 = src[min(q + 3, last) * kTile];
-                    double a0 = x[d0 * kTile], a1 = x[d1 * kTile], a2 = x[d2 * kTile], a3 = x[d3 * kTile];
+                    const double l0 = lds(src + unsigned(q) * RB), l1 = lds(src + unsigned(min(q + 1, last)) * RB);
+                    const double l2 = lds(src + unsigned(min(q + 2, last)) * RB);
+                    const double l3 = lds(src + unsigned(min(q + 3, last)) * RB);
+                    double a0 = lds(d0), a1 = lds(d1), a2 = lds(d2), a3 = lds(d3);
                     a0 = fma(-mult, l0, a0);
                     a1 = fma(-mult, l1, a1);
                     a2 = fma(-mult, l2, a2);
                     a3 = fma(-mult, l3, a3);
-                    x[d0 * kTile] = a0;
-                    x[d1 * kTile] = a1;
-                    x[d2 * kTile] = a2;
-                    x[d3 * kTile] = a3;
+                    sts(d0, a0);
+                    sts(d1, a1);
+                    sts(d2, a2);
+                    sts(d3, a3);
                 }
             }
             if (FS) {
                 const int fspos = int(unsigned(kpos_fs) >> 16);
-                if (fspos != 0xffff) acc_y = fma(-src[fspos * kTile], P.R[size_t(ysrc) * kTile + lane], acc_y);
+                if (fspos != 0xffff) acc_y = fma(-lds(src + unsigned(fspos) * RB), lds(R0 + unsigned(ysrc) * RB), acc_y);
             }
             P.cur += 4 + (n4 >> 1);
         } else if (type == kRecIssue) {
@@ -479,41 +494,41 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             h = r[6];
             P.cur += 6;
             prog_wait(P, op);
-            x = P.R + size_t(ring) * kTile + lane;
-            acc_y = FS ? x[len * kTile] : 0.0;
+            xs = R0 + unsigned(ring) * RB;
+            acc_y = FS ? lds(xs + unsigned(len) * RB) : 0.0;
         } else if (type == kRecEnd) {
             h = r[1 + dp];
             // normalization L = x * (1 / pivot) and the U scatter, with the
             // pivot check's column maximum folded into the same
             // passes over x (max |x| is exact in any order)
-            const double piv = x[dp * kTile];
+            const double piv = lds(xs + unsigned(dp) * RB);
             const double inv = 1.0 / piv;
             double c0 = fabs(piv), c1 = 0.0;
             double* lcol = lu_t + size_t(lslot) * kTile;  // diagonal, then L rows
             lcol[0] = piv;
             int z = dp + 1;
             for (; z + 2 <= len; z += 2) {
-                const double x0 = x[z * kTile], x1 = x[(z + 1) * kTile];
+                const double x0 = lds(xs + unsigned(z) * RB), x1 = lds(xs + unsigned(z + 1) * RB);
                 c0 = fmax(c0, fabs(x0));
                 c1 = fmax(c1, fabs(x1));
                 const double l0 = x0 * inv, l1 = x1 * inv;
-                x[z * kTile] = l0;
-                x[(z + 1) * kTile] = l1;
+                sts(xs + unsigned(z) * RB, l0);
+                sts(xs + unsigned(z + 1) * RB, l1);
                 lcol[size_t(z - dp) * kTile] = l0;
                 lcol[size_t(z + 1 - dp) * kTile] = l1;
             }
             if (z < len) {
-                const double x0 = x[z * kTile];
+                const double x0 = lds(xs + unsigned(z) * RB);
                 c0 = fmax(c0, fabs(x0));
                 const double l0 = x0 * inv;
-                x[z * kTile] = l0;
+                sts(xs + unsigned(z) * RB, l0);
                 lcol[size_t(z - dp) * kTile] = l0;
             }
             z = 0;
             for (; z + 4 <= dp; z += 4) {  // U part -> its row-major slots
                 const int32_t s0 = r[1 + z], s1 = r[2 + z], s2 = r[3 + z], s3 = r[4 + z];
-                const double u0 = x[z * kTile], u1 = x[(z + 1) * kTile], u2 = x[(z + 2) * kTile],
-                             u3 = x[(z + 3) * kTile];
+                const double u0 = lds(xs + unsigned(z) * RB), u1 = lds(xs + unsigned(z + 1) * RB),
+                             u2 = lds(xs + unsigned(z + 2) * RB), u3 = lds(xs + unsigned(z + 3) * RB);
                 c0 = fmax(c0, fabs(u0));
                 c1 = fmax(c1, fabs(u1));
                 c0 = fmax(c0, fabs(u2));
@@ -524,17 +539,17 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 lu_t[size_t(s3) * kTile] = u3;
             }
             for (; z < dp; ++z) {
-                const double u0 = x[z * kTile];
+                const double u0 = lds(xs + unsigned(z) * RB);
                 c0 = fmax(c0, fabs(u0));
                 lu_t[size_t(r[1 + z]) * kTile] = u0;
             }
             const double cmax = fmax(c0, c1);
             flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
             if (FS) {
-                x[len * kTile] = acc_y;
+                sts(xs + unsigned(len) * RB, acc_y);
                 b_t[size_t(brow) * kTile] = acc_y;
             }
-            if (!(v.dbg & 1)) fence_proxy_async_global();  // later TMA re-fetches of this column see it
+            fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1 + dp;
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
@@ -559,7 +574,7 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;
+    double* b_t = v.b + size_t(tile) * v.tstride + lane;
     double* blk = P.R;
     int ne = 0, e = 0, brow = 0;
     double acc = 0.0;
@@ -595,7 +610,7 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             const double xi = acc / blk[(ne + 1) * kTile];
             blk[ne * kTile] = xi;
             b_t[size_t(brow) * kTile] = xi;
-            if (!(v.dbg & 1)) fence_proxy_async_global();
+            fence_proxy_async_global();
             P.cur += 1;
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
@@ -631,7 +646,7 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
         return;
     }
     const size_t bp = v.bpad;
-    const double* b_t = v.b + size_t(tile) * v.nJ * kTile + lane;  // tile-blocked b tape
+    const double* b_t = v.b + size_t(tile) * v.tstride + lane;  // tile-blocked b tape
     const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
     for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
         const int zt = __ldg(v.zcol_t + bus);

@@ -29,8 +29,11 @@ struct DevView {
     const double *vm_in, *va_in;  // staged start voltages (kept for repeated runs)
     const double *p0, *q0;
     int32_t s_ld, s_inc;          // p0[bus * s_ld + task * s_inc]
-    double *A, *LU;               // tile-blocked [n_tiles][nnzLU][32]
-    double* b;                    // tile-blocked [n_tiles][nJ][32]: F, then y (forward walk), then dx
+    // tile-blocked tapes, one block per tile of tstride doubles:
+    //   [A: nnzLU rows][LU: nnzLU rows][b: nJ rows] x 32 lanes
+    // A = the Jacobian in LU slot order, b = F, then y (forward walk), then dx.
+    double *A, *LU, *b;           // tile 0's tapes; tile t's at + t * tstride
+    size_t tstride;
     // per-task state
     int32_t *status, *iters;
     uint8_t *active, *flag;

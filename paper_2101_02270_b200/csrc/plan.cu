@@ -263,13 +263,16 @@ struct gbnr_plan {
         v.s = static_cast<double*>(alloc(nb));
         v.p0 = static_cast<double*>(alloc(nb));
         v.q0 = static_cast<double*>(alloc(nb));
-        const size_t lub = size_t(v.nnzLU) * bpad * sizeof(double);
-        v.A = static_cast<double*>(alloc(lub));
+        // one block per tile: A, LU and b rows adjacent, so a walk copy's source is
+        // tile base + (tape * nnzLU + slot) rows
+        v.tstride = (2 * size_t(v.nnzLU) + size_t(v.nJ)) * gbnr::kTile;
+        const size_t tb = v.tstride * size_t(n_tiles) * sizeof(double);
+        v.A = static_cast<double*>(alloc(tb));
         // fill slots of the A tape are never written by the Jacobian kernel and
         // must read zero; tile-blocked addresses do not depend on the batch size
-        CK(cudaMemsetAsync(v.A, 0, lub, stream));
-        v.LU = static_cast<double*>(alloc(lub));
-        v.b = static_cast<double*>(alloc(size_t(v.nJ) * bpad * sizeof(double)));
+        CK(cudaMemsetAsync(v.A, 0, tb, stream));
+        v.LU = v.A + size_t(v.nnzLU) * gbnr::kTile;
+        v.b = v.LU + size_t(v.nnzLU) * gbnr::kTile;
         v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
         v.iters = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
         v.active = static_cast<uint8_t*>(alloc(bpad));
@@ -596,12 +599,12 @@ struct gbnr_plan {
         if (lu_out) {
             // tile-blocked tape -> element-major CCS order [nnzLU][n_tasks]
             const size_t z = size_t(v.nnzLU);
-            std::vector<double> tape(size_t(v.n_tiles) * z * gbnr::kTile);
-            CK(cudaMemcpy(tape.data(), v.LU, tape.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            std::vector<double> tape(size_t(v.n_tiles) * v.tstride);
+            CK(cudaMemcpy(tape.data(), v.A, tape.size() * sizeof(double), cudaMemcpyDeviceToHost));
             for (size_t c = 0; c < z; ++c) {
-                const size_t ts = size_t(lay.tape_of_ccs[c]);
+                const size_t ts = z + size_t(lay.tape_of_ccs[c]);  // LU rows follow the A rows
                 for (int32_t t = 0; t < nt; ++t)
-                    lu_out[c * nt + t] = tape[(size_t(t / gbnr::kTile) * z + ts) * gbnr::kTile + t % gbnr::kTile];
+                    lu_out[c * nt + t] = tape[size_t(t / gbnr::kTile) * v.tstride + ts * gbnr::kTile + t % gbnr::kTile];
             }
         }
     }
