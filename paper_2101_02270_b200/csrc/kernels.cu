@@ -575,8 +575,10 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
     double* b_t = v.b + size_t(tile) * v.tstride + lane;
-    double* blk = P.R;
-    int ne = 0, e = 0, brow = 0;
+    constexpr unsigned RB = kTile * 8;
+    const unsigned R0 = smem_u32(P.R) + unsigned(lane) * 8u;
+    unsigned blk = R0, e = R0;  // this step's block; its next U entry
+    int ne = 0, brow = 0;
     double acc = 0.0;
     int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
     for (;;) {
@@ -587,8 +589,8 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             const int ysrc = r[1];
             h = r[2];
             if (op >= 0) prog_wait(P, op);
-            acc = fma(-blk[e * kTile], P.R[size_t(ysrc) * kTile + lane], acc);
-            ++e;
+            acc = fma(-lds(e), lds(R0 + unsigned(ysrc) * RB), acc);
+            e += RB;
             P.cur += 2;
         } else if (type == kRecIssue) {
             const int len = prog_issue(v, P, r, lane);
@@ -602,13 +604,13 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             h = r[6];
             P.cur += 6;
             prog_wait(P, op);
-            blk = P.R + size_t(ring) * kTile + lane;
-            acc = blk[ne * kTile];
-            e = 0;
+            blk = R0 + unsigned(ring) * RB;
+            e = blk;
+            acc = lds(blk + unsigned(ne) * RB);
         } else if (type == kRecEnd) {
             h = r[1];
-            const double xi = acc / blk[(ne + 1) * kTile];
-            blk[ne * kTile] = xi;
+            const double xi = acc / lds(blk + unsigned(ne + 1) * RB);
+            sts(blk + unsigned(ne) * RB, xi);
             b_t[size_t(brow) * kTile] = xi;
             fence_proxy_async_global();
             P.cur += 1;
