@@ -238,6 +238,14 @@ __global__ void status_count_kernel(DevView v) {
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
+// Shared row address of the low / high 16-bit row index of a packed word
+// (PRMT / SHF, then one shift-add)
+__device__ __forceinline__ unsigned row_lo(unsigned base, int32_t w) {
+    return base + (__byte_perm(unsigned(w), 0u, 0x4410) << 8);
+}
+__device__ __forceinline__ unsigned row_hi(unsigned base, int32_t w) {
+    return base + (__byte_perm(unsigned(w), 0u, 0x4432) << 8);
+}
 // 32-bit shared-window accesses of the walk rows (no generic-address arithmetic)
 __device__ __forceinline__ double lds(unsigned a) {
     double r;
@@ -430,10 +438,10 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 for (; q + 8 <= nrows; q += 8) {  // eight independent rows in flight
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1], w2 = dw[(q >> 1) + 2],
                                   w3 = dw[(q >> 1) + 3];
-                    const unsigned d0 = xs + unsigned(w0 & 0xffff) * RB, d1 = xs + (unsigned(w0) >> 16) * RB;
-                    const unsigned d2 = xs + unsigned(w1 & 0xffff) * RB, d3 = xs + (unsigned(w1) >> 16) * RB;
-                    const unsigned d4 = xs + unsigned(w2 & 0xffff) * RB, d5 = xs + (unsigned(w2) >> 16) * RB;
-                    const unsigned d6 = xs + unsigned(w3 & 0xffff) * RB, d7 = xs + (unsigned(w3) >> 16) * RB;
+                    const unsigned d0 = row_lo(xs, w0), d1 = row_hi(xs, w0);
+                    const unsigned d2 = row_lo(xs, w1), d3 = row_hi(xs, w1);
+                    const unsigned d4 = row_lo(xs, w2), d5 = row_hi(xs, w2);
+                    const unsigned d6 = row_lo(xs, w3), d7 = row_hi(xs, w3);
                     const unsigned sq = src + unsigned(q) * RB;
                     double l[8], a[8];
 #pragma unroll
@@ -457,12 +465,15 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                     sts(d6, a[6]);
                     sts(d7, a[7]);
                 }
-                for (; q < nrows; q += 4) {  // whole groups of 4; padding rows re-read the last L row
+                for (; q < nrows; q += 4) {
+                    // whole groups of 4: padding rows re-read the last L row and
+                    // land in the scratch row
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1];
-                    const unsigned d0 = xs + unsigned(w0 & 0xffff) * RB, d1 = xs + (unsigned(w0) >> 16) * RB;
-                    const unsigned d2 = xs + unsigned(w1 & 0xffff) * RB, d3 = xs + (unsigned(w1) >> 16) * RB;
+                    const unsigned d0 = row_lo(xs, w0), d1 = row_hi(xs, w0);
+                    const unsigned d2 = row_lo(xs, w1), d3 = row_hi(xs, w1);
+                    const unsigned sq = src + unsigned(q) * RB;
                     const int last = nrows - 1;
-                    const double l0 = lds(src + unsigned(q) * RB), l1 = lds(src + unsigned(min(q + 1, last)) * RB);
+                    const double l0 = lds(sq), l1 = lds(src + unsigned(min(q + 1, last)) * RB);
                     const double l2 = lds(src + unsigned(min(q + 2, last)) * RB);
                     const double l3 = lds(src + unsigned(min(q + 3, last)) * RB);
                     double a0 = lds(d0), a1 = lds(d1), a2 = lds(d2), a3 = lds(d3);
