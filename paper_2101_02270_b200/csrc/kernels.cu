@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     for (;;) {
         const int32_t* r = P.cur;
         const int type = h & 15;
-        if (type == kRecDep) {
+        if (__builtin_expect(type == kRecDep, 1)) {
             const int op = (h >> 4) - 1;
             const int kpos_fs = r[1], nrows = r[2] & 0xffff, src_row = int(unsigned(r[2]) >> 16);
             const int ysrc = r[3];
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     for (;;) {
         const int32_t* r = P.cur;
         const int type = h & 15;
-        if (type == kRecDep) {
+        if (__builtin_expect(type == kRecDep, 1)) {
             const int op = (h >> 4) - 1;
             const int ysrc = r[1];
             h = r[2];
