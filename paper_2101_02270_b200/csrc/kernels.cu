@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 const double mult = lds(xs + unsigned(kpos_fs & 0xffff) * RB);
                 const int32_t* dw = r + 4;
                 int q = 0;
+#pragma unroll 1
                 for (; q + 8 <= nrows; q += 8) {  // eight independent rows in flight
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1], w2 = dw[(q >> 1) + 2],
                                   w3 = dw[(q >> 1) + 3];
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                     sts(d6, a[6]);
                     sts(d7, a[7]);
                 }
+#pragma unroll 1
                 for (; q < nrows; q += 4) {
                     // whole groups of 4: padding rows re-read the last L row and
                     // land in the scratch row
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 if (fspos != 0xffff) acc_y = fma(-lds(src + unsigned(fspos) * RB), lds(R0 + unsigned(ysrc) * RB), acc_y);
             }
             P.cur += 4 + (n4 >> 1);
-        } else if (type == kRecIssue) {
+        } else if (__builtin_expect(type == kRecIssue, 1)) {
             P.cur += prog_issue(v, P, r, lane);
             h = P.cur[0];
         } else if (type == kRecStep) {
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             acc = fma(-lds(e), lds(R0 + unsigned(ysrc) * RB), acc);
             e += RB;
             P.cur += 2;
-        } else if (type == kRecIssue) {
+        } else if (__builtin_expect(type == kRecIssue, 1)) {
             const int len = prog_issue(v, P, r, lane);
             P.cur += len;
             h = P.cur[0];
