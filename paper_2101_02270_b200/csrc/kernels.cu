@@ -96,7 +96,7 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
 }
 
 template <bool NPM, int JMODE>
-__global__ void __launch_bounds__(256) npm_kernel(DevView v) {
+__global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = my_tile(v, blockIdx.y, warp);
     if (tile < 0) return;
