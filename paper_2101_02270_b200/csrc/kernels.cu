@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
     if (tile < 0) return;
     const int t = tile * kTile + lane;
     const size_t bp = v.bpad;
-    double* b_t = v.b + size_t(tile) * v.tstride + lane;  // tile-blocked b tape
     double* a_t = v.A + size_t(tile) * v.tstride + lane;  // tile-blocked A tape
     const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
     bool act = JMODE != kJacNone && v.active[t] != 0;
@@ -134,12 +133,12 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
         if (NPM) {
             const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
             const double fp = P - v.p0[size_t(r) * v.s_ld + ts];
-            b_t[size_t(__ldg(v.brow_p + r)) * kTile] = fp;
+            a_t[size_t(__ldg(v.fslot_p + r)) * kTile] = fp;  // F beside its A column
             nrm = fmax(nrm, nan_as_inf_abs(fp));
-            const int bq = __ldg(v.brow_q + r);
-            if (bq >= 0) {
+            const int fq_slot = __ldg(v.fslot_q + r);
+            if (fq_slot >= 0) {
                 const double fq = Q - v.q0[size_t(r) * v.s_ld + ts];
-                b_t[size_t(bq) * kTile] = fq;
+                a_t[size_t(fq_slot) * kTile] = fq;
                 nrm = fmax(nrm, nan_as_inf_abs(fq));
             }
         }
@@ -307,7 +306,7 @@ struct Prog {
     const int32_t* gs;          // stream in global memory
     const int32_t* cur;         // next record
     const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
-    int32_t tape_rows;          // rows per tape id step (nnzLU): tape t starts at row t * nnzLU
+    int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
     int W, n_pages, page;
 };
 
@@ -344,7 +343,7 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.page = 0;
     P.cur = P.pg;
     P.tb = reinterpret_cast<const char*>(v.A + size_t(tile) * v.tstride);
-    P.tape_rows = v.nnzLU;
+    P.tape_rows = v.tape_rows;
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
     __syncwarp();  // every lane's barrier is initialised before lane 0 arms the page barriers
@@ -411,13 +410,12 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
     double* lu_t = v.LU + size_t(tile) * v.tstride + lane;
-    double* b_t = v.b + size_t(tile) * v.tstride + lane;
     const double stol = v.singular_tol;
     constexpr unsigned RB = kTile * 8;  // bytes per shared row
     const unsigned R0 = smem_u32(P.R) + unsigned(lane) * 8u;
     bool flagged = false;
     unsigned xs = R0;  // this step's block
-    int len = 0, dp = 0, lslot = 0, brow = 0;
+    int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
     double acc_y = 0.0;
     int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
     for (;;) {
@@ -558,9 +556,11 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             }
             const double cmax = fmax(c0, c1);
             flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
-            if (FS) {
+            lu_t[size_t(brow + 1) * kTile] = piv;  // U(m,m) closing the backward block
+            if (FS) {  // y_m after the L rows (forward re-fetches) and in the backward block
                 sts(xs + unsigned(len) * RB, acc_y);
-                b_t[size_t(brow) * kTile] = acc_y;
+                lcol[size_t(len - dp) * kTile] = acc_y;
+                lu_t[size_t(brow) * kTile] = acc_y;
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1 + dp;

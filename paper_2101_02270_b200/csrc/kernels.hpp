@@ -30,10 +30,13 @@ struct DevView {
     const double *p0, *q0;
     int32_t s_ld, s_inc;          // p0[bus * s_ld + task * s_inc]
     // tile-blocked tapes, one block per tile of tstride doubles:
-    //   [A: nnzLU rows][LU: nnzLU rows][b: nJ rows] x 32 lanes
-    // A = the Jacobian in LU slot order, b = F, then y (forward walk), then dx.
+    //   [A: tape_rows][LU: tape_rows][b: nJ rows] x 32 lanes   (layouts: walk.hpp LuLayout)
+    // A = the Jacobian columns, each followed by F_m; LU = the factors with y;
+    // b = dx (backward walk).
     double *A, *LU, *b;           // tile 0's tapes; tile t's at + t * tstride
     size_t tstride;
+    int32_t tape_rows;            // nnzLU + 3 nJ
+    const int32_t *fslot_p, *fslot_q;  // bus -> A-tape slot of its P / Q mismatch (-1: none)
     // per-task state
     int32_t *status, *iters;
     uint8_t *active, *flag;

@@ -155,9 +155,24 @@ struct gbnr_plan {
         v.rows = dev_upload(owned, s.rows);
         v.brow_p = dev_upload(owned, s.brow_p);
         v.brow_q = dev_upload(owned, s.brow_q);
+        {
+            // A-tape slots (walk.hpp LuLayout): CCS entry z of column j at z + j,
+            // F_m right after column m
+            std::vector<int32_t> col_of(s.nnzLU);
+            for (int32_t j = 0; j < s.nJ; ++j)
+                for (int32_t z = s.cp[j]; z < s.cp[j + 1]; ++z) col_of[z] = j;
+            std::vector<int32_t> lk(s.lk.size()), fp(s.brow_p.size()), fq(s.brow_q.size());
+            for (size_t i = 0; i < lk.size(); ++i) lk[i] = s.lk[i] >= 0 ? gbnr::a_slot(s.lk[i], col_of[s.lk[i]]) : -1;
+            auto fslot = [&](int32_t m) { return m >= 0 ? gbnr::a_slot(s.cp[m + 1], m) : -1; };
+            for (size_t r = 0; r < fp.size(); ++r) fp[r] = fslot(s.brow_p[r]);
+            for (size_t r = 0; r < fq.size(); ++r) fq[r] = fslot(s.brow_q[r]);
+            v.lk = dev_upload(owned, lk);
+            v.fslot_p = dev_upload(owned, fp);
+            v.fslot_q = dev_upload(owned, fq);
+            v.tape_rows = lay.rows;
+        }
         v.zcol_t = dev_upload(owned, s.zcol_t);
         v.zcol_v = dev_upload(owned, s.zcol_v);
-        v.lk = dev_upload(owned, s.lk);
         vf = upload_walk(wf);
         vl = upload_walk(wl);
         vb = upload_walk(wb);
@@ -264,15 +279,15 @@ struct gbnr_plan {
         v.p0 = static_cast<double*>(alloc(nb));
         v.q0 = static_cast<double*>(alloc(nb));
         // one block per tile: A, LU and b rows adjacent, so a walk copy's source is
-        // tile base + (tape * nnzLU + slot) rows
-        v.tstride = (2 * size_t(v.nnzLU) + size_t(v.nJ)) * gbnr::kTile;
+        // tile base + (tape * tape_rows + slot) rows
+        v.tstride = (2 * size_t(v.tape_rows) + size_t(v.nJ)) * gbnr::kTile;
         const size_t tb = v.tstride * size_t(n_tiles) * sizeof(double);
         v.A = static_cast<double*>(alloc(tb));
         // fill slots of the A tape are never written by the Jacobian kernel and
         // must read zero; tile-blocked addresses do not depend on the batch size
         CK(cudaMemsetAsync(v.A, 0, tb, stream));
-        v.LU = v.A + size_t(v.nnzLU) * gbnr::kTile;
-        v.b = v.LU + size_t(v.nnzLU) * gbnr::kTile;
+        v.LU = v.A + size_t(v.tape_rows) * gbnr::kTile;
+        v.b = v.LU + size_t(v.tape_rows) * gbnr::kTile;
         v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
         v.iters = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
         v.active = static_cast<uint8_t*>(alloc(bpad));
@@ -602,7 +617,7 @@ struct gbnr_plan {
             std::vector<double> tape(size_t(v.n_tiles) * v.tstride);
             CK(cudaMemcpy(tape.data(), v.A, tape.size() * sizeof(double), cudaMemcpyDeviceToHost));
             for (size_t c = 0; c < z; ++c) {
-                const size_t ts = z + size_t(lay.tape_of_ccs[c]);  // LU rows follow the A rows
+                const size_t ts = size_t(v.tape_rows) + size_t(lay.tape_of_ccs[c]);  // LU rows follow the A rows
                 for (int32_t t = 0; t < nt; ++t)
                     lu_out[c * nt + t] = tape[size_t(t / gbnr::kTile) * v.tstride + ts * gbnr::kTile + t % gbnr::kTile];
             }

@@ -543,7 +543,7 @@ LuLayout build_lu_layout(const Symbolic& s) {
     int32_t at = 0;
     for (int32_t k = 0; k < nJ; ++k) {
         lay.lslot[k] = at;
-        at += s.cp[k + 1] - s.dpos[k];
+        at += s.cp[k + 1] - s.dpos[k] + 1;  // diagonal, L rows, y_k
     }
     // U rows: entries (k descending) of row i
     std::vector<int32_t> cnt(nJ, 0);
@@ -551,8 +551,9 @@ LuLayout build_lu_layout(const Symbolic& s) {
         for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) cnt[s.ri[z]]++;
     lay.ucrs0.assign(nJ + 1, 0);
     lay.ucrs0[0] = at;
-    for (int32_t i = 0; i < nJ; ++i) lay.ucrs0[i + 1] = lay.ucrs0[i] + cnt[i];
-    if (lay.ucrs0[nJ] != s.nnzLU) throw Error(2, "LU layout does not cover the pattern");
+    for (int32_t i = 0; i < nJ; ++i) lay.ucrs0[i + 1] = lay.ucrs0[i] + cnt[i] + 2;  // U row, y_i, U(i,i)
+    lay.rows = lay.ucrs0[nJ];
+    if (lay.rows != s.nnzLU + 3 * nJ) throw Error(2, "LU layout does not cover the pattern");
     lay.tape_of_ccs.assign(s.nnzLU, -1);
     std::vector<int32_t> fill(nJ, 0);
     for (int32_t k = nJ - 1; k >= 0; --k)  // descending k within each row
@@ -694,12 +695,11 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
             const int32_t c0 = s.cp[m], len = s.cp[m + 1] - c0, dp = s.dpos[m] - c0;
             StepIn& si = pr.steps[i];
             si.blk_rows = len + 1;  // row len: b / y (FS), the update padding's scratch row
-            si.copies.push_back(copy(kTapeA, c0, len, 0));
-            if (with_fs) si.copies.push_back(copy(kTapeB, m, 1, len));
+            si.copies.push_back(copy(kTapeA, a_slot(c0, m), len + 1, 0));  // column + F_m
             si.rec.len_dp = len | (dp << 16);
             si.rec.lslot = lay.lslot[m];
             si.rec.ut0 = static_cast<int32_t>(pr.ut.size());
-            si.rec.brow = m;
+            si.rec.brow = lay.ucrs0[m + 1] - 2;  // y_m, U(m,m) of the backward block
             for (int32_t z = c0; z < s.dpos[m]; ++z) pr.ut.push_back(lay.tape_of_ccs[z]);
             for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = z - c0;
             std::vector<int32_t> ks;
@@ -733,11 +733,10 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
                 const int32_t klen = s.cp[k + 1] - s.cp[k], kdp = s.dpos[k] - s.cp[k];
                 di.ring_src = kdp + 1;
                 di.ring_ysrc = with_fs ? klen : -1;
-                di.fetch.push_back(copy(kTapeLU, lay.lslot[k] + 1, nl, 0));
+                di.fetch.push_back(copy(kTapeLU, lay.lslot[k] + 1, with_fs ? nl + 1 : nl, 0));  // L rows (+ y_k)
                 di.stage_src = 0;
                 di.fetch_rows = nl;
                 if (with_fs) {
-                    di.fetch.push_back(copy(kTapeB, k, 1, nl));
                     di.stage_ysrc = nl;
                     di.fetch_rows = nl + 1;
                 }
@@ -775,9 +774,7 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
             const int32_t ne = static_cast<int32_t>(urow[i].size());
             StepIn& si = pr.steps[t];
             si.blk_rows = ne + 2;
-            if (ne > 0) si.copies.push_back(copy(kTapeLU, lay.ucrs0[i], ne, 0));
-            si.copies.push_back(copy(kTapeB, i, 1, ne));
-            si.copies.push_back(copy(kTapeLU, lay.lslot[i], 1, ne + 1));
+            si.copies.push_back(copy(kTapeLU, lay.ucrs0[i], ne + 2, 0));  // U row, y_i, U(i,i)
             si.rec.len_dp = ne;
             si.rec.lslot = lay.lslot[i];
             si.rec.brow = i;

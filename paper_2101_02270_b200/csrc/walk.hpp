@@ -126,11 +126,21 @@ struct WalkSet {
 // LU tape layout of the walks: the L+diag part of every column contiguous
 // (column-major, diagonal first) followed by U row-major (each row's entries in
 // descending column order, the backward walk's consumption order).
+// Tape layouts (rows of 256 B = 32 lanes), each sized so one walk copy moves a
+// whole block:
+//   A tape  column m: its CCS entries, then F_m           (slots cp[m] + m ...)
+//   LU tape column k: diagonal, L rows, then y_k           (lslot[k] ...)
+//           row i:    U entries (k descending), y_i, U(i,i) (ucrs0[i] ...)
+// so a step block, a re-fetched dependency (L rows + y) and a backward block
+// are one contiguous copy each.
 struct LuLayout {
     std::vector<int32_t> lslot;        // [nJ] slot of the diagonal of column k
-    std::vector<int32_t> ucrs0;        // [nJ+1] first U-CRS slot of row i
+    std::vector<int32_t> ucrs0;        // [nJ+1] first U-CRS slot of row i (then y_i, U(i,i))
     std::vector<int32_t> tape_of_ccs;  // [nnzLU] CCS slot -> tape slot
+    int32_t rows = 0;                  // LU tape rows: nnzLU + 3 nJ
 };
+// A tape slot of CCS entry z of column j / of F_m
+inline int32_t a_slot(int32_t z, int32_t j) { return z + j; }
 
 LuLayout build_lu_layout(const Symbolic& s);
 // Columns -> (level, walker) by splitting the elimination tree into whole

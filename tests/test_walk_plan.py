@@ -161,9 +161,9 @@ def run_phases(w, tapes, step_fn):
     return R
 
 
-def replay_forward(w, A, b_tape, nnz, fs=True):
-    LU = np.full((nnz, 32), np.nan)
-    tapes = {TAPE_A: A, TAPE_LU: LU, TAPE_B: b_tape}
+def replay_forward(w, A_tape, nrows, fs=True):
+    LU = np.full((nrows, 32), np.nan)
+    tapes = {TAPE_A: A_tape, TAPE_LU: LU, TAPE_B: None}
 
     def step(M, r, t, S):
         R = M.R
@@ -186,7 +186,7 @@ def replay_forward(w, A, b_tape, nnz, fs=True):
             return 4 + ((nrows + 3) & ~3) // 2
         if t == REC_STEP:
             ring, ln = int(r[1]) & 0xFFFF, int(r[1]) >> 16
-            S.update(ring=ring, ln=ln, dp=int(r[2]), lslot=int(r[3]), brow=int(r[4]))
+            S.update(ring=ring, ln=ln, dp=int(r[2]), lslot=int(r[3]), uy=int(r[4]))
             M.wait(int(r[5]))
             S["x"] = R[ring:ring + ln]
             S["acc"] = R[ring + ln].copy() if fs else None
@@ -201,9 +201,11 @@ def replay_forward(w, A, b_tape, nnz, fs=True):
             LU[lslot + z - dp] = x[z]
         for z in range(dp):
             LU[int(r[1 + z])] = x[z]
-        if fs:
+        LU[S["uy"] + 1] = piv  # U(m,m) closing the backward block
+        if fs:  # y_m after the L rows and in the backward block
             R[S["ring"] + ln] = S["acc"]
-            b_tape[S["brow"]] = S["acc"]
+            LU[lslot + ln - dp] = S["acc"]
+            LU[S["uy"]] = S["acc"]
         return 1 + dp
 
     run_phases(w, tapes, step)
@@ -251,15 +253,26 @@ def test_walk_replay_bitwise(name, opts):
     ex, A, b = jacobian_tape(gc, plan)
     lu_ref, y_ref, x_ref = sequential(ex, A, b)
     wf, wl, wb = plan.walk_export(0), plan.walk_export(1), plan.walk_export(2)
-    toc = wf["tape_of_ccs"]
-    nnz = len(toc)
-    b_tape = b.copy()
-    LU = replay_forward(wf, A, b_tape, nnz, fs=True)
+    toc, lslot, ucrs0 = wf["tape_of_ccs"], wf["lslot"], wf["ucrs0"]
+    cp, ri = ex["col_ptr"], ex["row_ix"]
+    nJ = len(cp) - 1
+    nrows = len(toc) + 3 * nJ
+    assert ucrs0[-1] == nrows
+    # A tape: every column's CCS entries followed by its F row (walk.hpp LuLayout)
+    A_tape = np.full((len(toc) + nJ, 32), np.nan)
+    for m in range(nJ):
+        A_tape[cp[m] + m:cp[m + 1] + m] = A[cp[m]:cp[m + 1]]
+        A_tape[cp[m + 1] + m] = b[m]
+    LU = replay_forward(wf, A_tape, nrows, fs=True)
     np.testing.assert_array_equal(LU[toc], lu_ref)
-    np.testing.assert_array_equal(b_tape, y_ref)
+    dpos = np.array([cp[k] + np.searchsorted(ri[cp[k]:cp[k + 1]], k) for k in range(nJ)])
+    np.testing.assert_array_equal(LU[lslot + cp[1:] - dpos], y_ref)  # y_k after L(:,k)
+    np.testing.assert_array_equal(LU[ucrs0[1:] - 2], y_ref)  # and in row k's backward block
+    np.testing.assert_array_equal(LU[ucrs0[1:] - 1], LU[lslot])  # U(k,k) closing it
+    b_tape = np.full((nJ, 32), np.nan)
     replay_backward(wb, LU, b_tape)
     np.testing.assert_array_equal(b_tape, x_ref)
-    LU2 = replay_forward(wl, A, b.copy(), nnz, fs=False)
+    LU2 = replay_forward(wl, A_tape, nrows, fs=False)
     np.testing.assert_array_equal(LU2[toc], lu_ref)
     plan.close()
 
@@ -275,7 +288,9 @@ def test_walk_stats_and_layout():
         assert info["smem_bytes"] + 1024 <= 228 * 1024 // 3  # three tiles per SM
     w = plan.walk_export(0)
     toc = w["tape_of_ccs"]
-    assert sorted(toc.tolist()) == list(range(st["nnzLU"]))  # a permutation of the slots
+    # the pattern's slots plus, per column, y after L(:,k) and (y, U(k,k)) after U row k
+    extra = np.r_[w["lslot"] + np.diff(w["lslot"], append=w["ucrs0"][0]) - 1, w["ucrs0"][1:] - 2, w["ucrs0"][1:] - 1]
+    assert sorted(np.r_[toc, extra].tolist()) == list(range(st["nnzLU"] + 3 * st["nJ"]))
     own = w["owner"]
     level, walker = own >> 4, own & 15
     assert set(np.unique(level)) <= {0, 1, 2, 3}
