@@ -515,8 +515,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const double piv = lds(xs + unsigned(dp) * RB);
             const double inv = 1.0 / piv;
             double c0 = fabs(piv), c1 = 0.0;
-            double* lcol = lu_t + size_t(lslot) * kTile;  // diagonal, then L rows
-            lcol[0] = piv;
+            double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * kTile;  // L row z of x at lcol[z], y at lcol[len]
             int z = dp + 1;
             for (; z + 2 <= len; z += 2) {
                 const double x0 = lds(xs + unsigned(z) * RB), x1 = lds(xs + unsigned(z + 1) * RB);
@@ -525,15 +524,15 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 const double l0 = x0 * inv, l1 = x1 * inv;
                 sts(xs + unsigned(z) * RB, l0);
                 sts(xs + unsigned(z + 1) * RB, l1);
-                lcol[size_t(z - dp) * kTile] = l0;
-                lcol[size_t(z + 1 - dp) * kTile] = l1;
+                lcol[size_t(z) * kTile] = l0;
+                lcol[size_t(z + 1) * kTile] = l1;
             }
             if (z < len) {
                 const double x0 = lds(xs + unsigned(z) * RB);
                 c0 = fmax(c0, fabs(x0));
                 const double l0 = x0 * inv;
                 sts(xs + unsigned(z) * RB, l0);
-                lcol[size_t(z - dp) * kTile] = l0;
+                lcol[size_t(z) * kTile] = l0;
             }
             z = 0;
             for (; z + 4 <= dp; z += 4) {  // U part -> its row-major slots
@@ -559,7 +558,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             lu_t[size_t(brow + 1) * kTile] = piv;  // U(m,m) closing the backward block
             if (FS) {  // y_m after the L rows (forward re-fetches) and in the backward block
                 sts(xs + unsigned(len) * RB, acc_y);
-                lcol[size_t(len - dp) * kTile] = acc_y;
+                lcol[size_t(len) * kTile] = acc_y;
                 lu_t[size_t(brow) * kTile] = acc_y;
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it

@@ -345,9 +345,24 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
     auto issue_upto = [&](int64_t ev) {
         while (next < w.op.size() && w.op[next].after <= ev) {
             const WOp& o = w.op[next];
-            std::vector<int32_t> rec{kRecIssue | (o.ncopy << 4), op_base + int32_t(next), o.bytes};
+            // copies that continue each other in the tape and in shared memory
+            // (dependencies k, k+1 staged side by side) travel as one
+            std::vector<WCopy> cps;
             for (int32_t i = 0; i < o.ncopy; ++i) {
                 const WCopy& c = w.copies[o.c0 + i];
+                if (!cps.empty()) {
+                    WCopy& p = cps.back();
+                    const int32_t pr = p.tape_rows >> 8, cr = c.tape_rows >> 8;
+                    if ((p.tape_rows & 0xff) == (c.tape_rows & 0xff) && c.slot == p.slot + pr &&
+                        c.smem == p.smem + pr && pr + cr < 1024) {
+                        p.tape_rows = (p.tape_rows & 0xff) | ((pr + cr) << 8);
+                        continue;
+                    }
+                }
+                cps.push_back(c);
+            }
+            std::vector<int32_t> rec{kRecIssue | (int32_t(cps.size()) << 4), op_base + int32_t(next), o.bytes};
+            for (const WCopy& c : cps) {
                 const int32_t tape = c.tape_rows & 0xff, rows = c.tape_rows >> 8;
                 if (rows >= 1024 || c.smem >= (1 << 20)) throw Error(3, "walk copy too large to encode");
                 rec.push_back(tape | (rows << 2) | (c.smem << 12));
@@ -543,7 +558,7 @@ LuLayout build_lu_layout(const Symbolic& s) {
     int32_t at = 0;
     for (int32_t k = 0; k < nJ; ++k) {
         lay.lslot[k] = at;
-        at += s.cp[k + 1] - s.dpos[k] + 1;  // diagonal, L rows, y_k
+        at += s.cp[k + 1] - s.dpos[k];  // L rows, y_k
     }
     // U rows: entries (k descending) of row i
     std::vector<int32_t> cnt(nJ, 0);
@@ -553,7 +568,7 @@ LuLayout build_lu_layout(const Symbolic& s) {
     lay.ucrs0[0] = at;
     for (int32_t i = 0; i < nJ; ++i) lay.ucrs0[i + 1] = lay.ucrs0[i] + cnt[i] + 2;  // U row, y_i, U(i,i)
     lay.rows = lay.ucrs0[nJ];
-    if (lay.rows != s.nnzLU + 3 * nJ) throw Error(2, "LU layout does not cover the pattern");
+    if (lay.rows != s.nnzLU + 2 * nJ) throw Error(2, "LU layout does not cover the pattern");
     lay.tape_of_ccs.assign(s.nnzLU, -1);
     std::vector<int32_t> fill(nJ, 0);
     for (int32_t k = nJ - 1; k >= 0; --k)  // descending k within each row
@@ -561,8 +576,10 @@ LuLayout build_lu_layout(const Symbolic& s) {
             const int32_t i = s.ri[z];
             lay.tape_of_ccs[z] = lay.ucrs0[i] + fill[i]++;
         }
-    for (int32_t k = 0; k < nJ; ++k)
-        for (int32_t z = s.dpos[k]; z < s.cp[k + 1]; ++z) lay.tape_of_ccs[z] = lay.lslot[k] + (z - s.dpos[k]);
+    for (int32_t k = 0; k < nJ; ++k) {
+        lay.tape_of_ccs[s.dpos[k]] = lay.ucrs0[k + 1] - 1;  // U(k,k) closes row k's block
+        for (int32_t z = s.dpos[k] + 1; z < s.cp[k + 1]; ++z) lay.tape_of_ccs[z] = lay.lslot[k] + (z - s.dpos[k] - 1);
+    }
     return lay;
 }
 
@@ -733,7 +750,7 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
                 const int32_t klen = s.cp[k + 1] - s.cp[k], kdp = s.dpos[k] - s.cp[k];
                 di.ring_src = kdp + 1;
                 di.ring_ysrc = with_fs ? klen : -1;
-                di.fetch.push_back(copy(kTapeLU, lay.lslot[k] + 1, with_fs ? nl + 1 : nl, 0));  // L rows (+ y_k)
+                di.fetch.push_back(copy(kTapeLU, lay.lslot[k], with_fs ? nl + 1 : nl, 0));  // L rows (+ y_k)
                 di.stage_src = 0;
                 di.fetch_rows = nl;
                 if (with_fs) {

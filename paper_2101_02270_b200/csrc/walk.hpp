@@ -40,7 +40,7 @@ struct WStep {
     int32_t len_dp;  // forward: len | dp << 16; backward: number of U entries
     int32_t dep0;    // first WDep
     int32_t ndep;    // number of WDep
-    int32_t lslot;   // LU-tape slot of the diagonal (L+diag region, len-dp rows)
+    int32_t lslot;   // LU-tape slot of the first L row (L rows, then y)
     int32_t ut0;     // forward: first index into the U-scatter list (dp entries)
     int32_t op;      // op carrying the block
     int32_t brow;    // b-tape row of the step (LU row / column index)
@@ -129,15 +129,16 @@ struct WalkSet {
 // Tape layouts (rows of 256 B = 32 lanes), each sized so one walk copy moves a
 // whole block:
 //   A tape  column m: its CCS entries, then F_m           (slots cp[m] + m ...)
-//   LU tape column k: diagonal, L rows, then y_k           (lslot[k] ...)
+//   LU tape column k: L rows, then y_k                     (lslot[k] ...)
 //           row i:    U entries (k descending), y_i, U(i,i) (ucrs0[i] ...)
 // so a step block, a re-fetched dependency (L rows + y) and a backward block
-// are one contiguous copy each.
+// are one contiguous copy each, and the dependencies k, k+1 re-fetched side by
+// side merge into one copy.
 struct LuLayout {
-    std::vector<int32_t> lslot;        // [nJ] slot of the diagonal of column k
+    std::vector<int32_t> lslot;        // [nJ] slot of the first L row of column k
     std::vector<int32_t> ucrs0;        // [nJ+1] first U-CRS slot of row i (then y_i, U(i,i))
     std::vector<int32_t> tape_of_ccs;  // [nnzLU] CCS slot -> tape slot
-    int32_t rows = 0;                  // LU tape rows: nnzLU + 3 nJ
+    int32_t rows = 0;                  // LU tape rows: nnzLU + 2 nJ
 };
 // A tape slot of CCS entry z of column j / of F_m
 inline int32_t a_slot(int32_t z, int32_t j) { return z + j; }

@@ -195,16 +195,15 @@ def replay_forward(w, A_tape, nrows, fs=True):
         x, dp, ln, lslot = S["x"], S["dp"], S["ln"], S["lslot"]
         piv = x[dp].copy()
         inv = 1.0 / piv
-        LU[lslot] = piv
         for z in range(dp + 1, ln):
             x[z] = x[z] * inv
-            LU[lslot + z - dp] = x[z]
+            LU[lslot + z - dp - 1] = x[z]
         for z in range(dp):
             LU[int(r[1 + z])] = x[z]
         LU[S["uy"] + 1] = piv  # U(m,m) closing the backward block
         if fs:  # y_m after the L rows and in the backward block
             R[S["ring"] + ln] = S["acc"]
-            LU[lslot + ln - dp] = S["acc"]
+            LU[lslot + ln - dp - 1] = S["acc"]
             LU[S["uy"]] = S["acc"]
         return 1 + dp
 
@@ -256,7 +255,7 @@ def test_walk_replay_bitwise(name, opts):
     toc, lslot, ucrs0 = wf["tape_of_ccs"], wf["lslot"], wf["ucrs0"]
     cp, ri = ex["col_ptr"], ex["row_ix"]
     nJ = len(cp) - 1
-    nrows = len(toc) + 3 * nJ
+    nrows = len(toc) + 2 * nJ
     assert ucrs0[-1] == nrows
     # A tape: every column's CCS entries followed by its F row (walk.hpp LuLayout)
     A_tape = np.full((len(toc) + nJ, 32), np.nan)
@@ -266,9 +265,9 @@ def test_walk_replay_bitwise(name, opts):
     LU = replay_forward(wf, A_tape, nrows, fs=True)
     np.testing.assert_array_equal(LU[toc], lu_ref)
     dpos = np.array([cp[k] + np.searchsorted(ri[cp[k]:cp[k + 1]], k) for k in range(nJ)])
-    np.testing.assert_array_equal(LU[lslot + cp[1:] - dpos], y_ref)  # y_k after L(:,k)
+    np.testing.assert_array_equal(LU[lslot + cp[1:] - dpos - 1], y_ref)  # y_k after L(:,k)
     np.testing.assert_array_equal(LU[ucrs0[1:] - 2], y_ref)  # and in row k's backward block
-    np.testing.assert_array_equal(LU[ucrs0[1:] - 1], LU[lslot])  # U(k,k) closing it
+    np.testing.assert_array_equal(toc[dpos], ucrs0[1:] - 1)  # U(k,k) closing it
     b_tape = np.full((nJ, 32), np.nan)
     replay_backward(wb, LU, b_tape)
     np.testing.assert_array_equal(b_tape, x_ref)
@@ -288,9 +287,9 @@ def test_walk_stats_and_layout():
         assert info["smem_bytes"] + 1024 <= 228 * 1024 // 3  # three tiles per SM
     w = plan.walk_export(0)
     toc = w["tape_of_ccs"]
-    # the pattern's slots plus, per column, y after L(:,k) and (y, U(k,k)) after U row k
-    extra = np.r_[w["lslot"] + np.diff(w["lslot"], append=w["ucrs0"][0]) - 1, w["ucrs0"][1:] - 2, w["ucrs0"][1:] - 1]
-    assert sorted(np.r_[toc, extra].tolist()) == list(range(st["nnzLU"] + 3 * st["nJ"]))
+    # the pattern's slots plus, per column, y after L(:,k) and y before U(k,k) closing row k
+    extra = np.r_[w["lslot"] + np.diff(w["lslot"], append=w["ucrs0"][0]) - 1, w["ucrs0"][1:] - 2]
+    assert sorted(np.r_[toc, extra].tolist()) == list(range(st["nnzLU"] + 2 * st["nJ"]))
     own = w["owner"]
     level, walker = own >> 4, own & 15
     assert set(np.unique(level)) <= {0, 1, 2, 3}
