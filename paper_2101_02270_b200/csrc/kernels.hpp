@@ -32,7 +32,7 @@ struct DevView {
     // tile-blocked tapes, one block per tile of tstride doubles:
     //   [A: tape_rows][LU: tape_rows][b: nJ rows] x 32 lanes   (layouts: walk.hpp LuLayout)
     // A = the Jacobian columns, each followed by F_m; LU = the factors with y;
-    // b = dx (backward walk).
+    // b = dx, row nJ-1-k for J column k (backward walk).
     double *A, *LU, *b;           // tile 0's tapes; tile t's at + t * tstride
     size_t tstride;
     int32_t tape_rows;            // nnzLU + 3 nJ

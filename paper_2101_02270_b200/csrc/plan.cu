@@ -171,8 +171,15 @@ struct gbnr_plan {
             v.fslot_q = dev_upload(owned, fq);
             v.tape_rows = lay.rows;
         }
-        v.zcol_t = dev_upload(owned, s.zcol_t);
-        v.zcol_v = dev_upload(owned, s.zcol_v);
+        {
+            // dx_k sits at b-tape row nJ-1-k (walk.hpp: the backward walk's
+            // descending dependencies then re-fetch ascending rows and merge)
+            std::vector<int32_t> zt(s.zcol_t), zv(s.zcol_v);
+            for (int32_t& z : zt) z = z >= 0 ? s.nJ - 1 - z : -1;
+            for (int32_t& z : zv) z = z >= 0 ? s.nJ - 1 - z : -1;
+            v.zcol_t = dev_upload(owned, zt);
+            v.zcol_v = dev_upload(owned, zv);
+        }
         vf = upload_walk(wf);
         vl = upload_walk(wl);
         vb = upload_walk(wb);

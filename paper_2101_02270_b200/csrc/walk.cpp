@@ -794,12 +794,12 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
             si.copies.push_back(copy(kTapeLU, lay.ucrs0[i], ne + 2, 0));  // U row, y_i, U(i,i)
             si.rec.len_dp = ne;
             si.rec.lslot = lay.lslot[i];
-            si.rec.brow = i;
+            si.rec.brow = nJ - 1 - i;  // x_i's b-tape row: descending k re-fetches ascending rows
             for (int32_t k : urow[i]) {
                 DepIn di;
                 di.producer = local[k] >= 0 && local[k] < int32_t(t) ? local[k] : -1;
                 di.ring_ysrc = static_cast<int32_t>(urow[k].size());
-                di.fetch.push_back(copy(kTapeB, k, 1, 0));
+                di.fetch.push_back(copy(kTapeB, nJ - 1 - k, 1, 0));
                 di.stage_ysrc = 0;
                 di.fetch_rows = 1;
                 si.deps.push_back(std::move(di));
