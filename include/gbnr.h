@@ -72,7 +72,7 @@ typedef struct gbnr_options {
     int32_t profile;       /* 1 = record per-phase CUDA-event timings               */
     int32_t stage_rows;    /* per-walker staging ring rows (0 = auto)              */
     int32_t prefetch;      /* steps a walk copy may run ahead (0 = 8)              */
-    int32_t headroom;      /* ring residency margin in steps (0 = 2)               */
+    int32_t headroom;      /* ring residency margin in steps (0 = 1)               */
     int32_t walkers;       /* warps per tile walking disjoint subtrees (0 = 8, <= 8) */
     int32_t jacobian;      /* when the next Jacobian is built: 0 = inside the mismatch
                               sweep unless the task is predicted to converge at that

@@ -76,11 +76,11 @@ struct WalkConfig {
     int32_t stage_rows = 0;       // per-walker staging override (0 = from the budget)
     int32_t barriers = 32;        // mbarriers per walker (op i uses barrier i % 32)
     int32_t prefetch = 8;         // steps an op may run ahead of its consumer
-    int32_t headroom = 2;         // ring residency margin (steps) before an overwrite
+    int32_t headroom = 1;         // ring residency margin (steps) before an overwrite
     int32_t page_words = 128;     // program-stream page (grown to the longest record)
     int32_t pages = 2;            // program-stream pages resident per walker
     double balance = 2.0;         // split subtrees heavier than total / (walkers * balance)
-    double stage_frac = 0.4;      // staging share of a walker's rows
+    double stage_frac = 0.35;     // staging share of a walker's rows
 };
 
 // The device program of a walk: per walker one int32 word stream the warp
