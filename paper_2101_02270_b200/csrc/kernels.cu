@@ -429,6 +429,14 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             h = r[4 + (n4 >> 1)];
             if (op >= 0) prog_wait(P, op);
             const unsigned src = R0 + unsigned(src_row) * RB;
+            // forward-substitution operands first: they live in other blocks than
+            // the x being updated, so their latency hides under the update
+            const int fspos = int(unsigned(kpos_fs) >> 16);
+            double fl = 0.0, fy = 0.0;
+            if (FS && fspos != 0xffff) {
+                fl = lds(src + unsigned(fspos) * RB);
+                fy = lds(R0 + unsigned(ysrc) * RB);
+            }
             if (nrows > 0) {
                 const double mult = lds(xs + unsigned(kpos_fs & 0xffff) * RB);
                 const int32_t* dw = r + 4;
@@ -487,10 +495,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                     sts(d3, a3);
                 }
             }
-            if (FS) {
-                const int fspos = int(unsigned(kpos_fs) >> 16);
-                if (fspos != 0xffff) acc_y = fma(-lds(src + unsigned(fspos) * RB), lds(R0 + unsigned(ysrc) * RB), acc_y);
-            }
+            if (FS && fspos != 0xffff) acc_y = fma(-fl, fy, acc_y);
             P.cur += 4 + (n4 >> 1);
         } else if (__builtin_expect(type == kRecIssue, 1)) {
             P.cur += prog_issue(v, P, r, lane);
