@@ -421,7 +421,58 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     for (;;) {
         const int32_t* r = P.cur;
         const int type = h & 15;
-        if (__builtin_expect(type == kRecDep, 1)) {
+        if (__builtin_expect(type == kRecDep2, 1)) {
+            // supernode pair k, k+1: x[kpos2] -= m1 L(k+1,k) gives m2; then every
+            // other row gets k's update, then k+1's (the oracle's order per element)
+            const int op = (h >> 4) - 1;
+            const int w1 = r[1], w2 = r[2], w3 = r[3], w4 = r[4], fs2 = r[5];
+            const int nrows = w2 & 0xffff;
+            const int n4 = (nrows + 3) & ~3;
+            h = r[6 + (n4 >> 1)];
+            if (op >= 0) prog_wait(P, op);
+            const unsigned s1 = R0 + (unsigned(w2) >> 16) * RB, s2 = R0 + unsigned(w3 & 0xffff) * RB;
+            const int fs1 = int(unsigned(w3) >> 16);
+            double fl1 = 0.0, fy1 = 0.0, fl2 = 0.0, fy2 = 0.0;
+            if (FS && fs1 != 0xffff) {
+                fl1 = lds(s1 + unsigned(fs1) * RB);
+                fy1 = lds(R0 + unsigned(w4 & 0xffff) * RB);
+            }
+            if (FS && fs2 != 0xffff) {
+                fl2 = lds(s2 + unsigned(fs2) * RB);
+                fy2 = lds(R0 + (unsigned(w4) >> 16) * RB);
+            }
+            const double m1 = lds(xs + unsigned(w1 & 0xffff) * RB);
+            const unsigned p2 = xs + (unsigned(w1) >> 16) * RB;
+            const double m2 = fma(-m1, lds(s1), lds(p2));
+            sts(p2, m2);
+            const int32_t* dw = r + 6;
+            const int last = nrows - 1;
+#pragma unroll 1
+            for (int q = 0; q < nrows; q += 4) {
+                const int32_t v0 = dw[q >> 1], v1 = dw[(q >> 1) + 1];
+                const unsigned d0 = row_lo(xs, v0), d1 = row_hi(xs, v0);
+                const unsigned d2 = row_lo(xs, v1), d3 = row_hi(xs, v1);
+                const int q1 = min(q + 1, last), q2 = min(q + 2, last), q3 = min(q + 3, last);
+                const double a0 = lds(s1 + unsigned(q + 1) * RB), a1 = lds(s1 + unsigned(q1 + 1) * RB);
+                const double a2 = lds(s1 + unsigned(q2 + 1) * RB), a3 = lds(s1 + unsigned(q3 + 1) * RB);
+                const double b0 = lds(s2 + unsigned(q) * RB), b1 = lds(s2 + unsigned(q1) * RB);
+                const double b2 = lds(s2 + unsigned(q2) * RB), b3 = lds(s2 + unsigned(q3) * RB);
+                double x0 = lds(d0), x1 = lds(d1), x2 = lds(d2), x3 = lds(d3);
+                x0 = fma(-m2, b0, fma(-m1, a0, x0));
+                x1 = fma(-m2, b1, fma(-m1, a1, x1));
+                x2 = fma(-m2, b2, fma(-m1, a2, x2));
+                x3 = fma(-m2, b3, fma(-m1, a3, x3));
+                sts(d0, x0);
+                sts(d1, x1);
+                sts(d2, x2);
+                sts(d3, x3);
+            }
+            if (FS) {
+                if (fs1 != 0xffff) acc_y = fma(-fl1, fy1, acc_y);
+                if (fs2 != 0xffff) acc_y = fma(-fl2, fy2, acc_y);
+            }
+            P.cur += 6 + (n4 >> 1);
+        } else if (__builtin_expect(type == kRecDep, 1)) {
             const int op = (h >> 4) - 1;
             const int kpos_fs = r[1], nrows = r[2] & 0xffff, src_row = int(unsigned(r[2]) >> 16);
             const int ysrc = r[3];

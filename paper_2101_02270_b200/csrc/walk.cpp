@@ -336,6 +336,19 @@ struct Emitter {
     }
 };
 
+// Two consecutive forward dependencies k, k+1 of one step form a supernode
+// pair when L(:,k) is row k+1 followed by exactly the rows of L(:,k+1) (so the
+// destinations of k are kpos(k+1) then those of k+1) and the second needs no
+// wait of its own.  Every x element still sees k's update before k+1's.
+bool pairable(const Walk& w, const WDep& e, const WDep& f) {
+    if (e.nrows <= 0 || f.nrows < 0 || e.nrows != f.nrows + 1 || f.op >= 0) return false;
+    if ((f.kpos_fs & 0xffff) == 0xffff || f.nrows == 0) return false;
+    if (int32_t(w.dst[e.u0]) != (f.kpos_fs & 0xffff)) return false;
+    for (int32_t r = 0; r < f.nrows; ++r)
+        if (w.dst[e.u0 + 1 + r] != w.dst[f.u0 + r]) return false;
+    return e.ysrc < 65536 && f.ysrc < 65536 && f.src < 65536;
+}
+
 // Serialise one verified program: prologue issues, then per step: STEP,
 // (DEP, ISSUE*) per dependency, END, ISSUE* -- each ISSUE right after the
 // consumer event it waits for.  Op numbers continue at op_base (barrier parity
@@ -382,6 +395,24 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
             for (int32_t d = 0; d < s.ndep; ++d) {
                 const WDep& e = w.dep[s.dep0 + d];
                 if (e.src >= 65536 || e.nrows >= 65536) throw Error(3, "walk dependency too large to encode");
+                if (d + 1 < s.ndep && pairable(w, e, w.dep[s.dep0 + d + 1])) {
+                    // supernode pair: dep k's rows are row k+1 (x position kpos2) then
+                    // exactly dep k+1's rows; one pass applies both in order
+                    const WDep& f = w.dep[s.dep0 + d + 1];
+                    const int32_t kpos1 = e.kpos_fs & 0xffff, fs1 = int32_t(unsigned(e.kpos_fs) >> 16);
+                    const int32_t kpos2 = f.kpos_fs & 0xffff, fs2 = int32_t(unsigned(f.kpos_fs) >> 16);
+                    std::vector<int32_t> rec{kRecDep2 | ((opn(e.op) + 1) << 4), kpos1 | (kpos2 << 16),
+                                             f.nrows | (std::max(e.src, 0) << 16), std::max(f.src, 0) | (fs1 << 16),
+                                             (std::max(e.ysrc, 0) & 0xffff) | (std::max(f.ysrc, 0) << 16), fs2};
+                    const int32_t n4 = (f.nrows + 3) & ~3;
+                    auto dst = [&](int32_t r) { return r < f.nrows ? int32_t(w.dst[f.u0 + r]) : len; };
+                    for (int32_t r = 0; r < n4; r += 2) rec.push_back(dst(r) | (dst(r + 1) << 16));
+                    em.emit(rec);
+                    issue_upto(ev++);
+                    issue_upto(ev++);
+                    ++d;
+                    continue;
+                }
                 std::vector<int32_t> rec{kRecDep | ((opn(e.op) + 1) << 4), e.kpos_fs,
                                          e.nrows | (std::max(e.src, 0) << 16), e.ysrc};
                 // destinations padded to a multiple of 4 with the block's spare

@@ -82,7 +82,7 @@ def sequential(ex, A, b):
     return lu, y, x
 
 
-REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC = 1, 2, 3, 4, 5, 6, 7
+REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC, REC_DEP2 = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 class Machine:
@@ -184,6 +184,26 @@ def replay_forward(w, A_tape, nrows, fs=True):
             if fs and fsp != 0xFFFF:
                 S["acc"] = S["acc"] - R[src + fsp] * R[ysrc]
             return 4 + ((nrows + 3) & ~3) // 2
+        if t == REC_DEP2:  # supernode pair k, k+1 in one pass, k's update first per element
+            op = (h >> 4) - 1
+            w1, w2, w3, w4, fs2 = (int(v) for v in r[1:6])
+            if op >= 0:
+                M.wait(op)
+            x = S["x"]
+            kpos1, kpos2, nrows, s1 = w1 & 0xFFFF, w1 >> 16, w2 & 0xFFFF, w2 >> 16
+            s2, fs1, y1, y2 = w3 & 0xFFFF, w3 >> 16, w4 & 0xFFFF, w4 >> 16
+            m1 = x[kpos1].copy()
+            x[kpos2] = x[kpos2] - m1 * R[s1]
+            m2 = x[kpos2].copy()
+            for q in range(nrows):
+                wq = int(r[6 + q // 2])
+                d = (wq >> 16) & 0xFFFF if q & 1 else wq & 0xFFFF
+                x[d] = (x[d] - m1 * R[s1 + 1 + q]) - m2 * R[s2 + q]
+            if fs and fs1 != 0xFFFF:
+                S["acc"] = S["acc"] - R[s1 + fs1] * R[y1]
+            if fs and fs2 != 0xFFFF:
+                S["acc"] = S["acc"] - R[s2 + fs2] * R[y2]
+            return 6 + ((nrows + 3) & ~3) // 2
         if t == REC_STEP:
             ring, ln = int(r[1]) & 0xFFFF, int(r[1]) >> 16
             S.update(ring=ring, ln=ln, dp=int(r[2]), lslot=int(r[3]), uy=int(r[4]))
