@@ -652,14 +652,25 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     for (;;) {
         const int32_t* r = P.cur;
         const int type = h & 15;
-        if (__builtin_expect(type == kRecDep, 1)) {
+        if (__builtin_expect(type == kRecDepN, 1)) {
             const int op = (h >> 4) - 1;
-            const int ysrc = r[1];
-            h = r[2];
+            const int n = r[1];
+            h = r[2 + ((n + 1) >> 1)];
             if (op >= 0) prog_wait(P, op);
-            acc = fma(-lds(e), lds(R0 + unsigned(ysrc) * RB), acc);
-            e += RB;
-            P.cur += 2;
+            const int32_t* yw = r + 2;
+            int i = 0;
+            for (; i + 2 <= n; i += 2) {  // acc -= U(i,k) x_k, k descending (operand loads paired)
+                const int32_t w2 = yw[i >> 1];
+                const double u0 = lds(e), x0 = lds(row_lo(R0, w2)), u1 = lds(e + RB), x1 = lds(row_hi(R0, w2));
+                acc = fma(-u0, x0, acc);
+                acc = fma(-u1, x1, acc);
+                e += 2 * RB;
+            }
+            if (i < n) {
+                acc = fma(-lds(e), lds(row_lo(R0, yw[i >> 1])), acc);
+                e += RB;
+            }
+            P.cur += 2 + ((n + 1) >> 1);
         } else if (__builtin_expect(type == kRecIssue, 1)) {
             const int len = prog_issue(v, P, r, lane);
             P.cur += len;

@@ -430,10 +430,22 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
             issue_upto(ev++);
         } else {
             em.emit({kRecStep | (s.ndep << 4), s.ring | (s.len_dp << 16), 0, s.lslot, s.brow, opn(s.op)});
-            for (int32_t d = 0; d < s.ndep; ++d) {
-                const WDep& e = w.dep[s.dep0 + d];
-                em.emit({kRecDep | ((opn(e.op) + 1) << 4), e.ysrc});
-                issue_upto(ev++);
+            // runs of dependencies that need no wait of their own travel in one
+            // record (their copy issues follow the run)
+            const int32_t max_run = 2 * (em.W - 4);
+            for (int32_t d = 0; d < s.ndep;) {
+                int32_t n = 1;
+                while (d + n < s.ndep && n < max_run && w.dep[s.dep0 + d + n].op < 0) ++n;
+                std::vector<int32_t> rec{kRecDepN | ((opn(w.dep[s.dep0 + d].op) + 1) << 4), n};
+                for (int32_t i = 0; i < n; i += 2) {
+                    const int32_t lo = w.dep[s.dep0 + d + i].ysrc;
+                    const int32_t hi = i + 1 < n ? w.dep[s.dep0 + d + i + 1].ysrc : 0;
+                    if (lo >= 65536 || hi >= 65536) throw Error(3, "walk dependency too large to encode");
+                    rec.push_back(lo | (hi << 16));
+                }
+                em.emit(rec);
+                for (int32_t i = 0; i < n; ++i) issue_upto(ev++);
+                d += n;
             }
             em.emit({kRecEnd});
             issue_upto(ev++);

@@ -101,6 +101,9 @@ enum : int32_t {
     // nrows2 | src1 << 16, src2 | fspos1 << 16, ysrc1 | ysrc2 << 16, fspos2,
     // dst u16 pairs of L(:,k+1) (padded to 4)
     kRecDep2 = 8,
+    // bwd: n consecutive dependencies, only the first may wait:
+    // 9 | (op + 1) << 4, n, ysrc u16 pairs
+    kRecDepN = 9,
 };
 
 // One verified single-walker program (one walker in one phase).

@@ -82,7 +82,7 @@ def sequential(ex, A, b):
     return lu, y, x
 
 
-REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC, REC_DEP2 = 1, 2, 3, 4, 5, 6, 7, 8
+REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC, REC_DEP2, REC_DEPN = 1, 2, 3, 4, 5, 6, 7, 8, 9
 
 
 class Machine:
@@ -237,13 +237,17 @@ def replay_backward(w, LU, b_tape):
     def step(M, r, t, S):
         R = M.R
         h = int(r[0])
-        if t == REC_DEP:
+        if t == REC_DEPN:
             op = (h >> 4) - 1
             if op >= 0:
                 M.wait(op)
-            S["acc"] = S["acc"] - R[S["ring"] + S["e"]] * R[int(r[1])]
-            S["e"] += 1
-            return 2
+            n = int(r[1])
+            for i in range(n):
+                wq = int(r[2 + i // 2])
+                ysrc = (wq >> 16) & 0xFFFF if i & 1 else wq & 0xFFFF
+                S["acc"] = S["acc"] - R[S["ring"] + S["e"]] * R[ysrc]
+                S["e"] += 1
+            return 2 + (n + 1) // 2
         if t == REC_STEP:
             ring, ne = int(r[1]) & 0xFFFF, int(r[1]) >> 16
             S.update(ring=ring, ne=ne, brow=int(r[4]), e=0)
