@@ -122,22 +122,22 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
         double ire = 0.0, iim = 0.0;
         for (int q = q0; q < q1; ++q) {
             const int k = __ldg(v.yi + q);
-            const double vmk = v.vm[k * bp + t];
-            acc_current(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vmk * v.c[k * bp + t],
-                        vmk * v.s[k * bp + t], ire, iim);
+            const double vmk = __ldg(v.vm + k * bp + t);
+            acc_current(__ldg(v.yre + size_t(q) * v.y_ld + yt), __ldg(v.yim + size_t(q) * v.y_ld + yt), vmk * __ldg(v.c + k * bp + t),
+                        vmk * __ldg(v.s + k * bp + t), ire, iim);
         }
-        const double vmr = v.vm[r * bp + t];
-        const double vre = vmr * v.c[r * bp + t], vim = vmr * v.s[r * bp + t];
+        const double vmr = __ldg(v.vm + r * bp + t);
+        const double vre = vmr * __ldg(v.c + r * bp + t), vim = vmr * __ldg(v.s + r * bp + t);
         double P, Q;
         injection(vre, vim, ire, iim, P, Q);
         if (NPM) {
             const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
-            const double fp = P - v.p0[size_t(r) * v.s_ld + ts];
+            const double fp = P - __ldg(v.p0 + size_t(r) * v.s_ld + ts);
             a_t[size_t(__ldg(v.fslot_p + r)) * kTile] = fp;  // F beside its A column
             nrm = fmax(nrm, nan_as_inf_abs(fp));
             const int fq_slot = __ldg(v.fslot_q + r);
             if (fq_slot >= 0) {
-                const double fq = Q - v.q0[size_t(r) * v.s_ld + ts];
+                const double fq = Q - __ldg(v.q0 + size_t(r) * v.s_ld + ts);
                 a_t[size_t(fq_slot) * kTile] = fq;
                 nrm = fmax(nrm, nan_as_inf_abs(fq));
             }
@@ -145,9 +145,9 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
         if (JMODE != kJacNone && act) {
             for (int q = q0; q < q1; ++q) {
                 const int k = __ldg(v.yi + q);
-                const double ck = v.c[k * bp + t], sk = v.s[k * bp + t], vmk = v.vm[k * bp + t];
+                const double ck = __ldg(v.c + k * bp + t), sk = __ldg(v.s + k * bp + t), vmk = __ldg(v.vm + k * bp + t);
                 double zre, zim, j[4];
-                jac_z(v.yre[size_t(q) * v.y_ld + yt], v.yim[size_t(q) * v.y_ld + yt], vre, vim, ck, sk, zre, zim);
+                jac_z(__ldg(v.yre + size_t(q) * v.y_ld + yt), __ldg(v.yim + size_t(q) * v.y_ld + yt), vre, vim, ck, sk, zre, zim);
                 jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
                 const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
                 if (l.x >= 0) a_t[size_t(l.x) * kTile] = j[0];
