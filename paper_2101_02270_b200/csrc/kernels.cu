@@ -425,11 +425,13 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             // supernode pair k, k+1: x[kpos2] -= m1 L(k+1,k) gives m2; then every
             // other row gets k's update, then k+1's (the oracle's order per element)
             const int op = (h >> 4) - 1;
-            const int w1 = r[1], w2 = r[2], w3 = r[3], w4 = r[4], fs2 = r[5];
+            const int w1 = r[1], w2 = r[2], w3 = r[3], w4 = r[4], w5 = r[5];
+            const int fs2 = w5 & 0xffff, op2 = int(unsigned(w5) >> 16) - 1;
             const int nrows = w2 & 0xffff;
             const int n4 = (nrows + 3) & ~3;
             h = r[6 + (n4 >> 1)];
             if (op >= 0) prog_wait(P, op);
+            if (op2 >= 0) prog_wait(P, op2);
             const unsigned s1 = R0 + (unsigned(w2) >> 16) * RB, s2 = R0 + unsigned(w3 & 0xffff) * RB;
             const int fs1 = int(unsigned(w3) >> 16);
             double fl1 = 0.0, fy1 = 0.0, fl2 = 0.0, fy2 = 0.0;

@@ -338,10 +338,13 @@ struct Emitter {
 
 // Two consecutive forward dependencies k, k+1 of one step form a supernode
 // pair when L(:,k) is row k+1 followed by exactly the rows of L(:,k+1) (so the
-// destinations of k are kpos(k+1) then those of k+1) and the second needs no
-// wait of its own.  Every x element still sees k's update before k+1's.
-bool pairable(const Walk& w, const WDep& e, const WDep& f) {
-    if (e.nrows <= 0 || f.nrows < 0 || e.nrows != f.nrows + 1 || f.op >= 0) return false;
+// destinations of k are kpos(k+1) then those of k+1).  Every x element still
+// sees k's update before k+1's.
+bool pairable(const Walk& w, const WDep& e, const WDep& f, int64_t ev_e, int32_t op_base) {
+    if (e.nrows <= 0 || f.nrows < 0 || e.nrows != f.nrows + 1) return false;
+    // a second wait is hoisted to the pair's start: its op must already be issued
+    // there (issue event before e's) and its number must fit the record
+    if (f.op >= 0 && (w.op[f.op].after >= ev_e || op_base + f.op + 1 >= 65536)) return false;
     if ((f.kpos_fs & 0xffff) == 0xffff || f.nrows == 0) return false;
     if (int32_t(w.dst[e.u0]) != (f.kpos_fs & 0xffff)) return false;
     for (int32_t r = 0; r < f.nrows; ++r)
@@ -395,7 +398,7 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
             for (int32_t d = 0; d < s.ndep; ++d) {
                 const WDep& e = w.dep[s.dep0 + d];
                 if (e.src >= 65536 || e.nrows >= 65536) throw Error(3, "walk dependency too large to encode");
-                if (d + 1 < s.ndep && pairable(w, e, w.dep[s.dep0 + d + 1])) {
+                if (d + 1 < s.ndep && pairable(w, e, w.dep[s.dep0 + d + 1], ev, op_base)) {
                     // supernode pair: dep k's rows are row k+1 (x position kpos2) then
                     // exactly dep k+1's rows; one pass applies both in order
                     const WDep& f = w.dep[s.dep0 + d + 1];
@@ -403,7 +406,8 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
                     const int32_t kpos2 = f.kpos_fs & 0xffff, fs2 = int32_t(unsigned(f.kpos_fs) >> 16);
                     std::vector<int32_t> rec{kRecDep2 | ((opn(e.op) + 1) << 4), kpos1 | (kpos2 << 16),
                                              f.nrows | (std::max(e.src, 0) << 16), std::max(f.src, 0) | (fs1 << 16),
-                                             (std::max(e.ysrc, 0) & 0xffff) | (std::max(f.ysrc, 0) << 16), fs2};
+                                             (std::max(e.ysrc, 0) & 0xffff) | (std::max(f.ysrc, 0) << 16),
+                                             fs2 | ((opn(f.op) + 1) << 16)};
                     const int32_t n4 = (f.nrows + 3) & ~3;
                     auto dst = [&](int32_t r) { return r < f.nrows ? int32_t(w.dst[f.u0 + r]) : len; };
                     for (int32_t r = 0; r < n4; r += 2) rec.push_back(dst(r) | (dst(r + 1) << 16));

@@ -98,7 +98,7 @@ enum : int32_t {
     kRecSync = 7,
     // fwd: two dependencies k, k+1 of one supernode (L(:,k) = {k+1} u L(:,k+1)),
     // applied in one pass over x: 8 | (op + 1) << 4, kpos1 | kpos2 << 16,
-    // nrows2 | src1 << 16, src2 | fspos1 << 16, ysrc1 | ysrc2 << 16, fspos2,
+    // nrows2 | src1 << 16, src2 | fspos1 << 16, ysrc1 | ysrc2 << 16, fspos2 | (op2 + 1) << 16,
     // dst u16 pairs of L(:,k+1) (padded to 4)
     kRecDep2 = 8,
     // bwd: n consecutive dependencies, only the first may wait:

@@ -186,9 +186,12 @@ def replay_forward(w, A_tape, nrows, fs=True):
             return 4 + ((nrows + 3) & ~3) // 2
         if t == REC_DEP2:  # supernode pair k, k+1 in one pass, k's update first per element
             op = (h >> 4) - 1
-            w1, w2, w3, w4, fs2 = (int(v) for v in r[1:6])
+            w1, w2, w3, w4, w5 = (int(v) for v in r[1:6])
+            fs2, op2 = w5 & 0xFFFF, (w5 >> 16) - 1
             if op >= 0:
                 M.wait(op)
+            if op2 >= 0:
+                M.wait(op2)
             x = S["x"]
             kpos1, kpos2, nrows, s1 = w1 & 0xFFFF, w1 >> 16, w2 & 0xFFFF, w2 >> 16
             s2, fs1, y1, y2 = w3 & 0xFFFF, w3 >> 16, w4 & 0xFFFF, w4 >> 16
