@@ -59,6 +59,7 @@ extern "C" {
 #define GBNR_CONVERGED 0
 #define GBNR_DIVERGED 1
 #define GBNR_SINGULAR 2
+#define GBNR_FALLBACK_CONVERGED 3 /* converged after the second-chance factorization */
 
 typedef struct gbnr_plan gbnr_plan;
 
@@ -79,6 +80,10 @@ typedef struct gbnr_options {
                               check (a wrong guess adds a Jacobian-only launch);
                               1 = always inside the sweep; 2 = always after the check
                               (the reference's order).  Results are identical.        */
+    int32_t second_chance; /* 1 (default) = a task whose frozen pivot collapses is
+                              re-planned alone with fresh pivoting at its current
+                              voltages and continues; status 3 on
+                              convergence.  0 = it stays singular.                    */
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);

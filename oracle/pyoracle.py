@@ -37,7 +37,9 @@ def _f64(a):
 
 
 class OracleError(RuntimeError):
-    pass
+    def __init__(self, msg, code=0):
+        super().__init__(msg)
+        self.code = code
 
 
 class Oracle:
@@ -68,7 +70,7 @@ class Oracle:
 
     def _check(self, rc):
         if rc != 0:
-            raise OracleError(f"oracle error {rc}: {self.lib.orc_last_error().decode()}")
+            raise OracleError(f"oracle error {rc}: {self.lib.orc_last_error().decode()}", rc)
 
     def sincos(self, x):
         s, c = C.c_double(), C.c_double()
@@ -123,6 +125,7 @@ class OraclePlan:
         self.n_bus = n_bus
         self.h = C.c_void_p()
         self._keep = (_i32(indptr), _i32(indices), _f64(yre), _f64(yim), _i32(pv), _i32(pq))
+        self.ref, self.pivot_tol = int(ref), float(pivot_tol)
         orc._check(orc.lib.orc_plan_create(
             n_bus, self._keep[0], self._keep[1], self._keep[2], self._keep[3], int(ref),
             self._keep[4], len(pv), self._keep[5], len(pq), _f64(vm0), _f64(va0),
@@ -148,7 +151,7 @@ class OraclePlan:
         return dict(row_fwd=rf, col_fwd=cf, col_ptr=cp, row_ix=ri, level=lev)
 
     def solve(self, p0, q0, vm0, va0, n_tasks=None, y=None, tol=1e-8, max_iter=10,
-              singular_tol=1e-14, n_threads=None):
+              singular_tol=1e-14, n_threads=None, second_chance=True):
         p0 = _f64(p0); q0 = _f64(q0); vm0 = _f64(vm0); va0 = _f64(va0)
         if n_tasks is None:
             n_tasks = max(p0.shape[1] if p0.ndim == 2 else 1, vm0.shape[1] if vm0.ndim == 2 else 1)
@@ -166,7 +169,44 @@ class OraclePlan:
         nt = n_threads or os.cpu_count() or 1
         self.o._check(self.o.lib.orc_solve(self.h, n_tasks, yre, yim, ny, p0, q0, ns, vm0, va0, nv,
                                            tol, max_iter, singular_tol, vm, va, it, cv, st, mm, nt))
+        if second_chance:
+            self._second_chance(n_tasks, yre, yim, ny, p0, q0, ns, tol, max_iter, singular_tol,
+                                vm, va, it, cv, st, mm)
         return dict(vm=vm, va=va, iterations=it, converged=cv, status=st, max_mismatch=mm)
+
+    def _second_chance(self, n_tasks, yre, yim, ny, p0, q0, ns, tol, max_iter, singular_tol,
+                       vm, va, it, cv, st, mm):
+        """second_chance_refactorize (open question :436): a task
+        whose frozen pivot collapsed (status singular after `it` linear solves) is
+        re-planned alone -- a fresh threshold-pivoting factorization at its current
+        voltages, kept for the rest of its Newton loop -- and continues with the
+        remaining budget max_iter - (it - 1).  Converged -> status 3
+        (fallback_converged); otherwise the re-run's status.  A fresh
+        factorization that is itself singular leaves the task singular."""
+        ip, ix, _, _, pv, pq = self._keep
+        for t in np.nonzero(st == 2)[0]:
+            budget = max_iter - (int(it[t]) - 1)
+            if budget < 1:
+                continue
+            yr = yre[:, t] if ny > 1 else (yre[:, 0] if yre.ndim == 2 else yre)
+            yi = yim[:, t] if ny > 1 else (yim[:, 0] if yim.ndim == 2 else yim)
+            pp = p0[:, t] if ns > 1 else (p0[:, 0] if p0.ndim == 2 else p0)
+            qq = q0[:, t] if ns > 1 else (q0[:, 0] if q0.ndim == 2 else q0)
+            v_m, v_a = vm[:, t].copy(), va[:, t].copy()
+            try:
+                sub = OraclePlan(self.o, self.n_bus, ip, ix, yr, yi, self.ref, pv, pq, v_m, v_a,
+                                 self.pivot_tol)
+            except OracleError as e:
+                if e.code != 4:  # only a numerically singular fresh factorization leaves it failed
+                    raise
+                continue
+            r = sub.solve(pp[:, None], qq[:, None], v_m[:, None], v_a[:, None], n_tasks=1, tol=tol,
+                          max_iter=budget, singular_tol=singular_tol, n_threads=1, second_chance=False)
+            s2 = int(r["status"][0])
+            st[t] = 3 if s2 == 0 else s2
+            cv[t] = 1 if s2 == 0 else 0
+            it[t] = int(it[t]) - 1 + int(r["iterations"][0])
+            vm[:, t], va[:, t], mm[t] = r["vm"][:, 0], r["va"][:, 0], r["max_mismatch"][0]
 
     def refactor(self, vm, va, singular_tol=1e-14, n_threads=None):
         vm = _f64(vm); va = _f64(va)

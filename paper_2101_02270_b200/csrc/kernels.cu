@@ -212,15 +212,15 @@ __global__ void bump_kernel(DevView v) {
 
 // Final per-status task counts -> mapped host memory.
 __global__ void status_count_kernel(DevView v) {
-    __shared__ int c[3];
-    if (threadIdx.x < 3) c[threadIdx.x] = 0;
+    __shared__ int c[4];
+    if (threadIdx.x < 4) c[threadIdx.x] = 0;
     __syncthreads();
     for (int t = threadIdx.x; t < v.n_tasks; t += blockDim.x) {
         const int s = v.status[t];
-        atomicAdd(&c[(s >= 0 && s <= 2) ? s : 2], 1);
+        atomicAdd(&c[(s >= 0 && s <= 3) ? s : 2], 1);
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 4) {
         volatile int32_t* h = v.h_counts;
         h[64 + threadIdx.x] = c[threadIdx.x];
     }

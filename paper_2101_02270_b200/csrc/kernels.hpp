@@ -47,7 +47,7 @@ struct DevView {
     int32_t *tile_active, *active_count;
     int32_t* it_dev;                // Newton iteration counter on the device
     int32_t* h_counts;              // mapped host memory: [0,32) active tasks, [32,64) active
-                                    // tiles per iteration, [64,67) tasks per final status,
+                                    // tiles per iteration, [64,68) tasks per final status,
                                     // [96,128) active tasks whose Jacobian was not written
     double tol, singular_tol;
     int32_t max_iter;

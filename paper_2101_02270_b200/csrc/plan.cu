@@ -12,6 +12,7 @@
 #include <cstring>
 #include <functional>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -66,6 +67,7 @@ enum Phase { kNpm = 0, kJac, kLu, kFsbs, kVupd, kPhases };
 
 struct gbnr_plan {
     gbnr::Symbolic sym;
+    std::vector<int32_t> in_pv, in_pq;  // creation inputs kept for second-chance re-plans
     gbnr::LuLayout lay;
     gbnr::WalkSet wf, wl, wb;        // forward LU+FS, LU-only, backward walks
     gbnr::WalkView vf{}, vl{}, vb{};
@@ -433,7 +435,12 @@ struct gbnr_plan {
         }
         timing[14] = tiles;
         timing[15] = tasks;
-        for (int x = 0; x < 3; ++x) timing[16 + x] = h_count[64 + x];
+        if (opt.second_chance && h_count[66] > 0) second_chance();
+        // converged (incl. second-chance), diverged, singular; [20] second-chance subset
+        timing[16] = h_count[64] + h_count[67];
+        timing[17] = h_count[65];
+        timing[18] = h_count[66];
+        timing[20] = h_count[67];
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
         resolve_profile();
@@ -442,6 +449,68 @@ struct gbnr_plan {
         timing[13] = v.n_tasks;
         timing[19] = double(launches_per_iteration()) * it_done + 4 + jac_fix;  // kernels launched
         solved = true;
+    }
+
+    // second_chance_refactorize (open question :436): a task
+    // whose frozen pivot collapsed (status singular after `it` linear solves) is
+    // re-planned alone -- a fresh threshold-pivoting factorization at its current
+    // voltages, kept for the rest of its Newton loop -- and continues on the GPU
+    // with the remaining budget max_iter - (it - 1).  Its results replace the
+    // task's column of the batch state; status GBNR_FALLBACK_CONVERGED if it
+    // converges, else the re-run's status.  A fresh factorization that is itself
+    // singular leaves the task singular.  Host orchestration only: the re-run uses
+    // the same kernels (oracle/pyoracle.py OraclePlan._second_chance is the checker).
+    void second_chance() {
+        const int32_t nt = v.n_tasks, n = sym.n, nY = sym.nnzY;
+        std::vector<int32_t> st(nt), it(nt);
+        CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(it.data(), v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        gbnr_options o = opt;
+        o.second_chance = 0;  // one chance
+        o.profile = 0;
+        std::vector<double> vm(n), va(n), yr(nY), yi(nY), pp(n), qq(n);
+        auto column = [&](double* dst, const double* src, size_t pitch, int32_t rows) {
+            CK(cudaMemcpy2DAsync(dst, 8, src, pitch * 8, 8, size_t(rows), cudaMemcpyDeviceToHost, stream));
+        };
+        for (int32_t t = 0; t < nt; ++t) {
+            if (st[t] != GBNR_SINGULAR) continue;
+            o.max_iter = opt.max_iter - (it[t] - 1);
+            if (o.max_iter < 1) continue;
+            const size_t bp = size_t(v.bpad);
+            column(vm.data(), v.vm + t, bp, n);
+            column(va.data(), v.va + t, bp, n);
+            column(yr.data(), v.yre + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
+            column(yi.data(), v.yim + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
+            column(pp.data(), v.p0 + size_t(t) * v.s_inc, size_t(v.s_ld), n);
+            column(qq.data(), v.q0 + size_t(t) * v.s_inc, size_t(v.s_ld), n);
+            CK(cudaStreamSynchronize(stream));
+            gbnr_plan* sub = nullptr;
+            const int rc = gbnr_plan_create(n, sym.yp.data(), sym.yi.data(), yr.data(), yi.data(), sym.ref,
+                                            in_pv.data(), int32_t(in_pv.size()), in_pq.data(),
+                                            int32_t(in_pq.size()), vm.data(), va.data(), &o, &sub);
+            if (rc == GBNR_ESINGULAR) continue;  // still singular: the task stays failed
+            if (rc != GBNR_OK) throw Error(rc, std::string("second chance: ") + gbnr_last_error());
+            std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(sub, gbnr_plan_destroy);
+            sub->stage_ybus(nullptr, nullptr, 1, 1);
+            sub->stage(1, pp.data(), qq.data(), 1, vm.data(), va.data(), 1);
+            sub->run();
+            int32_t s2 = 0, i2 = 0;
+            CK(cudaMemcpy(&s2, sub->v.status, 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&i2, sub->v.iters, 4, cudaMemcpyDeviceToHost));
+            const int32_t s_new = s2 == GBNR_CONVERGED ? GBNR_FALLBACK_CONVERGED : s2;
+            const int32_t i_new = it[t] - 1 + i2;
+            CK(cudaSetDevice(opt.device));
+            CK(cudaMemcpyAsync(v.status + t, &s_new, 4, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(v.iters + t, &i_new, 4, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(v.maxmis + t, sub->v.maxmis, 8, cudaMemcpyDeviceToDevice, stream));
+            const size_t sp = size_t(sub->v.bpad) * 8;
+            for (auto [dst, src] : {std::pair{v.vm, sub->v.vm}, {v.va, sub->v.va}, {v.c, sub->v.c}, {v.s, sub->v.s}})
+                CK(cudaMemcpy2DAsync(dst + t, bp * 8, src, sp, 8, size_t(n), cudaMemcpyDeviceToDevice, stream));
+            CK(cudaStreamSynchronize(stream));  // before the sub-plan's buffers go
+        }
+        gbnr::launch_status_count(v, stream);
+        CK(cudaStreamSynchronize(stream));
     }
 
     void ensure_pipe(int32_t n_tiles) {
@@ -564,7 +633,7 @@ struct gbnr_plan {
         CK(cudaStreamSynchronize(stream));
         if (status) std::memcpy(status, st.data(), size_t(nt) * 4);
         if (conv)
-            for (int32_t t = 0; t < nt; ++t) conv[t] = st[t] == GBNR_CONVERGED;
+            for (int32_t t = 0; t < nt; ++t) conv[t] = st[t] == GBNR_CONVERGED || st[t] == GBNR_FALLBACK_CONVERGED;
     }
 
     // calc_branch_flows on the voltages of the last solve (device-resident)
@@ -645,8 +714,10 @@ void gbnr_default_options(gbnr_options* o) {
     o->profile = 0;
     o->stage_rows = 0;
     o->prefetch = 8;
-    o->headroom = 2;
+    o->headroom = 1;
     o->walkers = 8;
+    o->jacobian = 0;
+    o->second_chance = 1;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -737,6 +808,8 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (p->opt.jacobian < 0 || p->opt.jacobian > 2) throw Error(GBNR_ECONFIG, "jacobian policy must be 0, 1 or 2");
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
+        p->in_pv.assign(pv, pv + n_pv);
+        p->in_pq.assign(pq, pq + n_pq);
         p->lay = gbnr::build_lu_layout(p->sym);
         gbnr::WalkConfig wc;
         if (p->opt.ring_rows) wc.ring_rows = p->opt.ring_rows;

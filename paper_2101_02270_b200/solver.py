@@ -49,7 +49,7 @@ class Options(C.Structure):
                 ("singular_tol", C.c_double), ("device", C.c_int32), ("ring_rows", C.c_int32),
                 ("profile", C.c_int32), ("stage_rows", C.c_int32),
                 ("prefetch", C.c_int32), ("headroom", C.c_int32), ("walkers", C.c_int32),
-                ("jacobian", C.c_int32)]
+                ("jacobian", C.c_int32), ("second_chance", C.c_int32)]
 
 
 _lib = None
@@ -340,6 +340,7 @@ class NrPlan:
         d["converged"] = int(out[16])
         d["diverged"] = int(out[17])
         d["singular"] = int(out[18])
+        d["fallback_converged"] = int(out[20])  # second-chance successes (included in converged)
         d["kernels"] = int(out[19])
         return d
 

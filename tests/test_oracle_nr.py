@@ -192,3 +192,40 @@ def test_branch_flows_oracle_kats():
     np.testing.assert_allclose(total + shunt, Sbus, atol=1e-10)
     sf2, st2 = po.Oracle().branch_flows(gc, adm, r["vm"], r["va"], outage=np.array([3], np.int32))
     assert sf2[3, 0] == 0 and st2[3, 0] == 0 and sf2[2, 0] == sf[2, 0]
+
+
+def _two_bus_instability(T=8, special=3, angle=np.pi / 2):
+    """SPEC.md:342 example: a task whose frozen pivot collapses but is well
+    conditioned under fresh pivoting.  Slack + one PQ bus on a lossless line
+    (x = 0.1): dP1/dtheta1 = V1 V0 B10 cos(theta1), so a task starting at
+    theta1 = 90 degrees has a zero frozen (diagonal) pivot while J stays
+    nonsingular ([[0, a], [b, c]])."""
+    ip = np.array([0, 2, 4], np.int32)
+    ix = np.array([0, 1, 0, 1], np.int32)
+    yr, yi = np.zeros(4), np.array([-10.0, 10.0, 10.0, -10.0])
+    vm0, va0 = np.ones(2), np.zeros(2)
+    p0 = np.tile(np.array([0.0, -0.5])[:, None], (1, T))
+    q0 = np.tile(np.array([0.0, -0.2])[:, None], (1, T))
+    vm, va = np.ones((2, T)), np.zeros((2, T))
+    va[1, special] = angle
+    pq = np.array([1], np.int32)
+    return (ip, ix, yr, yi, 0, np.array([], np.int32), pq, vm0, va0), p0, q0, vm, va
+
+
+def test_second_chance_fallback_oracle():
+    """second_chance_refactorize: the flagged task is re-planned
+    with fresh pivoting and converges as fallback_converged (status 3); batch peers
+    are unaffected (solo-run comparison, SPEC.md:502 criterion 7); without the
+    second chance it stays singular."""
+    args, p0, q0, vm, va = _two_bus_instability()
+    op = po.Oracle().plan(2, *args)
+    off = op.solve(p0, q0, vm, va, n_tasks=8, second_chance=False)
+    assert off["status"][3] == 2 and off["iterations"][3] == 1
+    r = op.solve(p0, q0, vm, va, n_tasks=8)
+    assert r["status"][3] == 3 and r["converged"][3] == 1 and r["max_mismatch"][3] < 1e-8
+    assert r["iterations"][3] > 1
+    peers = [t for t in range(8) if t != 3]
+    assert (r["status"][peers] == 0).all()
+    solo = op.solve(p0[:, :1], q0[:, :1], vm[:, :1], va[:, :1], n_tasks=1)
+    np.testing.assert_array_equal(r["vm"][:, peers], np.repeat(solo["vm"], 7, axis=1))
+    np.testing.assert_array_equal(r["iterations"][peers], solo["iterations"][0])
