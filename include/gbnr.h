@@ -80,10 +80,13 @@ typedef struct gbnr_options {
                               check (a wrong guess adds a Jacobian-only launch);
                               1 = always inside the sweep; 2 = always after the check
                               (the reference's order).  Results are identical.        */
-    int32_t second_chance; /* 1 (default) = a task whose frozen pivot collapses is
-                              re-planned alone with fresh pivoting at its current
-                              voltages and continues; status 3 on
-                              convergence.  0 = it stays singular.                    */
+    int32_t second_chance; /* up to this many tasks per solve (default 16) whose
+                              frozen pivot collapsed are re-planned alone with fresh
+                              pivoting at their current voltages and continue
+                              (SPEC.md:337-345); status 3 on convergence.  0 = off.
+                              With a shared Ybus, >5% of the tasks failing at their
+                              first solve restarts the batch once from the worst
+                              task's pivots (SPEC.md design decisions).               */
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);

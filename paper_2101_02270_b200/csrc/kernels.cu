@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
     v.norm_bits[t] = 0ull;
     bool act = v.tile_active[tile] != 0 && v.active[t] != 0;
     if (act) {
+        if (it == 0) v.mis0[t] = m;
         v.mis_prev[t] = v.maxmis[t];
         v.maxmis[t] = m;
         if (m < v.tol) {

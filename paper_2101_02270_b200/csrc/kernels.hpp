@@ -42,6 +42,7 @@ struct DevView {
     uint8_t *active, *flag;
     double* maxmis;                 // max-norm at the last check (inf before the first)
     double* mis_prev;               // max-norm one check earlier (inf before)
+    double* mis0;                   // max-norm at V0 (representative re-derivation)
     uint8_t* jskip;                 // the last NPM skipped this task's speculative Jacobian
     unsigned long long* norm_bits;  // running max-norm (IEEE bits) of the current NPM
     int32_t *tile_active, *active_count;

@@ -303,6 +303,7 @@ struct gbnr_plan {
         v.flag = static_cast<uint8_t*>(alloc(bpad));
         v.maxmis = static_cast<double*>(alloc(bpad * sizeof(double)));
         v.mis_prev = static_cast<double*>(alloc(bpad * sizeof(double)));
+        v.mis0 = static_cast<double*>(alloc(bpad * sizeof(double)));
         v.jskip = static_cast<uint8_t*>(alloc(bpad));
         v.norm_bits = static_cast<unsigned long long*>(alloc(bpad * sizeof(unsigned long long)));
         v.tile_active = static_cast<int32_t*>(alloc(size_t(n_tiles) * sizeof(int32_t)));
@@ -435,12 +436,16 @@ struct gbnr_plan {
         }
         timing[14] = tiles;
         timing[15] = tasks;
-        if (opt.second_chance && h_count[66] > 0) second_chance();
-        // converged (incl. second-chance), diverged, singular; [20] second-chance subset
-        timing[16] = h_count[64] + h_count[67];
-        timing[17] = h_count[65];
-        timing[18] = h_count[66];
-        timing[20] = h_count[67];
+        if (opt.second_chance && h_count[66] > 0) {
+            // representative re-derivation (SPEC.md DESIGN DECISIONS): the frozen
+            // pivot order failed for more than 5% of the tasks at their first
+            // solve -> gbnr_solve restarts the batch once from the worst task
+            if (allow_rederive && flagged_at_first_solve() * 20 > v.n_tasks)
+                rederive_pending = true;
+            else
+                second_chance();
+        }
+        count_statuses();
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
         resolve_profile();
@@ -460,6 +465,84 @@ struct gbnr_plan {
     // converges, else the re-run's status.  A fresh factorization that is itself
     // singular leaves the task singular.  Host orchestration only: the re-run uses
     // the same kernels (oracle/pyoracle.py OraclePlan._second_chance is the checker).
+    bool allow_rederive = false, rederive_pending = false;
+
+    // converged (incl. second chance), diverged, singular; [20] the second-chance subset
+    void count_statuses() {
+        timing[16] = h_count[64] + h_count[67];
+        timing[17] = h_count[65];
+        timing[18] = h_count[66];
+        timing[20] = h_count[67];
+    }
+
+    int32_t flagged_at_first_solve() {
+        const int32_t nt = v.n_tasks;
+        std::vector<int32_t> st(nt), it(nt);
+        CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(it.data(), v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        int32_t c = 0;
+        for (int32_t t = 0; t < nt; ++t) c += st[t] == GBNR_SINGULAR && it[t] == 1;
+        return c;
+    }
+
+    // The restart of gbnr_solve: a plan whose pivots come from the task with the
+    // worst mismatch at V0 (its V0 and Ybus values) solves the whole batch again,
+    // with second chance; results and device voltages come from it.
+    void rederive_and_solve(int32_t n_tasks, const double* y_re, const double* y_im, int32_t n_ysets,
+                            const double* p0, const double* q0, int32_t n_ssets, const double* vm0,
+                            const double* va0, int32_t n_vsets, double* vm_out, double* va_out,
+                            int32_t* it_out, uint8_t* conv_out, int32_t* st_out, double* mm_out) {
+        const int32_t nt = v.n_tasks, n = sym.n, nY = sym.nnzY;
+        std::vector<double> m0(nt);
+        CK(cudaMemcpy(m0.data(), v.mis0, size_t(nt) * 8, cudaMemcpyDeviceToHost));
+        int32_t w = 0;
+        for (int32_t t = 1; t < nt; ++t)
+            if (m0[t] > m0[w]) w = t;  // first of the largest
+        std::vector<double> vm(n), va(n), yr(nY), yi(nY);
+        const int32_t vw = n_vsets == 1 ? 0 : w;
+        for (int32_t b = 0; b < n; ++b) {
+            vm[b] = vm0[size_t(b) * n_vsets + vw];
+            va[b] = va0[size_t(b) * n_vsets + vw];
+        }
+        if (y_re && y_im) {
+            const int32_t yw = n_ysets == 1 ? 0 : w;
+            for (int32_t q = 0; q < nY; ++q) {
+                yr[q] = y_re[size_t(q) * n_ysets + yw];
+                yi[q] = y_im[size_t(q) * n_ysets + yw];
+            }
+        } else {
+            CK(cudaMemcpy(yr.data(), y_shared_re, size_t(nY) * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(yi.data(), y_shared_im, size_t(nY) * 8, cudaMemcpyDeviceToHost));
+        }
+        gbnr_plan* alt = nullptr;
+        const int rc = gbnr_plan_create(n, sym.yp.data(), sym.yi.data(), yr.data(), yi.data(), sym.ref,
+                                        in_pv.data(), int32_t(in_pv.size()), in_pq.data(), int32_t(in_pq.size()),
+                                        vm.data(), va.data(), &opt, &alt);
+        if (rc == GBNR_ESINGULAR) {  // no better representative: per-task second chance
+            second_chance();
+            count_statuses();
+            fetch(vm_out, va_out, it_out, conv_out, st_out, mm_out);
+            return;
+        }
+        if (rc != GBNR_OK) throw Error(rc, std::string("re-derivation: ") + gbnr_last_error());
+        std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(alt, gbnr_plan_destroy);
+        alt->stage_ybus(y_re, y_im, n_ysets, n_tasks);
+        alt->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
+        alt->run();
+        alt->fetch(vm_out, va_out, it_out, conv_out, st_out, mm_out);
+        std::memcpy(timing, alt->timing, sizeof timing);
+        timing[21] = 1;  // restarted from a re-derived representative
+        // device state for gbnr_branch_flows: the restarted solve's voltages
+        CK(cudaSetDevice(opt.device));
+        const size_t nb = size_t(n) * size_t(v.bpad) * 8;
+        for (auto [dst, src] : {std::pair{v.vm, alt->v.vm}, {v.va, alt->v.va}, {v.c, alt->v.c}, {v.s, alt->v.s}})
+            CK(cudaMemcpy(dst, src, nb, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpy(v.status, alt->v.status, size_t(nt) * 4, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpy(v.iters, alt->v.iters, size_t(nt) * 4, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpy(v.maxmis, alt->v.maxmis, size_t(nt) * 8, cudaMemcpyDeviceToDevice));
+    }
+
     void second_chance() {
         const int32_t nt = v.n_tasks, n = sym.n, nY = sym.nnzY;
         std::vector<int32_t> st(nt), it(nt);
@@ -473,10 +556,12 @@ struct gbnr_plan {
         auto column = [&](double* dst, const double* src, size_t pitch, int32_t rows) {
             CK(cudaMemcpy2DAsync(dst, 8, src, pitch * 8, 8, size_t(rows), cudaMemcpyDeviceToHost, stream));
         };
-        for (int32_t t = 0; t < nt; ++t) {
+        int32_t budget = opt.second_chance;  // re-plans per solve (each is a plan build)
+        for (int32_t t = 0; t < nt && budget > 0; ++t) {
             if (st[t] != GBNR_SINGULAR) continue;
             o.max_iter = opt.max_iter - (it[t] - 1);
             if (o.max_iter < 1) continue;
+            --budget;
             const size_t bp = size_t(v.bpad);
             column(vm.data(), v.vm + t, bp, n);
             column(va.data(), v.va + t, bp, n);
@@ -717,7 +802,7 @@ void gbnr_default_options(gbnr_options* o) {
     o->headroom = 1;
     o->walkers = 8;
     o->jacobian = 0;
-    o->second_chance = 1;
+    o->second_chance = 16;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -806,6 +891,7 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             p->opt.walkers < 0 || p->opt.walkers > 8)
             throw Error(GBNR_ECONFIG, "negative walk parameter");
         if (p->opt.jacobian < 0 || p->opt.jacobian > 2) throw Error(GBNR_ECONFIG, "jacobian policy must be 0, 1 or 2");
+        if (p->opt.second_chance < 0) throw Error(GBNR_ECONFIG, "second_chance must be >= 0");
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
         p->in_pv.assign(pv, pv + n_pv);
@@ -908,7 +994,21 @@ int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* 
         CK(cudaSetDevice(p->opt.device));
         p->stage_ybus(y_re, y_im, n_ysets, n_tasks);
         p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
-        p->run();
+        p->allow_rederive = !y_re || n_ysets == 1;  // N-1 batches: islanded tasks dominate the flags
+        p->rederive_pending = false;
+        try {
+            p->run();
+        } catch (...) {
+            p->allow_rederive = false;
+            throw;
+        }
+        p->allow_rederive = false;
+        if (p->rederive_pending) {
+            p->rederive_pending = false;
+            p->rederive_and_solve(n_tasks, y_re, y_im, n_ysets, p0, q0, n_ssets, vm0, va0, n_vsets, vm_out,
+                                  va_out, iterations_out, converged_out, status_out, max_mismatch_out);
+            return;
+        }
         p->fetch(vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out);
     });
 }

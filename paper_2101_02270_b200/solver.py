@@ -341,6 +341,7 @@ class NrPlan:
         d["diverged"] = int(out[17])
         d["singular"] = int(out[18])
         d["fallback_converged"] = int(out[20])  # second-chance successes (included in converged)
+        d["rederived"] = int(out[21])  # batch restarted from a re-derived representative task
         d["kernels"] = int(out[19])
         return d
 

@@ -216,7 +216,7 @@ def test_second_chance_matches_oracle(second_chance):
     ip, ix, yr, yi, ref, pv, pq, vm0, va0 = args
     plan = S.NrPlan(2, ip, ix, yr, yi, ref, pv, pq, vm0, va0, device=0, second_chance=second_chance)
     r = plan.solve(p0, q0, vm, va, n_tasks=40)
-    o = po.Oracle().plan(2, *args).solve(p0, q0, vm, va, n_tasks=40, second_chance=bool(second_chance))
+    o = po.Oracle().plan(2, *args).solve(p0, q0, vm, va, n_tasks=40, second_chance=second_chance)
     _compare(r, o)
     assert r.status[3] == (3 if second_chance else 2)
     if second_chance:
@@ -225,3 +225,18 @@ def test_second_chance_matches_oracle(second_chance):
     assert (r.status[peers] == 0).all()
     solo = plan.solve(p0[:, :1], q0[:, :1], vm[:, :1], va[:, :1], n_tasks=1)
     np.testing.assert_array_equal(r.vm[:, peers], np.repeat(solo.vm, len(peers), axis=1))
+
+
+def test_representative_rederivation_matches_oracle():
+    """More than 5% of the tasks flagged at their first solve: gbnr_solve restarts
+    the batch once from the worst-V0-mismatch task's pivots (SPEC.md DESIGN
+    DECISIONS), exactly as the oracle does, then second chances what still fails."""
+    from test_oracle_nr import _two_bus_instability
+    args, p0, q0, vm, va = _two_bus_instability(T=8, special=3)
+    ip, ix, yr, yi, ref, pv, pq, vm0, va0 = args
+    plan = S.NrPlan(2, ip, ix, yr, yi, ref, pv, pq, vm0, va0, device=0)
+    r = plan.solve(p0, q0, vm, va, n_tasks=8)
+    o = po.Oracle().plan(2, *args).solve(p0, q0, vm, va, n_tasks=8)
+    _compare(r, o)
+    tm = plan.timing()
+    assert tm["rederived"] == 1 and r.status[3] == 0 and tm["fallback_converged"] == 7
