@@ -276,6 +276,9 @@ class Reference:
         L.ref_crs_to_ccs.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, _i32p, _i32p, _i32p]
         L.ref_scatter_lookup.argtypes = [C.c_int32, _i32p, _i32p, _i32p, _i32p, C.c_int32, _i32p,
                                          _i32p, _i32p, _i32p, _i32p]
+        L.ref_parse_scenario.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_int32), C.c_void_p,
+                                         C.c_void_p]
+        L.ref_parse_outages.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_int32), C.c_void_p]
 
     def err(self):
         return self.lib.ref_last_error().decode()
@@ -336,6 +339,27 @@ class RefCase:
         if self.r.lib.ref_ybus_outage(self.h, int(branch), yr, yi, C.byref(isl)) != 0:
             raise OracleError(self.r.err())
         return yr, yi, bool(isl.value)
+
+    def scenario(self, text: str):
+        """parse_scenario_csv (case_io.hpp:368-447) -> (p_mw, q_mvar) [n_bus][n_tasks];
+        raises OracleError with the reference's error code."""
+        nt = C.c_int32()
+        rc = self.r.lib.ref_parse_scenario(self.h, text.encode(), C.byref(nt), None, None)
+        if rc != 0:
+            raise OracleError(self.r.err(), rc)
+        p = np.zeros((self.n_bus, nt.value)); q = np.zeros((self.n_bus, nt.value))
+        self.r.lib.ref_parse_scenario(self.h, text.encode(), C.byref(nt), p.ctypes.data, q.ctypes.data)
+        return p, q
+
+    def outages(self, text: str):
+        """parse_outage_list (case_io.hpp:449-471) -> int32 branch indices."""
+        n = C.c_int32()
+        rc = self.r.lib.ref_parse_outages(self.h, text.encode(), C.byref(n), None)
+        if rc != 0:
+            raise OracleError(self.r.err(), rc)
+        out = np.zeros(n.value, np.int32)
+        self.r.lib.ref_parse_outages(self.h, text.encode(), C.byref(n), out.ctypes.data)
+        return out
 
     def loads(self):
         p = np.zeros(self.n_bus); q = np.zeros(self.n_bus)

@@ -151,6 +151,29 @@ int ref_ybus_outage(void* h, int32_t branch, double* yre, double* yim, int32_t* 
     });
 }
 
+// parse_scenario_csv (case_io.hpp:368-447): per-task bus loads [bus][n_tasks];
+// call with p_mw = nullptr first to get n_tasks.
+int ref_parse_scenario(void* h, const char* text, int32_t* n_tasks, double* p_mw, double* q_mvar) {
+    return guarded([&] {
+        const GridCase& gc = *static_cast<GridCase*>(h);
+        const ScenarioTable sc = parse_scenario_csv(text, gc);
+        *n_tasks = sc.n_tasks;
+        if (p_mw) std::memcpy(p_mw, sc.p_mw.data(), sc.p_mw.size() * sizeof(double));
+        if (q_mvar) std::memcpy(q_mvar, sc.q_mvar.data(), sc.q_mvar.size() * sizeof(double));
+    });
+}
+
+// parse_outage_list (case_io.hpp:449-471); call with out = nullptr for the count.
+int ref_parse_outages(void* h, const char* text, int32_t* n, int32_t* out) {
+    return guarded([&] {
+        const GridCase& gc = *static_cast<GridCase*>(h);
+        const std::vector<index_t> o = parse_outage_list(text, gc);
+        *n = static_cast<int32_t>(o.size());
+        if (out)
+            for (size_t i = 0; i < o.size(); ++i) out[i] = static_cast<int32_t>(o[i]);
+    });
+}
+
 // amd_order on a square CCS pattern; writes forward[old] = new.
 int ref_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int32_t* fwd) {
     return guarded([&] {

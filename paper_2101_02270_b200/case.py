@@ -333,6 +333,82 @@ def _finalize(gc: GridCase, br_ext, gen_ext) -> None:
         raise CaseError("disconnected island in base case", 2)
 
 
+# ---------------------------------------------------------------------------
+# Scenario and outage files (case_io.hpp:363-471)
+# ---------------------------------------------------------------------------
+
+def _internal_bus(gc: GridCase, bus_id: int) -> int:
+    """GridCase::internal_bus (grid.hpp:76-81): unknown id -> structural error."""
+    hit = np.nonzero(gc.bus_id == bus_id)[0]
+    if hit.size == 0:
+        raise CaseError(f"unknown bus id {bus_id}", 2)
+    return int(hit[0])
+
+
+def parse_scenario_csv(text: str, gc: GridCase):
+    """parse_scenario_csv (case_io.hpp:368-447).  Header ``bus:<id>:p,bus:<id>:q,...``,
+    one row per task; the named columns replace those bus loads (MW / MVAr), the
+    other buses keep the case loads.  Returns (p_mw, q_mvar) [n_bus][n_tasks];
+    malformed input raises CaseError (code 1 parse / 2 unknown bus) with the line."""
+    lines = text.split("\n")
+    if text == "" or not lines:
+        raise CaseError("empty scenario file")
+
+    def split(s):
+        return s.replace("\r", "").split(",")
+
+    cols = []
+    for h in split(lines[0]):
+        if len(h) < 7 or not h.startswith("bus:"):
+            raise CaseError(f"bad scenario column '{h}'", 1, 1)
+        second = h.find(":", 4)
+        if second < 0:
+            raise CaseError(f"bad scenario column '{h}'", 1, 1)
+        id_str, fld = h[4:second], h[second + 1:]
+        if fld not in ("p", "q"):
+            raise CaseError(f"scenario column must end in :p or :q, got '{h}'", 1, 1)
+        # std::from_chars(int): optional '-', decimal digits, whole token
+        body = id_str[1:] if id_str.startswith("-") else id_str
+        if not body.isdigit() or not body.isascii():
+            raise CaseError(f"bad bus id in column '{h}'", 1, 1)
+        cols.append((_internal_bus(gc, int(id_str)), fld == "p"))
+    rows = []
+    for ln, line in enumerate(lines[1:], start=2):
+        if line.strip(" \t\n\v\f\r") == "":
+            continue
+        cells = split(line)
+        if len(cells) != len(cols):
+            raise CaseError(f"scenario row has {len(cells)} cells, header has {len(cols)}", 1, ln)
+        rows.append([_number(c, ln) for c in cells])
+    if not rows:
+        raise CaseError("scenario file has no task rows")
+    T = len(rows)
+    p = np.repeat(gc.pd[:, None].astype(np.float64), T, axis=1)
+    q = np.repeat(gc.qd[:, None].astype(np.float64), T, axis=1)
+    for t, r in enumerate(rows):
+        for (bus, is_p), val in zip(cols, r):
+            (p if is_p else q)[bus, t] = val
+    return p, q
+
+
+def parse_outage_list(text: str, gc: GridCase) -> np.ndarray:
+    """parse_outage_list (case_io.hpp:449-471): one 0-based branch index per token,
+    '#' starts a comment; out-of-range or non-integral indices and an empty list
+    are parse errors.  Returns int32 branch indices in file order."""
+    out = []
+    for ln, line in enumerate(text.split("\n"), start=1):
+        line = line.split("#", 1)[0]
+        for tok in line.split():
+            v = _number(tok, ln)
+            idx = int(v) if math.isfinite(v) else -1
+            if idx < 0 or idx >= gc.n_branch or float(idx) != v:
+                raise CaseError(f"branch index out of range: {tok}", 1, ln)
+            out.append(idx)
+    if not out:
+        raise CaseError("outage list is empty")
+    return np.asarray(out, np.int32)
+
+
 def load_case(path: str) -> GridCase:
     with open(path, "r") as fh:
         return parse_matpower(fh.read())

@@ -240,3 +240,29 @@ def test_representative_rederivation_matches_oracle():
     _compare(r, o)
     tm = plan.timing()
     assert tm["rederived"] == 1 and r.status[3] == 0 and tm["fallback_converged"] == 7
+
+
+def test_runtime_modes_match_oracle():
+    """batch_runtime modes through paper_2101_02270_b200.runtime:
+    contingency over every case14 branch (islanded outages excluded by the
+    pre-check, status ISLANDED) and a 24-step time series from a scenario CSV,
+    each bit-identical to the oracle on the solved tasks."""
+    from paper_2101_02270_b200 import runtime
+    gc, plan, oplan, vm0, va0 = _setup("case14")
+    inp = runtime.job_inputs(gc, "contingency", outages=np.arange(gc.n_branch))
+    res = runtime.run(plan, gc, "contingency", outages=np.arange(gc.n_branch))
+    keep = ~inp.islanded
+    assert (res.status[~keep] == runtime.ISLANDED).all() and (~keep).sum() == 1
+    o = oplan.solve(inp.p0[:, keep], inp.q0[:, keep], vm0[:, None], va0[:, None],
+                    y=(np.ascontiguousarray(inp.y[0][:, keep]), np.ascontiguousarray(inp.y[1][:, keep])))
+    np.testing.assert_array_equal(res.status[keep], o["status"])
+    np.testing.assert_array_equal(res.iterations[keep], o["iterations"])
+    np.testing.assert_array_equal(res.vm[:, keep], o["vm"])
+    assert res.report["counts"]["islanded"] == 1
+    csv = "bus:4:p,bus:4:q,bus:9:p\n" + "\n".join(f"{40 + i},{-3 + 0.1 * i},{20 + i}" for i in range(24)) + "\n"
+    ts = runtime.run(plan, gc, "timeseries", scenario_csv=csv)
+    ti = runtime.job_inputs(gc, "timeseries", scenario_csv=csv)
+    o = oplan.solve(ti.p0, ti.q0, vm0[:, None], va0[:, None])
+    np.testing.assert_array_equal(ts.status, o["status"])
+    np.testing.assert_array_equal(ts.va, o["va"])
+    assert ts.report["counts"]["converged"] == 24

@@ -110,6 +110,50 @@ def sparse_kats(ref: po.Reference) -> dict:
     return out
 
 
+SCENARIO_TEXTS = {
+    "valid_two_rows": "bus:4:p,bus:4:q,bus:14:p\n10,2,5\n11,3,6\n",
+    "valid_crlf_blank": "bus:9:q\r\n\r\n16.6\r\n  \n17\n",
+    "valid_neg_exp": "bus:2:p,bus:3:q\n-1.5e1,0.25\n",
+    "bad_field": "bus:4:x\n1\n",
+    "unknown_bus": "bus:99:p\n1\n",
+    "cell_count": "bus:4:p,bus:5:p\n1\n",
+    "no_rows": "bus:4:p\n",
+    "empty": "",
+    "bad_number": "bus:4:p\n1e\n",
+    "plus_id": "bus:+4:p\n1\n",
+    "short_header": "bus:4p\n1\n",
+}
+OUTAGE_TEXTS = {
+    "valid_comments": "0 3 # comment\n5\n\n19\n",
+    "valid_float_int": "2.0 7\n",
+    "only_comment": "# nothing\n",
+    "out_of_range": "20\n",
+    "fractional": "1.5\n",
+    "negative": "-1\n",
+    "bad_token": "3 x\n",
+}
+
+
+def io_kats(ref: po.Reference) -> dict:
+    """parse_scenario_csv / parse_outage_list (case_io.hpp:368-471) on case14, as the
+    reference returns them (values, or the error category code)."""
+    with open(util.case_path("case14")) as fh:
+        rc = ref.parse(fh.read())
+    out = {"case": "case14", "scenario": {}, "outages": {}}
+    for k, text in SCENARIO_TEXTS.items():
+        try:
+            p, q = rc.scenario(text)
+            out["scenario"][k] = {"text": text, "p_mw": p.tolist(), "q_mvar": q.tolist()}
+        except po.OracleError as e:
+            out["scenario"][k] = {"text": text, "error": e.code}
+    for k, text in OUTAGE_TEXTS.items():
+        try:
+            out["outages"][k] = {"text": text, "branches": rc.outages(text).tolist()}
+        except po.OracleError as e:
+            out["outages"][k] = {"text": text, "error": e.code}
+    return out
+
+
 def main():
     po.build(ref=True)
     ref = po.Reference()
@@ -126,6 +170,8 @@ def main():
                                        nnzY=int(g["indptr"][-1]))
         print(name, manifest["cases"][name], flush=True)
     np.savez_compressed(os.path.join(OUT, "sparse_kats.npz"), **sparse_kats(ref))
+    with open(os.path.join(OUT, "io_kats.json"), "w") as fh:
+        json.dump(io_kats(ref), fh, indent=1)
     with open(os.path.join(OUT, "MANIFEST.json"), "w") as fh:
         json.dump(manifest, fh, indent=1)
 
