@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--tasks", type=int, default=10000, help="tasks per GPU (weak scaling)")
     ap.add_argument("--total-tasks", type=int, default=0, help="strong scaling: total tasks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
-    ap.add_argument("--e2e-steps", type=int, default=8, help="batches in the pipelined e2e call")
+    ap.add_argument("--e2e-steps", type=int, default=10,
+                    help="batches in the pipelined e2e call (10 x 10k = the 100k-scenario job of configs[4])")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 

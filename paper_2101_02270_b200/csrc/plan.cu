@@ -906,6 +906,15 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (const char* e = std::getenv("GBNR_STAGE_FRAC")) wc.stage_frac = std::atof(e);
         if (const char* e = std::getenv("GBNR_SMEM_BUDGET")) wc.smem_budget = std::atoi(e);
         if (const char* e = std::getenv("GBNR_BALANCE")) wc.balance = std::atof(e);
+        if (const char* e = std::getenv("GBNR_LEVELS")) {  // e.g. "8,8,4,2,1"
+            for (const char* q = e; *q;) {
+                wc.levels.push_back(std::atoi(q));
+                while (*q && *q != ',') ++q;
+                if (*q == ',') ++q;
+            }
+            if (wc.levels.empty() || wc.levels.front() != wc.walkers || wc.levels.back() != 1)
+                throw Error(GBNR_ECONFIG, "GBNR_LEVELS must start at the walker count and end at 1");
+        }
         auto build_walks = [&] {
             p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
             p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);

@@ -585,8 +585,12 @@ Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g, 
     for (;;) {
         g = geometry(s, cfg, sc.K);
         sc.lvl_walkers.clear();
-        for (int32_t k = sc.K; k > 1; k /= 2) sc.lvl_walkers.push_back(k);
-        sc.lvl_walkers.push_back(1);
+        if (!cfg.levels.empty() && sc.K == cfg.walkers) {
+            sc.lvl_walkers = cfg.levels;  // explicit walkers per level (experiments)
+        } else {
+            for (int32_t k = sc.K; k > 1; k /= 2) sc.lvl_walkers.push_back(k);
+            sc.lvl_walkers.push_back(1);
+        }
         sc.levels = static_cast<int32_t>(sc.lvl_walkers.size());
         std::vector<int32_t> ring(sc.levels), stage(sc.levels);
         for (int32_t l = 0; l < sc.levels; ++l) split_share(cfg, g.rows / sc.lvl_walkers[l], ring[l], stage[l]);
