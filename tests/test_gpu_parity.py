@@ -266,3 +266,21 @@ def test_runtime_modes_match_oracle():
     np.testing.assert_array_equal(ts.status, o["status"])
     np.testing.assert_array_equal(ts.va, o["va"])
     assert ts.report["counts"]["converged"] == 24
+
+
+def test_full_size_batch_sampled_parity():
+    """BASELINE configs[4] per-GPU slice at full size (synth9241 x 12.5k tasks, past
+    the 2^31-element mark of a [zLU][B] tape, 64-bit tile offsets): tasks sampled
+    across the batch -- first, last, both sides of tile boundaries -- match the
+    oracle run on just those tasks bitwise (solo == batch)."""
+    gc, plan, oplan, vm0, va0 = _setup("synth9241")
+    T = 12500
+    p0, q0 = montecarlo(gc, T)
+    r = plan.solve(p0, q0, vm0, va0, n_tasks=T)
+    assert (r.status == 0).all()
+    pick = np.array([0, 1, 31, 32, 4095, 4096, 6250, 9999, 10000, 12287, 12288, 12479, 12480, 12498, 12499])
+    o = oplan.solve(p0[:, pick], q0[:, pick], vm0[:, None], va0[:, None], n_tasks=len(pick))
+    np.testing.assert_array_equal(r.iterations[pick], o["iterations"])
+    np.testing.assert_array_equal(r.vm[:, pick], o["vm"])
+    np.testing.assert_array_equal(r.va[:, pick], o["va"])
+    np.testing.assert_array_equal(r.max_mismatch[pick], o["max_mismatch"])
