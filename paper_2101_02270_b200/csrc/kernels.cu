@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
     const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
     for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
         const size_t o = size_t(bus) * v.bpad + t;
-        const double vm = real ? v.vm_in[o] : 1.0, va = real ? v.va_in[o] : 0.0;
+        const size_t vi = size_t(bus) * v.vin_ld + size_t(real ? t : 0) * v.vin_inc;
+        const double vm = real ? v.vm_in[vi] : 1.0, va = real ? v.va_in[vi] : 0.0;
         v.vm[o] = vm;
         v.va[o] = va;
         double s, c;

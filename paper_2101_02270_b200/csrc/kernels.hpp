@@ -26,7 +26,8 @@ struct DevView {
     const int32_t* lk;
     // per-task tapes [elem][bpad]
     double *vm, *va, *c, *s;
-    const double *vm_in, *va_in;  // staged start voltages (kept for repeated runs)
+    const double *vm_in, *va_in;  // staged start voltages (kept for repeated runs):
+    int32_t vin_ld, vin_inc;      //   bus b of task t at b * vin_ld + t * vin_inc ((1, 0) = shared)
     const double *p0, *q0;
     int32_t s_ld, s_inc;          // p0[bus * s_ld + task * s_inc]
     // tile-blocked tapes, one block per tile of tstride doubles:

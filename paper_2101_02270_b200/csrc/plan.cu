@@ -338,8 +338,14 @@ struct gbnr_plan {
         v.n_tiles = n_tiles;
         v.bpad = n_tiles * gbnr::kTile;
         v.n_tasks = n_tasks;
-        put_tape(const_cast<double*>(v.vm_in), vm0, n_vsets, n_tasks);
-        put_tape(const_cast<double*>(v.va_in), va0, n_vsets, n_tasks);
+        // start voltages as given: [n] shared or [n][n_tasks], one linear copy each
+        // (init_kernel reads them through vin_ld / vin_inc)
+        const bool vshared = n_vsets == 1;
+        const size_t vbytes = size_t(sym.n) * (vshared ? 1 : size_t(n_tasks)) * sizeof(double);
+        CK(cudaMemcpyAsync(const_cast<double*>(v.vm_in), vm0, vbytes, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(const_cast<double*>(v.va_in), va0, vbytes, cudaMemcpyHostToDevice, stream));
+        v.vin_ld = vshared ? 1 : n_tasks;
+        v.vin_inc = vshared ? 0 : 1;
         if (n_ssets == 0) {
             // injections are placed by the caller (batch pipeline)
         } else if (n_ssets == 1 && n_tasks > 1) {
