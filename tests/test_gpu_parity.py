@@ -284,3 +284,20 @@ def test_full_size_batch_sampled_parity():
     np.testing.assert_array_equal(r.vm[:, pick], o["vm"])
     np.testing.assert_array_equal(r.va[:, pick], o["va"])
     np.testing.assert_array_equal(r.max_mismatch[pick], o["max_mismatch"])
+
+
+def test_nonfinite_task_isolated():
+    """A task with a NaN / inf injection (a corrupted scenario row) never converges
+    (the max-norm treats NaN as inf), ends diverged after max_iter like the
+    oracle's, and leaves every other task bit-identical (per-task independence,
+    SPEC.md:216)."""
+    gc, plan, oplan, vm0, va0 = _setup("synth118")
+    T = 70
+    p0, q0 = montecarlo(gc, T)
+    p0[5, 10] = np.nan
+    q0[7, 41] = np.inf
+    r = plan.solve(p0, q0, vm0, va0, n_tasks=T)
+    o = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T)
+    _compare(r, o)
+    assert r.status[10] != 0 and r.status[41] != 0
+    assert (np.delete(r.status, [10, 41]) == 0).all()
