@@ -924,7 +924,9 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         auto build_walks = [&] {
             p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
             p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
-            p->wb = gbnr::build_backward_walk(p->sym, p->lay, wc);
+            gbnr::WalkConfig wcb = wc;
+            if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
+            p->wb = gbnr::build_backward_walk(p->sym, p->lay, wcb);
         };
         build_walks();
         if (p->opt.device >= 0) {
