@@ -280,10 +280,13 @@ def main():
             arr([outs[j].status for j in sel]), arr([outs[j].max_mismatch for j in sel]))
         S._check(rc)
     solve_e2e()  # warm
-    dist.barrier(rk)
-    e0 = time.perf_counter()
-    solve_e2e()
-    e2e_s = dist.reduce_max(rk, time.perf_counter() - e0)
+    e2e_runs = []
+    for _ in range(3):  # median of three jobs (host-side PCIe / pinned-memory jitter)
+        dist.barrier(rk)
+        e0 = time.perf_counter()
+        solve_e2e()
+        e2e_runs.append(dist.reduce_max(rk, time.perf_counter() - e0))
+    e2e_s = sorted(e2e_runs)[1]
     e2e_conv = dist.reduce_sum(rk, sum(int(outs[j].converged.sum()) for j in sel))
     h2d = 2 * n * T * 8
     d2h = 2 * n * T * 8 + T * (4 + 4 + 8)
@@ -325,7 +328,7 @@ def main():
                           "wall_s_timed": wall},
                "clocks": clk.summary(),
                "e2e": {"value": e2e_conv / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h, "steps": K,
+                       "d2h_bytes_per_step": d2h, "steps": K, "jobs_timed": 3, "statistic": "median",
                        "call": "gbnr_solve_batches (pinned host buffers, per-batch H2D/D2H pipelined "
                                "against the neighbouring batches' solves)"},
                "gpu_launches": int(launches),

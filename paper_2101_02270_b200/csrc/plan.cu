@@ -652,7 +652,8 @@ struct gbnr_plan {
             if (sts && sts[j]) std::memcpy(sts[j], h_st[set], ntt * 4);
             if (mms && mms[j]) std::memcpy(mms[j], h_mm[set], ntt * 8);
             if (convs && convs[j])
-                for (size_t t = 0; t < ntt; ++t) convs[j][t] = h_st[set][t] == GBNR_CONVERGED;
+                for (size_t t = 0; t < ntt; ++t)
+                    convs[j][t] = h_st[set][t] == GBNR_CONVERGED || h_st[set][t] == GBNR_FALLBACK_CONVERGED;
         };
         // geometry, the plan's Ybus and the shared start voltages (injections come per batch below)
         stage_ybus(nullptr, nullptr, 1, n_tasks);
