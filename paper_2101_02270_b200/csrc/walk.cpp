@@ -484,8 +484,9 @@ Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
 }
 
 // Per-walker ring / staging split of a share of rows.
-void split_share(const WalkConfig& cfg, int32_t share, int32_t& ring, int32_t& stage) {
-    stage = cfg.stage_rows ? cfg.stage_rows : int32_t(share * cfg.stage_frac);
+void split_share(const WalkConfig& cfg, int32_t share, int32_t& ring, int32_t& stage, int32_t level = 0) {
+    const double frac = level > 0 && cfg.stage_frac_up >= 0.0 ? cfg.stage_frac_up : cfg.stage_frac;
+    stage = cfg.stage_rows ? cfg.stage_rows : int32_t(share * frac);
     ring = cfg.ring_rows ? cfg.ring_rows : share - stage;
 }
 
@@ -517,7 +518,7 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
             if (!list.empty()) {
                 PlanCfg pc{};
                 pc.ring_base = slot * share;
-                split_share(cfg, share, pc.ring_rows, pc.stage_rows);
+                split_share(cfg, share, pc.ring_rows, pc.stage_rows, int32_t(ph));
                 if (pc.ring_rows + pc.stage_rows > share) throw Error(3, "walk ring overrides exceed the CTA budget");
                 pc.barriers = cfg.barriers;
                 pc.prefetch = cfg.prefetch;
@@ -593,7 +594,7 @@ Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g, 
         }
         sc.levels = static_cast<int32_t>(sc.lvl_walkers.size());
         std::vector<int32_t> ring(sc.levels), stage(sc.levels);
-        for (int32_t l = 0; l < sc.levels; ++l) split_share(cfg, g.rows / sc.lvl_walkers[l], ring[l], stage[l]);
+        for (int32_t l = 0; l < sc.levels; ++l) split_share(cfg, g.rows / sc.lvl_walkers[l], ring[l], stage[l], l);
         if (partition_levels(s, cfg, sc.lvl_walkers, ring, stage, backward, sc.level, sc.bin)) return sc;
         if (sc.K == 1) throw Error(3, "walk schedule failed with one walker");
         sc.K = 1;  // dependencies cross subtrees: one walker

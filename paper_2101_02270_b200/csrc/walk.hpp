@@ -81,6 +81,7 @@ struct WalkConfig {
     int32_t pages = 2;            // program-stream pages resident per walker
     double balance = 2.0;         // split subtrees heavier than total / (walkers * balance)
     double stage_frac = 0.35;     // staging share of a walker's rows
+    double stage_frac_up = 0.45;  // staging share above level 0 (< 0: stage_frac)
     std::vector<int32_t> levels;  // walkers per level (empty: walkers, walkers/2, ..., 1)
 };
 
