@@ -327,3 +327,16 @@ def test_walk_stats_and_layout():
     bl = plan.walk_export(2)["owner"] >> 4
     assert (bl == 0).mean() >= (level == 0).mean()
     plan.close()
+
+
+def test_sequential_reference_kat():
+    """SPEC.md:335 known answer for the sequential Alg. 2 + FS/BS the replays are
+    compared with: L = [[1], [2, 1], [0, 3, 1]] (unit lower triangular, so U = I),
+    b = [1, 4, 11] -> y = x = [1, 2, 5]."""
+    ex = {"col_ptr": np.array([0, 2, 4, 5]), "row_ix": np.array([0, 1, 1, 2, 2])}
+    A = np.array([[1.0], [2.0], [1.0], [3.0], [1.0]])
+    b = np.array([[1.0], [4.0], [11.0]])
+    lu, y, x = sequential(ex, A, b)
+    np.testing.assert_array_equal(y[:, 0], [1.0, 2.0, 5.0])
+    np.testing.assert_array_equal(x[:, 0], [1.0, 2.0, 5.0])
+    np.testing.assert_array_equal(lu, A)  # already factored: L unchanged, U = I
