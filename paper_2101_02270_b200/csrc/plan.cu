@@ -913,6 +913,7 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (const char* e = std::getenv("GBNR_STAGE_FRAC")) wc.stage_frac = std::atof(e);
         if (const char* e = std::getenv("GBNR_STAGE_FRAC_UP")) wc.stage_frac_up = std::atof(e);
         if (const char* e = std::getenv("GBNR_PAGE_WORDS")) wc.page_words = std::atoi(e);
+        if (const char* e = std::getenv("GBNR_UNIFIED")) wc.unified = std::atoi(e) != 0;  // 0: split plans
         if (const char* e = std::getenv("GBNR_SMEM_BUDGET")) wc.smem_budget = std::atoi(e);
         if (const char* e = std::getenv("GBNR_BALANCE")) wc.balance = std::atof(e);
         if (const char* e = std::getenv("GBNR_LEVELS")) {  // e.g. "8,8,4,2,1"

@@ -316,6 +316,299 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
     return w;
 }
 
+// Unified-pool variant of plan(): the step blocks and the re-fetched
+// dependencies share one circular pool of ring + staging rows, allocated in
+// consumption order, so a step with few fetches prefetches its successors'
+// blocks further ahead and a step with many fetches borrows block rows.  A
+// dependency stays resident while its producer's block is intact.  Every
+// overlap with live rows becomes an issue constraint; an overlap that would
+// make the op late (or hit the step's own block or its chunk) moves the
+// allocation past that region.  Same verification as plan().
+Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
+    const int32_t T = static_cast<int32_t>(steps.size());
+    Walk w;
+    w.ring_base = cfg.ring_base;
+    w.ring_rows = cfg.ring_rows;
+    w.stage_rows = cfg.stage_rows;
+    w.barriers = cfg.barriers;
+    w.n_steps = T;
+    const int32_t XR = w.ring_rows, SR = w.stage_rows, NB = w.barriers, RB = cfg.ring_base;
+    const int32_t PR = XR + SR;
+    for (const StepIn& st : steps) {
+        if (st.blk_rows > PR) throw Error(3, "walk block larger than the walker's pool");
+        for (const DepIn& d : st.deps)
+            if (d.fetch_rows > PR) throw Error(3, "walk fetch larger than the walker's pool");
+    }
+    std::vector<int64_t> ev0(T + 1);
+    int64_t e = 0;
+    for (int32_t t = 0; t < T; ++t) {
+        ev0[t] = e;
+        e += int64_t(steps[t].deps.size()) + 1;
+    }
+    ev0[T] = e;
+    w.events = e;
+    if (e >= kInf) throw Error(3, "walk too long");
+    auto ev_dep = [&](int32_t t, size_t d) { return int32_t(ev0[t] + int64_t(d)); };
+    auto ev_done = [&](int32_t t) { return t < 0 ? -1 : int32_t(ev0[t + 1] - 1); };
+
+    struct Reg {
+        int32_t a, b, release, block;  // block: producing step, -1 = a fetch
+    };
+    std::vector<Reg> live;
+    std::vector<int32_t> ring(T, 0);
+    std::vector<char> intact(T, 0);
+    std::vector<std::vector<char>> resident(T);
+    int32_t cur = 0;
+    // place n rows: returns the row or -1; `after` gets the overlapped releases
+    auto place = [&](int32_t n, int32_t consume, int32_t lo, int32_t hi, int32_t self_block, int32_t& after) {
+        int32_t at = cur;
+        for (int32_t tries = 0; tries < 2 * PR + 2; ++tries) {
+            if (at + n > PR) at = 0;
+            bool ok = true;
+            int32_t aft = -1, skip_to = at + 1;
+            for (const Reg& r : live) {
+                if (r.a < at + n && at < r.b) {
+                    if (r.release > consume || (self_block >= 0 && r.block == self_block)) {
+                        ok = false;
+                        skip_to = std::max(skip_to, r.b);
+                    } else {
+                        aft = std::max(aft, r.release);
+                    }
+                }
+            }
+            if (ok && hi >= 0 && at < hi && lo < at + n) {  // the open chunk's own rows
+                ok = false;
+                skip_to = std::max(skip_to, hi);
+            }
+            if (ok) {
+                after = aft;
+                return at;
+            }
+            at = skip_to;
+        }
+        return int32_t(-1);
+    };
+    auto occupy = [&](int32_t at, int32_t n, int32_t release, int32_t block) {
+        std::vector<Reg> keep;
+        for (const Reg& r : live) {
+            if (r.a < at + n && at < r.b) {
+                if (r.block >= 0) intact[r.block] = 0;
+            } else {
+                keep.push_back(r);
+            }
+        }
+        keep.push_back(Reg{at, at + n, release, block});
+        live.swap(keep);
+        cur = at + n;
+    };
+
+    std::vector<int32_t> release;
+    std::vector<int32_t> tag_of_copy;
+    std::vector<int32_t> dep_tag0(T + 1, 0);
+    for (int32_t t = 0; t < T; ++t) dep_tag0[t + 1] = dep_tag0[t] + int32_t(steps[t].deps.size());
+    std::vector<int32_t> tag_producer(dep_tag0[T], -1), op_of_tag(dep_tag0[T], kInf);
+    for (int32_t t = 0; t < T; ++t)
+        for (size_t d = 0; d < steps[t].deps.size(); ++d) tag_producer[dep_tag0[t] + d] = steps[t].deps[d].producer;
+    struct Chunk {
+        std::vector<WCopy> cps;
+        std::vector<int32_t> tags;
+        int32_t after = -1, consume = -1, rel = -1, lo = kInf, hi = -1;
+    };
+    auto push_chunk = [&](Chunk& c) {
+        const int32_t s = static_cast<int32_t>(w.op.size());
+        int32_t after = c.after;
+        if (s >= NB) after = std::max(after, release[s - NB]);
+        if (s > 0) after = std::max(after, w.op[s - 1].after);
+        if (after > c.consume) throw Error(3, "walk plan infeasible (shared-memory pool too small)");
+        WOp o{};
+        o.after = after;
+        o.ncopy = static_cast<int32_t>(c.cps.size());
+        o.c0 = static_cast<int32_t>(w.copies.size());
+        for (size_t i = 0; i < c.cps.size(); ++i) {
+            o.bytes += copy_rows(c.cps[i]) * 256;
+            w.copies.push_back(c.cps[i]);
+            tag_of_copy.push_back(c.tags[i]);
+            if (c.tags[i] >= T) op_of_tag[c.tags[i] - T] = s;
+        }
+        w.op.push_back(o);
+        release.push_back(c.rel);
+        return s;
+    };
+    for (int32_t t = 0; t < T; ++t) {
+        StepIn& si = steps[t];
+        WStep rec = si.rec;
+        Chunk ch;
+        ch.consume = ev_done(t - 1);
+        ch.rel = int32_t(ev0[t]);
+        // the block goes where it leaves a contiguous gap for the step's largest
+        // fetch (a block in the middle of the pool fragments it): the FIFO
+        // position first, then either end
+        int32_t need = 0;
+        for (const DepIn& di : si.deps) need = std::max(need, di.fetch_rows);
+        int32_t aft = -1, at = -1;
+        for (int32_t cand : {cur, 0, PR - si.blk_rows}) {
+            const int32_t keep_cur = cur;
+            cur = cand;
+            int32_t a2 = -1;
+            const int32_t pos = place(si.blk_rows, ch.consume, 0, -1, -1, a2);
+            cur = keep_cur;
+            if (pos < 0) continue;
+            if (at < 0) {
+                at = pos;
+                aft = a2;
+            }
+            if (std::max(pos, PR - pos - si.blk_rows) >= need) {
+                at = pos;
+                aft = a2;
+                break;
+            }
+        }
+        if (at < 0) throw Error(3, "walk plan infeasible (no pool rows for a block)");
+        occupy(at, si.blk_rows, ev_done(t), t);
+        intact[t] = 1;
+        ring[t] = at;
+        ch.after = std::max(ev_done(t - cfg.prefetch - 1), aft);
+        rec.ring = RB + at;
+        rec.dep0 = static_cast<int32_t>(w.dep.size());
+        rec.ndep = static_cast<int32_t>(si.deps.size());
+        w.block_rows += si.blk_rows;
+        for (WCopy c : si.copies) {
+            c.smem += RB + at;
+            ch.cps.push_back(c);
+            ch.tags.push_back(t);
+        }
+        bool first_chunk = true;
+        std::vector<size_t> chunk_deps;
+        auto close_chunk = [&]() {
+            const int32_t op = push_chunk(ch);
+            if (first_chunk)
+                rec.op = op;
+            else
+                w.dep[chunk_deps.front()].op = op;
+            first_chunk = false;
+            chunk_deps.clear();
+        };
+        resident[t].assign(si.deps.size(), 0);
+        for (size_t d = 0; d < si.deps.size(); ++d) {
+            DepIn& di = si.deps[d];
+            WDep dr = di.rec;
+            dr.op = -1;
+            const int32_t pr = di.producer;
+            if (pr >= 0 && intact[pr] && di.ring_src >= 0) {
+                resident[t][d] = 1;
+                for (Reg& r : live)
+                    if (r.block == pr) r.release = std::max(r.release, ev_dep(t, d));
+                dr.src = RB + ring[pr] + di.ring_src;
+                dr.ysrc = di.ring_ysrc >= 0 ? RB + ring[pr] + di.ring_ysrc : -1;
+                w.ring_dep_rows += di.fetch_rows;
+                w.dep.push_back(dr);
+                continue;
+            }
+            if (di.fetch_rows <= 0) throw Error(3, "walk dependency with nothing to fetch");
+            int32_t faft = -1;
+            int32_t fat = int32_t(int(ch.cps.size() + di.fetch.size()) <= cfg.max_copies
+                                      ? place(di.fetch_rows, ch.consume, ch.lo, ch.hi, t, faft) : -1);
+            if (fat < 0) {  // a new chunk, waited on at this dependency
+                close_chunk();
+                ch = Chunk{};
+                ch.after = ev_done(t - cfg.prefetch - 1);
+                ch.consume = d == 0 ? ev_done(t - 1) : ev_dep(t, d - 1);
+                ch.rel = ev_dep(t, d);
+                fat = place(di.fetch_rows, ch.consume, 0, -1, t, faft);
+                if (fat < 0) throw Error(3, "walk plan infeasible (no pool rows for a fetch)");
+            }
+            occupy(fat, di.fetch_rows, ev_dep(t, d), -1);
+            ch.after = std::max(ch.after, faft);
+            if (pr >= 0) ch.after = std::max(ch.after, ev_done(pr));
+            ch.lo = std::min(ch.lo, fat);
+            ch.hi = std::max(ch.hi, fat + di.fetch_rows);
+            for (WCopy c : di.fetch) {
+                c.smem += RB + fat;
+                ch.cps.push_back(c);
+                ch.tags.push_back(T + dep_tag0[t] + int32_t(d));
+            }
+            dr.src = di.stage_src >= 0 ? RB + fat + di.stage_src : -1;
+            dr.ysrc = di.stage_ysrc >= 0 ? RB + fat + di.stage_ysrc : -1;
+            w.fetched_rows += di.fetch_rows;
+            chunk_deps.push_back(w.dep.size());
+            w.dep.push_back(dr);
+        }
+        close_chunk();
+        w.step.push_back(rec);
+    }
+
+    // 5. independent verification: replay the consumer's events, issue ops at
+    //    their events and check that no shared-memory row is overwritten while
+    //    its content is still to be read, that every op is issued before it is
+    //    waited on, that every read finds the content it expects, and that
+    //    every fetch of produced data follows its producer.
+    {
+        const int32_t rows = XR + SR;
+        const int32_t n_tags = T + dep_tag0[T];
+        std::vector<int32_t> need(n_tags, -1);  // last event reading each content tag
+        for (int32_t t = 0; t < T; ++t) {
+            need[t] = std::max(need[t], ev_done(t));
+            for (int32_t d = 0; d < w.step[t].ndep; ++d) {
+                const int32_t p = steps[t].deps[d].producer;
+                const int32_t g = resident[t][d] ? p : T + dep_tag0[t] + d;
+                need[g] = std::max(need[g], ev_dep(t, d));
+            }
+        }
+        std::vector<int32_t> row_tag(rows, -1);
+        size_t next = 0;
+        auto issue_upto = [&](int32_t ev) {
+            while (next < w.op.size() && w.op[next].after <= ev) {
+                const WOp& o = w.op[next];
+                for (int32_t i = 0; i < o.ncopy; ++i) {
+                    const WCopy& c = w.copies[o.c0 + i];
+                    const int32_t a = c.smem - RB, n = copy_rows(c), g = tag_of_copy[o.c0 + i];
+                    if (a < 0 || a + n > rows) throw Error(3, "walk copy outside the walker's shared memory");
+                    for (int32_t r = a; r < a + n; ++r) {
+                        if (row_tag[r] >= 0 && need[row_tag[r]] > ev)
+                            throw Error(3, "walk plan overwrites live shared memory (row " +
+                                               std::to_string(r) + ")");
+                        row_tag[r] = g;
+                    }
+                    if (g >= T) {  // a re-fetch of produced data: its producer must be done
+                        const int32_t p = tag_producer[g - T];
+                        if (p >= 0 && ev < ev_done(p))
+                            throw Error(3, "walk fetch issued before its producer finished");
+                    }
+                }
+                ++next;
+            }
+        };
+        auto expect = [&](int32_t row, int32_t g) {
+            if (row >= 0 && row_tag[row - RB] != g) throw Error(3, "walk reads content that is not there");
+        };
+        issue_upto(-1);
+        int32_t waited = -1;
+        for (int32_t t = 0; t < T; ++t) {
+            const WStep& st = w.step[t];
+            if (size_t(st.op) >= next) throw Error(3, "walk waits on an unissued op");
+            waited = std::max(waited, st.op);
+            expect(st.ring, t);
+            for (int32_t d = 0; d < st.ndep; ++d) {
+                const WDep& dr = w.dep[st.dep0 + d];
+                if (dr.op >= 0) {
+                    if (size_t(dr.op) >= next) throw Error(3, "walk waits on an unissued fetch");
+                    waited = std::max(waited, dr.op);
+                }
+                const int32_t p = steps[t].deps[d].producer;
+                const int32_t g = resident[t][d] ? p : T + dep_tag0[t] + d;
+                expect(dr.src, g);
+                expect(dr.ysrc, g);
+                if (!resident[t][d] && op_of_tag[g - T] > waited)
+                    throw Error(3, "walk reads a fetch it never waited for");
+                issue_upto(ev_dep(t, d));
+            }
+            issue_upto(ev_done(t));
+        }
+        if (next != w.op.size()) throw Error(3, "walk ops left unissued");
+    }
+    return w;
+}
+
 // Program-stream writer of one walker: pads to the next page whenever a record
 // would straddle one.
 struct Emitter {
@@ -525,7 +818,15 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
                 pc.headroom = cfg.headroom;
                 pc.max_copies = (g.W - 5) / 2;
                 Program pr = make_program(list);
-                part = plan(pr.steps, pc);
+                bool done = false;
+                if (cfg.unified) {
+                    try {
+                        part = plan_unified(pr.steps, pc);
+                        done = true;
+                    } catch (const Error&) {  // infeasible: the split ring / staging plan
+                    }
+                }
+                if (!done) part = plan(pr.steps, pc);
                 part.dst = std::move(pr.dst);
                 part.ut = std::move(pr.ut);
                 encode(em[w], part, forward, op_base[w]);

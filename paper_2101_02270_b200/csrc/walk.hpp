@@ -80,9 +80,12 @@ struct WalkConfig {
     int32_t page_words = 128;     // program-stream page (grown to the longest record)
     int32_t pages = 2;            // program-stream pages resident per walker
     double balance = 2.0;         // split subtrees heavier than total / (walkers * balance)
-    double stage_frac = 0.35;     // staging share of a walker's rows
-    double stage_frac_up = 0.45;  // staging share above level 0 (< 0: stage_frac)
+    double stage_frac = 0.3;      // staging share of a walker's rows (split plan; the
+                                  // subtree partition sizes columns against it too)
+    double stage_frac_up = 0.3;   // staging share above level 0 (< 0: stage_frac)
     std::vector<int32_t> levels;  // walkers per level (empty: walkers, walkers/2, ..., 1)
+    bool unified = true;          // blocks and fetches share one pool (plan_unified;
+                                  // the split ring / staging plan where it is infeasible)
 };
 
 // The device program of a walk: per walker one int32 word stream the warp

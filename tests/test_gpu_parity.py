@@ -139,13 +139,17 @@ def test_repeat_solve_is_deterministic():
 @pytest.mark.parametrize("opts", [dict(walkers=4, ring_rows=36, stage_rows=24, prefetch=3),
                                   dict(walkers=1, ring_rows=64, stage_rows=40, prefetch=1, headroom=1),
                                   dict(walkers=1),
-                                  dict(walkers=8, prefetch=16, headroom=4)])
-def test_walk_plan_invariance(opts):
+                                  dict(walkers=8, prefetch=16, headroom=4),
+                                  dict(walkers=8, split=True)])
+def test_walk_plan_invariance(opts, monkeypatch):
     """execute_schedule == refactorize_batch bitwise for any execution plan:
     changing the number of walkers per tile (how the elimination tree is split into
     concurrently walked subtrees) or shrinking / growing the shared-memory rings moves
     dependencies between ring residency and TMA re-fetches and changes every copy's
     issue point, never a bit."""
+    opts = dict(opts)
+    if opts.pop("split", False):  # the split ring + staging planner (GBNR_UNIFIED=0)
+        monkeypatch.setenv("GBNR_UNIFIED", "0")
     gc, plan, oplan, vm0, va0 = _setup("synth300")
     ip, ix, _, yr, yi = S.build_ybus(gc)
     plan2 = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, **opts)

@@ -273,7 +273,11 @@ def replay_backward(w, LU, b_tape):
                                        ("synth300", dict(walkers=2, ring_rows=40, stage_rows=24, prefetch=3)),
                                        ("synth300", dict(walkers=1, ring_rows=200, stage_rows=80, prefetch=20)),
                                        ("synth2383", dict(walkers=3, prefetch=5, headroom=1))])
-def test_walk_replay_bitwise(name, opts):
+@pytest.mark.parametrize("unified", ["1", "0"])
+def test_walk_replay_bitwise(name, opts, unified, monkeypatch):
+    """Both planners: the unified block/staging pool (default) and the split
+    ring + staging plan it falls back to (GBNR_UNIFIED=0)."""
+    monkeypatch.setenv("GBNR_UNIFIED", unified)
     gc = load_case(util.case_path(name))
     plan = S.NrPlan.from_case(gc, device=-1, **opts)
     ex, A, b = jacobian_tape(gc, plan)
@@ -340,3 +344,18 @@ def test_sequential_reference_kat():
     np.testing.assert_array_equal(y[:, 0], [1.0, 2.0, 5.0])
     np.testing.assert_array_equal(x[:, 0], [1.0, 2.0, 5.0])
     np.testing.assert_array_equal(lu, A)  # already factored: L unchanged, U = I
+
+
+def test_unified_pool_planner_is_used(monkeypatch):
+    """The default plans come from the unified pool planner (its placements differ
+    from the split ring + staging plans), not from its silent fallback."""
+    gc = load_case(util.case_path("synth2383"))
+    infos = {}
+    for u in ("1", "0"):
+        monkeypatch.setenv("GBNR_UNIFIED", u)
+        plan = S.NrPlan.from_case(gc, device=-1)
+        infos[u] = [plan.walk_info(w) for w in (0, 1, 2)]
+        plan.close()
+    for a, b in zip(infos["1"], infos["0"]):
+        assert a["steps"] == b["steps"]
+        assert (a["n_ops"], a["ring_dep_rows"], a["stream_words"]) != (b["n_ops"], b["ring_dep_rows"], b["stream_words"])
