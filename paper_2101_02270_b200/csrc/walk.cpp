@@ -494,11 +494,11 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
             WDep dr = di.rec;
             dr.op = -1;
             const int32_t pr = di.producer;
-            if (pr >= 0 && intact[pr] && di.ring_src >= 0) {
+            if (pr >= 0 && intact[pr] && (di.ring_src >= 0 || di.ring_ysrc >= 0)) {
                 resident[t][d] = 1;
                 for (Reg& r : live)
                     if (r.block == pr) r.release = std::max(r.release, ev_dep(t, d));
-                dr.src = RB + ring[pr] + di.ring_src;
+                dr.src = di.ring_src >= 0 ? RB + ring[pr] + di.ring_src : -1;
                 dr.ysrc = di.ring_ysrc >= 0 ? RB + ring[pr] + di.ring_ysrc : -1;
                 w.ring_dep_rows += di.fetch_rows;
                 w.dep.push_back(dr);
