@@ -446,6 +446,18 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         int32_t need = 0;
         for (const DepIn& di : si.deps) need = std::max(need, di.fetch_rows);
         int32_t aft = -1, at = -1;
+        // producers this step could read from the pool (still intact)
+        std::vector<int32_t> prods;
+        for (const DepIn& di : si.deps)
+            if (di.producer >= 0 && intact[di.producer]) prods.push_back(di.producer);
+        auto hits_prod = [&](int32_t pos) {
+            for (const Reg& r : live)
+                if (r.block >= 0 && r.a < pos + si.blk_rows && pos < r.b &&
+                    std::find(prods.begin(), prods.end(), r.block) != prods.end())
+                    return true;
+            return false;
+        };
+        int score_best = -1;
         for (int32_t cand : {cur, 0, PR - si.blk_rows}) {
             const int32_t keep_cur = cur;
             cur = cand;
@@ -453,15 +465,14 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
             const int32_t pos = place(si.blk_rows, ch.consume, 0, -1, -1, a2);
             cur = keep_cur;
             if (pos < 0) continue;
-            if (at < 0) {
+            const bool gap = std::max(pos, PR - pos - si.blk_rows) >= need;
+            const int score = (gap ? 2 : 0) + (hits_prod(pos) ? 0 : 1);
+            if (score > score_best) {
+                score_best = score;
                 at = pos;
                 aft = a2;
             }
-            if (std::max(pos, PR - pos - si.blk_rows) >= need) {
-                at = pos;
-                aft = a2;
-                break;
-            }
+            if (score == 3) break;
         }
         if (at < 0) throw Error(3, "walk plan infeasible (no pool rows for a block)");
         occupy(at, si.blk_rows, ev_done(t), t);
