@@ -12,7 +12,7 @@ namespace gbnr {
 
 constexpr int kTile = 32;      // tasks per tile = lanes of a warp
 constexpr int kSuper = 8;      // tiles per super-tile = warps per block (2 KB access runs)
-constexpr int kRowChunk = 8;  // Ybus rows per block in the NPM / Jacobian kernels
+constexpr int kRowChunk = 4;  // Ybus rows per warp in the NPM / Jacobian kernels
 
 // Everything a kernel needs, by value (device pointers + sizes).  All per-task
 // tapes are element-major: value(elem, task) at elem * bpad + task.
