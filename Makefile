@@ -9,7 +9,7 @@ SRC     := $(PKG)/csrc
 LIB     := $(PKG)/libgbnr.so
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -std=c++20 -O3 $(ARCH) -lineinfo --fmad=false -Xptxas -v \
-           -Xcompiler -fPIC,-ffp-contract=off,-Wall -cudart static $(if $(GBNR_TRACE),-DGBNR_TRACE)
+           -Xcompiler -fPIC,-ffp-contract=off,-Wall -cudart static $(if $(GBNR_TRACE),-DGBNR_TRACE) $(if $(GBNR_PROF),-DGBNR_PROF)
 SRCS    := $(SRC)/symbolic.cpp $(SRC)/walk.cpp $(SRC)/kernels.cu $(SRC)/plan.cu
 HDRS    := $(SRC)/symbolic.hpp $(SRC)/walk.hpp $(SRC)/kernels.hpp $(SRC)/numerics.cuh include/gbnr.h
 

@@ -327,6 +327,25 @@ __device__ __forceinline__ void walk_trace(const DevView& v, int tile, int warp,
 #endif
 }
 
+// Walker time breakdown (make GBNR_PROF=1, GBNR_DBG & 8): clock64 deltas per
+// record category, summed over tiles per (phase, warp) into DevView::prof.
+#ifdef GBNR_PROF
+#define PROF_DECL long long pf_t = clock64(), pf[12] = {0}; int pf_ph = 0;
+#define PROF_MARK(c) { const long long now_ = clock64(); pf[c] += now_ - pf_t; pf_t = now_; }
+#define PROF_CNT(c) { pf[c] += 1; }
+#define PROF_FLUSH                                                                          \
+    if (v.prof && lane == 0) {                                                              \
+        for (int i_ = 0; i_ < 12; ++i_)                                                     \
+            atomicAdd(v.prof + (size_t(pf_ph) * 8 + warp) * 16 + i_, (unsigned long long)pf[i_]); \
+        for (int i_ = 0; i_ < 12; ++i_) pf[i_] = 0;                                         \
+    }
+#else
+#define PROF_DECL
+#define PROF_MARK(c)
+#define PROF_CNT(c)
+#define PROF_FLUSH
+#endif
+
 // Shared memory of a walk CTA: [rows][32] doubles shared by the walkers (each
 // phase's plan gives every walker a disjoint share), then per walker its
 // program pages and its op / page mbarriers.
@@ -420,6 +439,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
     double acc_y = 0.0;
     int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
+    PROF_DECL
     for (;;) {
         const int32_t* r = P.cur;
         const int type = h & 15;
@@ -432,8 +452,11 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const int nrows = w2 & 0xffff;
             const int n4 = (nrows + 3) & ~3;
             h = r[6 + (n4 >> 1)];
+            PROF_MARK(5)
             if (op >= 0) prog_wait(P, op);
             if (op2 >= 0) prog_wait(P, op2);
+            PROF_MARK(1)
+            PROF_CNT(10)
             const unsigned s1 = R0 + (unsigned(w2) >> 16) * RB, s2 = R0 + unsigned(w3 & 0xffff) * RB;
             const int fs1 = int(unsigned(w3) >> 16);
             double fl1 = 0.0, fy1 = 0.0, fl2 = 0.0, fy2 = 0.0;
@@ -476,13 +499,17 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 if (fs2 != 0xffff) acc_y = fma(-fl2, fy2, acc_y);
             }
             P.cur += 6 + (n4 >> 1);
+            PROF_MARK(5)
         } else if (__builtin_expect(type == kRecDep, 1)) {
             const int op = (h >> 4) - 1;
             const int kpos_fs = r[1], nrows = r[2] & 0xffff, src_row = int(unsigned(r[2]) >> 16);
             const int ysrc = r[3];
             const int n4 = (nrows + 3) & ~3;  // destinations padded with the scratch row len
             h = r[4 + (n4 >> 1)];
+            PROF_MARK(4)
             if (op >= 0) prog_wait(P, op);
+            PROF_MARK(1)
+            PROF_CNT(9)
             const unsigned src = R0 + unsigned(src_row) * RB;
             // forward-substitution operands first: they live in other blocks than
             // the x being updated, so their latency hides under the update
@@ -552,9 +579,12 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             }
             if (FS && fspos != 0xffff) acc_y = fma(-fl, fy, acc_y);
             P.cur += 4 + (n4 >> 1);
+            PROF_MARK(4)
         } else if (__builtin_expect(type == kRecIssue, 1)) {
             P.cur += prog_issue(v, P, r, lane);
             h = P.cur[0];
+            PROF_MARK(7)
+            PROF_CNT(11)
         } else if (type == kRecStep) {
             const int ring = r[1] & 0xffff;
             len = int(unsigned(r[1]) >> 16);
@@ -564,7 +594,10 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const int op = r[5];
             h = r[6];
             P.cur += 6;
+            PROF_MARK(8)
             prog_wait(P, op);
+            PROF_MARK(0)
+            PROF_CNT(3)
             xs = R0 + unsigned(ring) * RB;
             acc_y = FS ? lds(xs + unsigned(len) * RB) : 0.0;
         } else if (type == kRecEnd) {
@@ -623,16 +656,27 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1 + dp;
+            PROF_MARK(6)
         } else if (type == kRecPage) {
+            PROF_MARK(8)
             prog_next_page(P, lane);
             h = P.cur[0];
+            PROF_MARK(2)
         } else if (type == kRecSync) {
             walk_trace(v, tile, warp, lane, 0);
+            PROF_MARK(8)
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
+            PROF_MARK(3)
+            PROF_FLUSH
+#ifdef GBNR_PROF
+            ++pf_ph;
+#endif
             P.cur += 1;
             h = P.cur[0];
         } else {
             walk_trace(v, tile, warp, lane, 1);
+            PROF_MARK(8)
+            PROF_FLUSH
             break;
         }
     }

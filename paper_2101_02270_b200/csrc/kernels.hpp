@@ -55,6 +55,7 @@ struct DevView {
     int32_t max_iter;
     int32_t jpolicy;                // gbnr_options.jacobian
     int32_t dbg;                    // experiment switches (GBNR_DBG), 0 in production
+    unsigned long long* prof;       // walker time breakdown (GBNR_PROF builds), else null
 };
 
 // Device copy of a Walk (walk.hpp).

@@ -190,6 +190,12 @@ struct gbnr_plan {
         owned.push_back(itd);
         v.it_dev = itd;
         if (const char* d = std::getenv("GBNR_DBG")) v.dbg = std::atoi(d);
+#ifdef GBNR_PROF
+        if (v.dbg & 8) {
+            CK(cudaMalloc(&v.prof, 4 * 8 * 16 * sizeof(unsigned long long)));
+            owned.push_back(v.prof);
+        }
+#endif
         v.tol = opt.tol;
         v.singular_tol = opt.singular_tol;
         v.max_iter = opt.max_iter;
@@ -762,6 +768,28 @@ struct gbnr_plan {
         for (void* q : tmp) cudaFree(q);
     }
 
+    // walker time breakdown of the launches since the last reset (GBNR_PROF builds)
+    void prof_report(const char* what) {
+        if (!v.prof) return;
+        std::vector<unsigned long long> h(4 * 8 * 16);
+        CK(cudaMemcpy(h.data(), v.prof, h.size() * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemset(v.prof, 0, h.size() * 8));
+        static const char* cat[12] = {"stepwait", "depwait", "page", "sync", "dep", "dep2", "end", "issue",
+                                      "other", "n_dep", "n_dep2", "n_issue"};
+        std::fprintf(stderr, "[prof %s] per phase: cycles summed over tiles, per walker warp\n", what);
+        for (int ph = 0; ph < 4; ++ph)
+            for (int w = 0; w < 8; ++w) {
+                const unsigned long long* c = h.data() + (ph * 8 + w) * 16;
+                unsigned long long tot = 0;
+                for (int i = 0; i < 9; ++i) tot += c[i];
+                if (!tot) continue;
+                std::fprintf(stderr, "ph%d w%d tot %.3g:", ph, w, double(tot));
+                for (int i = 0; i < 12; ++i)
+                    std::fprintf(stderr, " %s=%.3g", cat[i], i < 9 ? double(c[i]) / double(tot) : double(c[i]));
+                std::fprintf(stderr, "\n");
+            }
+    }
+
     void refactor(int32_t reps, double* lu_out, uint8_t* flags_out, double* ms_out) {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_refactor before gbnr_stage");
         CK(cudaSetDevice(opt.device));
@@ -769,6 +797,10 @@ struct gbnr_plan {
         gbnr::launch_jacobian(v, true, stream);
         CK(cudaGetLastError());
         gbnr::launch_lu_walk(v, vl, false, stream);  // warm-up
+        if (v.prof) {
+            CK(cudaStreamSynchronize(stream));
+            CK(cudaMemset(v.prof, 0, 4 * 8 * 16 * 8));
+        }
         CK(cudaEventRecord(ev0, stream));
         for (int32_t r = 0; r < reps; ++r) gbnr::launch_lu_walk(v, vl, false, stream);
         CK(cudaEventRecord(ev1, stream));
@@ -777,6 +809,7 @@ struct gbnr_plan {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
         if (ms_out) *ms_out = reps > 0 ? ms / reps : 0.0;
+        prof_report("refactor");
         const int32_t nt = v.n_tasks;
         if (flags_out) CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
         if (lu_out) {
@@ -941,7 +974,9 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             gbnr::configure_kernels();
             // three tiles per SM: shrink the shared-memory budget until the
             // device really co-schedules three walk CTAs
-            while (gbnr::walk_ctas_per_sm(p->wf.smem_bytes(), 32 * p->wf.walkers) < 3 && wc.smem_budget > 65536) {
+            int ctas = 3;
+            if (const char* e = std::getenv("GBNR_CTAS")) ctas = std::max(1, std::atoi(e));
+            while (gbnr::walk_ctas_per_sm(p->wf.smem_bytes(), 32 * p->wf.walkers) < ctas && wc.smem_budget > 65536) {
                 wc.smem_budget -= 1024;
                 build_walks();
             }
