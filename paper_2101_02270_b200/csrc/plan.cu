@@ -91,6 +91,7 @@ struct gbnr_plan {
     double* d_scratch = nullptr;  // [n] staging for broadcast sets
     std::vector<void*> batch;     // per-batch tapes
     int32_t cap_tiles = 0;        // allocated tile capacity
+    double *p0_own = nullptr, *q0_own = nullptr;  // [n][bpad] injections owned by the plan
     bool staged = false;
     bool solved = false;  // device voltages hold a finished solve
     gbnr::DevView v{};
@@ -231,8 +232,9 @@ struct gbnr_plan {
         v.y_inc = 0;
     }
 
-    // Ybus values for the next solve: n_ysets = 1 refreshes the shared set, n_tasks
-    // stages one set per task (linear copies of the caller's [nnzY][n_tasks]).
+    // Ybus values for the next solve: NULL = the plan's shared set; otherwise the
+    // caller's set(s) are staged into a per-call buffer (one shared set, y_inc = 0,
+    // or one per task, [nnzY][n_tasks]) and the plan's own set is never touched.
     void stage_ybus(const double* y_re, const double* y_im, int32_t n_ysets, int32_t n_tasks) {
         if (!y_re || !y_im) {
             if (n_ysets != 1) throw Error(GBNR_ECONFIG, "per-task Ybus sets need y_re and y_im");
@@ -242,24 +244,16 @@ struct gbnr_plan {
             v.y_inc = 0;
             return;
         }
-        if (n_ysets == 1 || n_tasks == 1) {
-            CK(cudaMemcpyAsync(const_cast<double*>(y_shared_re), y_re, size_t(sym.nnzY) * 8,
-                               cudaMemcpyHostToDevice, stream));
-            CK(cudaMemcpyAsync(const_cast<double*>(y_shared_im), y_im, size_t(sym.nnzY) * 8,
-                               cudaMemcpyHostToDevice, stream));
-            v.yre = y_shared_re;
-            v.yim = y_shared_im;
-            v.y_ld = 1;
-            v.y_inc = 0;
-            return;
-        }
-        if (n_ysets != n_tasks) throw Error(GBNR_ECONFIG, "n_ysets must be 1 or n_tasks");
-        const size_t bytes = size_t(sym.nnzY) * size_t(n_tasks) * 8;
+        const bool shared = n_ysets == 1 || n_tasks == 1;
+        if (!shared && n_ysets != n_tasks) throw Error(GBNR_ECONFIG, "n_ysets must be 1 or n_tasks");
+        const size_t sets = shared ? 1 : size_t(n_tasks);
+        const size_t bytes = size_t(sym.nnzY) * sets * 8;
         if (bytes > y_task_cap) {
             CK(cudaStreamSynchronize(stream));
             if (y_task_re) cudaFree(y_task_re);
             if (y_task_im) cudaFree(y_task_im);
             y_task_re = y_task_im = nullptr;
+            y_task_cap = 0;
             CK(cudaMalloc(&y_task_re, bytes));
             CK(cudaMalloc(&y_task_im, bytes));
             y_task_cap = bytes;
@@ -268,8 +262,8 @@ struct gbnr_plan {
         CK(cudaMemcpyAsync(y_task_im, y_im, bytes, cudaMemcpyHostToDevice, stream));
         v.yre = y_task_re;
         v.yim = y_task_im;
-        v.y_ld = n_tasks;
-        v.y_inc = 1;
+        v.y_ld = shared ? 1 : n_tasks;
+        v.y_inc = shared ? 0 : 1;
     }
 
     void ensure_capacity(int32_t n_tiles) {
@@ -291,8 +285,10 @@ struct gbnr_plan {
         v.va_in = static_cast<double*>(alloc(nb));
         v.c = static_cast<double*>(alloc(nb));
         v.s = static_cast<double*>(alloc(nb));
-        v.p0 = static_cast<double*>(alloc(nb));
-        v.q0 = static_cast<double*>(alloc(nb));
+        // the plan's own injection tapes; the batch pipeline points v.p0 / v.q0 at
+        // its input sets for the duration of gbnr_solve_batches only
+        v.p0 = p0_own = static_cast<double*>(alloc(nb));
+        v.q0 = q0_own = static_cast<double*>(alloc(nb));
         // one block per tile: A, LU and b rows adjacent, so a walk copy's source is
         // tile base + (tape * tape_rows + slot) rows
         v.tstride = (2 * size_t(v.tape_rows) + size_t(v.nJ)) * gbnr::kTile;
@@ -352,6 +348,10 @@ struct gbnr_plan {
         CK(cudaMemcpyAsync(const_cast<double*>(v.va_in), va0, vbytes, cudaMemcpyHostToDevice, stream));
         v.vin_ld = vshared ? 1 : n_tasks;
         v.vin_inc = vshared ? 0 : 1;
+        if (n_ssets != 0) {
+            v.p0 = p0_own;
+            v.q0 = q0_own;
+        }
         if (n_ssets == 0) {
             // injections are placed by the caller (batch pipeline)
         } else if (n_ssets == 1 && n_tasks > 1) {
@@ -649,6 +649,14 @@ struct gbnr_plan {
                        const double* vm0, const double* va0, double* const* vms, double* const* vas,
                        int32_t* const* its, uint8_t* const* convs, int32_t* const* sts, double* const* mms) {
         if (n_batches <= 0) return;
+        // whatever happens, the plan's own injection tapes are the staged ones afterwards
+        struct Restore {
+            gbnr_plan* p;
+            ~Restore() {
+                p->v.p0 = p->p0_own;
+                p->v.q0 = p->q0_own;
+            }
+        } restore{this};
         const size_t ntt = size_t(n_tasks);
         // batch j's small results: pinned staging -> the caller's arrays
         auto unstage_small = [&](int32_t j) {

@@ -79,10 +79,15 @@ def job_inputs(gc, mode: str, n_tasks: int | None = None, scenario_csv: str | No
     return JobInputs(p0, q0, y, np.zeros(p0.shape[1], bool), out)
 
 
-def run(plan: S.NrPlan, gc, mode: str, **kw) -> JobResult:
-    """batch_runtime.run for one job on one plan (one GPU).  Tasks removed by the
-    islanding pre-check keep status ISLANDED and zero voltages; all others go
-    through one gbnr_solve (second chance and re-derivation included)."""
+def run(plan: S.NrPlan, gc, mode: str, batch_size: int | None = None, **kw) -> JobResult:
+    """batch_runtime.run for one job on one plan.  Tasks removed by the islanding
+    pre-check keep status ISLANDED and zero voltages; all others go through
+    gbnr_solve (second chance and re-derivation included) in mini-batches of
+    ``batch_size`` tasks (JobSpec.batch_size; None = one batch --
+    the library itself still splits a batch that exceeds device memory).
+    Results do not depend on the batch size."""
+    if batch_size is not None and batch_size < 1:
+        raise ValueError("batch_size must be >= 1 (JobSpec invariant, SPEC.md:380)")
     t0 = time.perf_counter()
     inp = job_inputs(gc, mode, **kw)
     t_init = time.perf_counter() - t0
@@ -96,18 +101,22 @@ def run(plan: S.NrPlan, gc, mode: str, **kw) -> JobResult:
     va = np.zeros((n, T))
     mm = np.full(T, np.inf)
     t1 = time.perf_counter()
-    if keep.size:
-        y = None if inp.y is None else (np.ascontiguousarray(inp.y[0][:, keep]),
-                                        np.ascontiguousarray(inp.y[1][:, keep]))
-        r = plan.solve(np.ascontiguousarray(inp.p0[:, keep]), np.ascontiguousarray(inp.q0[:, keep]),
-                       vm0, va0, n_tasks=int(keep.size), y=y)
-        status[keep], iters[keep], mm[keep] = r.status, r.iterations, r.max_mismatch
-        vm[:, keep], va[:, keep] = r.vm, r.va
+    step = int(keep.size) if batch_size is None else int(batch_size)
+    device_ms, batches = 0.0, 0
+    for b0 in range(0, int(keep.size), max(step, 1)):
+        ids = keep[b0:b0 + step]
+        y = None if inp.y is None else (np.ascontiguousarray(inp.y[0][:, ids]),
+                                        np.ascontiguousarray(inp.y[1][:, ids]))
+        r = plan.solve(np.ascontiguousarray(inp.p0[:, ids]), np.ascontiguousarray(inp.q0[:, ids]),
+                       vm0, va0, n_tasks=int(ids.size), y=y)
+        status[ids], iters[ids], mm[ids] = r.status, r.iterations, r.max_mismatch
+        vm[:, ids], va[:, ids] = r.vm, r.va
+        device_ms += plan.timing()["total_ms"]
+        batches += 1
     t_solve = time.perf_counter() - t1
-    tm = plan.timing() if keep.size else {}
-    report = {"mode": mode, "tasks": T, "solved": int(keep.size),
+    report = {"mode": mode, "tasks": T, "solved": int(keep.size), "batches": batches,
               "init_s": t_init, "solve_wall_s": t_solve,
-              "device_ms": tm.get("total_ms", 0.0),
+              "device_ms": device_ms,
               "counts": {name: int((status == code).sum()) for name, code in
                          (("converged", CONVERGED), ("diverged", DIVERGED), ("singular", SINGULAR),
                           ("fallback_converged", FALLBACK_CONVERGED), ("islanded", ISLANDED))}}

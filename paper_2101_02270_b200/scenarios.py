@@ -8,6 +8,12 @@ rank or GPU can generate exactly its own slice of a batch:
   dispatch stays balanced before losses (the slack absorbs losses);
 * ``mode="loadpv"`` additionally scales each PV-bus generator by U(0.5, 1.0).
 
+``montecarlo`` is the benchmark workload.  Its generator
+rescaling is this repo's choice, not the reference's: SPEC.md's
+``sample_montecarlo`` only replaces bus loads and lets the slack absorb the
+change.  ``sample_montecarlo`` below is that operation as specified, with the
+per-bus distribution table {normal(mu, sigma), uniform(lo, hi), fixed}.
+
 Outputs are element-major [n_bus][n_tasks] (task innermost), the BatchTape
 layout of batch_tape.hpp:6-9 and the C ABI.
 """
@@ -58,3 +64,58 @@ def montecarlo(gc, n_tasks: int, task0: int = 0, seed: int = SEED, lo: float = 0
         raise ValueError(f"unknown scenario mode {mode!r}")
     gen_scale[gc.slack, :] = 1.0
     return gc.profiles(p_mw, q_mvar, gen_scale)
+
+
+_KINDS = ("normal", "uniform", "fixed")
+
+
+def _spec_table(spec, n: int):
+    """Per-bus (kind, a, b) arrays from one tuple (every bus) or a list of n tuples."""
+    rows = [spec] * n if isinstance(spec, tuple) else list(spec)
+    if len(rows) != n:
+        raise ValueError(f"distribution table needs {n} rows (one per bus), got {len(rows)}")
+    kind = np.empty(n, np.int8)
+    a = np.zeros(n)
+    b = np.zeros(n)
+    for i, r in enumerate(rows):
+        k = r[0]
+        if k not in _KINDS:
+            raise ValueError(f"bus {i}: unknown distribution {k!r}; expected one of {_KINDS}")
+        if k == "fixed":
+            if len(r) != 2:
+                raise ValueError(f"bus {i}: fixed takes one value")
+            kind[i], a[i] = 2, float(r[1])
+        else:
+            if len(r) != 3:
+                raise ValueError(f"bus {i}: {k} takes two parameters")
+            x, y = float(r[1]), float(r[2])
+            if k == "normal" and not (y >= 0.0 and np.isfinite(x) and np.isfinite(y)):
+                raise ValueError(f"bus {i}: normal needs finite mu and sigma >= 0")
+            if k == "uniform" and not (np.isfinite(x) and np.isfinite(y) and x <= y):
+                raise ValueError(f"bus {i}: uniform needs lo <= hi")
+            kind[i], a[i], b[i] = (0 if k == "normal" else 1), x, y
+    return kind, a, b
+
+
+def sample_montecarlo(gc, spec, n_tasks: int, task0: int = 0, seed: int = SEED):
+    """``sample_montecarlo``: per-bus load multipliers drawn from
+    a distribution table -- ('normal', mu, sigma), ('uniform', lo, hi) or
+    ('fixed', value); one tuple applies to every bus, else one per bus.  The
+    multiplier scales the bus's P and Q load; generator dispatch is unchanged
+    (the slack absorbs the difference).  Counter-based and seeded, so the same
+    seed gives the same table and any slice of tasks can be drawn on its own.
+    Returns (p0, q0) [n_bus][n_tasks] p.u. for tasks task0 .. task0+n_tasks-1."""
+    if n_tasks < 1:
+        raise ValueError("n_tasks must be >= 1")
+    n = gc.n_bus
+    kind, a, b = _spec_table(spec, n)
+    tasks = np.arange(task0, task0 + n_tasks, dtype=np.uint64)[None, :]
+    buses = np.arange(n, dtype=np.uint64)[:, None]
+    u0 = uniform(seed, 2, tasks, buses)
+    u1 = uniform(seed, 3, tasks, buses)
+    # Box-Muller on (0, 1] x [0, 1)
+    z = np.sqrt(-2.0 * np.log1p(-u0)) * np.cos(2.0 * np.pi * u1)
+    s = np.where(kind[:, None] == 0, a[:, None] + b[:, None] * z,
+                 np.where(kind[:, None] == 1, a[:, None] + (b - a)[:, None] * u0,
+                          np.broadcast_to(a[:, None], (n, n_tasks))))
+    return gc.profiles(gc.pd[:, None] * s, gc.qd[:, None] * s)

@@ -236,23 +236,34 @@ class NrPlan:
                                                ("row_fwd", "col_fwd", "col_ptr", "row_ix", "level"))))
         return d
 
-    @staticmethod
-    def _sets(a, n_tasks):
+    def _sets(self, a, n_tasks, name="array"):
         a = _f64(a)
+        if a.shape[0] != self.n_bus:
+            raise ValueError(f"{name} must have n_bus = {self.n_bus} rows, got {a.shape[0]}")
         if a.ndim == 1:
             return a, 1
-        if a.shape[1] not in (1, n_tasks):
-            raise ValueError("set count must be 1 or n_tasks")
+        if a.ndim != 2 or a.shape[1] not in (1, n_tasks):
+            raise ValueError(f"{name}: set count must be 1 or n_tasks")
         return a, a.shape[1]
 
-    def stage(self, p0, q0, vm0, va0, n_tasks: int | None = None):
+    def _inputs(self, p0, q0, vm0, va0, n_tasks):
+        """Validated (p0, q0, n_ssets, vm0, va0, n_vsets): q0 must have p0's set
+        count and va0 vm0's, or the C side would read past a host array."""
         p0 = _f64(p0); vm0 = _f64(vm0)
         if n_tasks is None:
             n_tasks = max(p0.shape[1] if p0.ndim == 2 else 1, vm0.shape[1] if vm0.ndim == 2 else 1)
-        p0, ns = self._sets(p0, n_tasks)
-        q0, _ = self._sets(q0, n_tasks)
-        vm0, nv = self._sets(vm0, n_tasks)
-        va0, _ = self._sets(va0, n_tasks)
+        p0, ns = self._sets(p0, n_tasks, "p0")
+        q0, nq = self._sets(q0, n_tasks, "q0")
+        vm0, nv = self._sets(vm0, n_tasks, "vm0")
+        va0, na = self._sets(va0, n_tasks, "va0")
+        if nq != ns:
+            raise ValueError(f"q0 has {nq} sets but p0 has {ns}")
+        if na != nv:
+            raise ValueError(f"va0 has {na} sets but vm0 has {nv}")
+        return n_tasks, p0, q0, ns, vm0, va0, nv
+
+    def stage(self, p0, q0, vm0, va0, n_tasks: int | None = None):
+        n_tasks, p0, q0, ns, vm0, va0, nv = self._inputs(p0, q0, vm0, va0, n_tasks)
         self._keep = (p0, q0, vm0, va0)
         _check(lib().gbnr_stage(self.h, n_tasks, _ptr(p0), _ptr(q0), ns, _ptr(vm0), _ptr(va0), nv))
         self._n_tasks = n_tasks
@@ -272,18 +283,14 @@ class NrPlan:
         """``nr_solve_batch`` through gbnr_solve: H2D, solve, D2H.
         ``y`` = (y_re, y_im) [nnzY] (a new shared value set) or [nnzY][T] (one per
         task, e.g. N-1 contingencies from ``contingency_values``)."""
-        p0 = _f64(p0); vm0 = _f64(vm0)
-        if n_tasks is None:
-            n_tasks = max(p0.shape[1] if p0.ndim == 2 else 1, vm0.shape[1] if vm0.ndim == 2 else 1)
-        p0, ns = self._sets(p0, n_tasks)
-        q0, _ = self._sets(q0, n_tasks)
-        vm0, nv = self._sets(vm0, n_tasks)
-        va0, _ = self._sets(va0, n_tasks)
+        n_tasks, p0, q0, ns, vm0, va0, nv = self._inputs(p0, q0, vm0, va0, n_tasks)
         yre = yim = None
         ny = 1
         if y is not None:
             yre, yim = _f64(y[0]), _f64(y[1])
             ny = yre.shape[1] if yre.ndim == 2 else 1
+            if yre.shape != yim.shape or ny not in (1, n_tasks):
+                raise ValueError("y_re / y_im must share one shape [nnzY] or [nnzY][n_tasks]")
         n, T = self.n_bus, n_tasks
         r = TaskResults(np.empty((n, T)), np.empty((n, T)), np.empty(T, np.int32),
                         np.empty(T, np.uint8), np.empty(T, np.int32), np.empty(T))
@@ -298,10 +305,17 @@ class NrPlan:
         p0s[i]/q0s[i] [n][T], shared start voltages; returns a list of TaskResults
         (or fills the preallocated `outs`)."""
         nb = len(p0s)
+        if nb == 0 or len(q0s) != nb:
+            raise ValueError("solve_batches needs one q0 per p0 and at least one batch")
         T = p0s[0].shape[1]
         n = self.n_bus
         p0s = [_f64(a) for a in p0s]
         q0s = [_f64(a) for a in q0s]
+        for a in p0s + q0s:
+            if a.shape != (n, T):
+                raise ValueError(f"every batch's p0/q0 must be [n_bus][T] = {(n, T)}, got {a.shape}")
+        if _f64(vm0).shape != (n,) or _f64(va0).shape != (n,):
+            raise ValueError("solve_batches takes shared start voltages vm0/va0 [n_bus]")
         if outs is None:
             outs = [TaskResults(np.empty((n, T)), np.empty((n, T)), np.empty(T, np.int32),
                                 np.empty(T, np.uint8), np.empty(T, np.int32), np.empty(T))
