@@ -197,10 +197,11 @@ int gbnr_last_timing(const gbnr_plan* plan, double* out);
 
 /* Tile-walk execution plans (the static TMA copy programs of the LU+FS, LU-only
  * and BS walks).  which: 0 forward LU+FS, 1 LU only, 2 backward.
- * out[16]: steps, walkers, phases, smem rows, page words, pages per walker,
+ * out[20]: steps, walkers, phases, smem rows, page words, pages per walker,
  * barriers per walker, program words, events, ring-resident dependency rows,
  * fetched rows, ops, copies, shared-memory bytes per CTA, first walker's ring
- * rows and staging rows. */
+ * rows and staging rows, steps and dependencies in global memory (blocks /
+ * fetches too large for a walker's pool), global scratch rows per walker, 0. */
 int gbnr_walk_info(const gbnr_plan* plan, int32_t which, int64_t* out);
 /* Raw walk arrays for host-side replay (tests): part 0 program words (int32,
  * walker-major pages), 1 first page per walker (int32 [walkers+1]), 2 owner

@@ -438,6 +438,10 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     unsigned xs = R0;  // this step's block
     int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
     double acc_y = 0.0;
+    // global forms (walk.hpp kRec*G): the step's block as a generic pointer (shared
+    // rows or this walker's global scratch), and the running column maximum
+    double* xg = nullptr;
+    double gmax = 0.0;
     int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
     PROF_DECL
     for (;;) {
@@ -599,6 +603,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             PROF_MARK(0)
             PROF_CNT(3)
             xs = R0 + unsigned(ring) * RB;
+            xg = P.R + size_t(ring) * kTile + lane;
             acc_y = FS ? lds(xs + unsigned(len) * RB) : 0.0;
         } else if (type == kRecEnd) {
             h = r[1 + dp];
@@ -662,6 +667,69 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             prog_next_page(P, lane);
             h = P.cur[0];
             PROF_MARK(2)
+        } else if (type == kRecDepG) {
+            // a dependency read from global memory (L(:,k) and y_k in the LU tape)
+            const int op = (h >> 4) - 1;
+            const int kpos_fs = r[1], nrows = r[2], slot = r[3], nl = r[4];
+            h = r[5 + ((nrows + 1) >> 1)];
+            if (op >= 0) prog_wait(P, op);
+            const double* src = lu_t + size_t(slot) * kTile;
+            const int fspos = int(unsigned(kpos_fs) >> 16);
+            if (nrows > 0) {
+                const double mult = xg[size_t(kpos_fs & 0xffff) * kTile];
+                const int32_t* dw = r + 5;
+                for (int q = 0; q < nrows; ++q) {
+                    const int32_t wq = dw[q >> 1];
+                    const int d = (q & 1) ? int(unsigned(wq) >> 16) : (wq & 0xffff);
+                    xg[size_t(d) * kTile] = fma(-mult, src[size_t(q) * kTile], xg[size_t(d) * kTile]);
+                }
+            }
+            if (FS && fspos != 0xffff) acc_y = fma(-src[size_t(fspos) * kTile], src[size_t(nl) * kTile], acc_y);
+            P.cur += 5 + ((nrows + 1) >> 1);
+        } else if (type == kRecStepG) {
+            // a column too large for the pool: A rows + F into this walker's scratch
+            len = r[1] & 0xffff;
+            dp = int(unsigned(r[1]) >> 16);
+            const int a0 = r[2];
+            lslot = r[3];
+            brow = r[4];
+            h = r[5];
+            P.cur += 5;
+            xg = v.scratch + (size_t(tile) * 8 + warp) * size_t(v.scratch_rows) * kTile + lane;
+            const double* at = v.A + size_t(tile) * v.tstride + lane + size_t(a0) * kTile;
+            for (int z = 0; z <= len; ++z) xg[size_t(z) * kTile] = at[size_t(z) * kTile];
+            acc_y = FS ? xg[size_t(len) * kTile] : 0.0;
+            gmax = 0.0;
+        } else if (type == kRecEndU) {
+            // U entries z0 .. z0+cnt-1 of a global step -> their row-major slots
+            const int cnt = (h >> 4) & 0xfffff, z0 = r[1];
+            h = r[2 + cnt];
+            for (int i = 0; i < cnt; ++i) {
+                const double u = xg[size_t(z0 + i) * kTile];
+                gmax = fmax(gmax, fabs(u));
+                lu_t[size_t(r[2 + i]) * kTile] = u;
+            }
+            P.cur += 2 + cnt;
+        } else if (type == kRecEndG) {
+            // END of a global step (the U part went out in kRecEndU records)
+            h = r[1];
+            const double piv = xg[size_t(dp) * kTile];
+            const double inv = 1.0 / piv;
+            double c0 = fmax(gmax, fabs(piv));
+            double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * kTile;
+            for (int z = dp + 1; z < len; ++z) {
+                const double x0 = xg[size_t(z) * kTile];
+                c0 = fmax(c0, fabs(x0));
+                lcol[size_t(z) * kTile] = x0 * inv;
+            }
+            flagged |= isfinite(c0) && (piv == 0.0 || fabs(piv) < stol * c0);
+            lu_t[size_t(brow + 1) * kTile] = piv;
+            if (FS) {
+                lcol[size_t(len) * kTile] = acc_y;
+                lu_t[size_t(brow) * kTile] = acc_y;
+            }
+            fence_proxy_async_global();  // later TMA re-fetches of this column see it
+            P.cur += 1;
         } else if (type == kRecSync) {
             walk_trace(v, tile, warp, lane, 0);
             PROF_MARK(8)
@@ -691,9 +759,11 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
     double* b_t = v.b + size_t(tile) * v.tstride + lane;
+    const double* lu_t = v.LU + size_t(tile) * v.tstride + lane;
     constexpr unsigned RB = kTile * 8;
     const unsigned R0 = smem_u32(P.R) + unsigned(lane) * 8u;
     unsigned blk = R0, e = R0;  // this step's block; its next U entry
+    const double *blk_g = lu_t, *e_g = lu_t;  // a global step's row block in the LU tape
     int ne = 0, brow = 0;
     double acc = 0.0;
     int32_t h = P.cur[0];  // header of the next record, loaded one record ahead
@@ -744,6 +814,27 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
             h = P.cur[0];
+        } else if (type == kRecStepG) {
+            // a row too long for the pool: its block read in place from the LU tape
+            ne = r[1];
+            blk_g = e_g = lu_t + size_t(r[2]) * kTile;
+            brow = r[3];
+            h = r[4];
+            P.cur += 4;
+            acc = blk_g[size_t(ne) * kTile];
+        } else if (type == kRecDepNG) {
+            const int n = (h >> 4) & 0xfffff;
+            h = r[1 + n];
+            for (int i = 0; i < n; ++i) {  // acc -= U(i,k) x_k, k descending, x_k from the b tape
+                acc = fma(-e_g[0], b_t[size_t(r[1 + i]) * kTile], acc);
+                e_g += kTile;
+            }
+            P.cur += 1 + n;
+        } else if (type == kRecEndG) {
+            h = r[1];
+            b_t[size_t(brow) * kTile] = acc / blk_g[size_t(ne + 1) * kTile];
+            fence_proxy_async_global();
+            P.cur += 1;
         } else if (type == kRecSync) {
             walk_trace(v, tile, warp, lane, 0);
             __syncthreads();  // phase boundary: every walker's columns are written and fenced

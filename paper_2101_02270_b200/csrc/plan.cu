@@ -309,6 +309,12 @@ struct gbnr_plan {
         v.jskip = static_cast<uint8_t*>(alloc(bpad));
         v.norm_bits = static_cast<unsigned long long*>(alloc(bpad * sizeof(unsigned long long)));
         v.tile_active = static_cast<int32_t*>(alloc(size_t(n_tiles) * sizeof(int32_t)));
+        // global scratch of the forward walks' global steps (columns too large for
+        // a walker's shared-memory pool), 8 walkers per tile
+        v.scratch_rows = std::max(wf.scratch_rows, wl.scratch_rows);
+        v.scratch = v.scratch_rows > 0
+                        ? static_cast<double*>(alloc(size_t(n_tiles) * 8 * size_t(v.scratch_rows) * gbnr::kTile * 8))
+                        : nullptr;
         v.active_count = static_cast<int32_t*>(alloc(128 * sizeof(int32_t)));
         cap_tiles = n_tiles;
     }
@@ -957,6 +963,8 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         if (const char* e = std::getenv("GBNR_UNIFIED")) wc.unified = std::atoi(e) != 0;  // 0: split plans
         if (const char* e = std::getenv("GBNR_SMEM_BUDGET")) wc.smem_budget = std::atoi(e);
         if (const char* e = std::getenv("GBNR_BALANCE")) wc.balance = std::atof(e);
+        // tests: also move blocks larger than this share of a walker's pool to global memory
+        if (const char* e = std::getenv("GBNR_GLOBAL_FRAC")) wc.global_frac = std::atof(e);
         if (const char* e = std::getenv("GBNR_LEVELS")) {  // e.g. "8,8,4,2,1"
             for (const char* q = e; *q;) {
                 wc.levels.push_back(std::atoi(q));
@@ -1103,11 +1111,12 @@ static const gbnr::WalkSet& pick_walk(const gbnr_plan* p, int32_t which) {
 int gbnr_walk_info(const gbnr_plan* p, int32_t which, int64_t* o) {
     return guarded([&] {
         const gbnr::WalkSet& w = pick_walk(p, which);
-        const int64_t vals[16] = {w.steps, w.walkers, w.phases, w.rows, w.page_words, w.pages,
+        const int64_t vals[20] = {w.steps, w.walkers, w.phases, w.rows, w.page_words, w.pages,
                                   w.barriers, int64_t(w.stream.size()), w.events, w.ring_dep_rows,
                                   w.fetched_rows, w.n_ops, w.n_copies, int64_t(w.smem_bytes()),
                                   w.parts.empty() ? 0 : w.parts[0].ring_rows,
-                                  w.parts.empty() ? 0 : w.parts[0].stage_rows};
+                                  w.parts.empty() ? 0 : w.parts[0].stage_rows,
+                                  w.global_steps, w.global_deps, w.scratch_rows, 0};
         std::memcpy(o, vals, sizeof vals);
     });
 }

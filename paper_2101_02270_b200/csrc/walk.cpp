@@ -27,13 +27,16 @@ struct DepIn {
     std::vector<WCopy> fetch;  // copies relative to a staging allocation
     int32_t fetch_rows = 0;
     int32_t stage_src = -1, stage_ysrc = -1;
-    WDep rec{};                // payload fields (kpos_fs, nrows, u0)
+    bool global = false;       // read from global memory, never staged
+    WDep rec{};                // payload fields (kpos_fs, nrows, u0, gslot, gnl)
 };
 struct StepIn {
     int32_t blk_rows = 0;
     std::vector<WCopy> copies;  // smem relative to the block
     std::vector<DepIn> deps;
-    WStep rec{};                // payload fields (len_dp, lslot, ut0, brow)
+    bool global = false;        // block in global memory (scratch / the LU tape)
+    int32_t global_rows = 0;    // forward: scratch rows a global block needs
+    WStep rec{};                // payload fields (len_dp, lslot, ut0, brow, gslot)
 };
 // A walker's program before planning: its steps and their payload arrays.
 struct Program {
@@ -103,7 +106,7 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         for (size_t d = 0; d < steps[t].deps.size(); ++d) {
             const DepIn& di = steps[t].deps[d];
             if (di.producer >= t) throw Error(3, "walk dependency is not earlier in the walk");
-            const bool res = di.producer >= 0 &&
+            const bool res = !di.global && di.producer >= 0 && !steps[di.producer].global &&
                              (ovw[di.producer] == kInf || t + cfg.headroom < ovw[di.producer]);
             resident[t][d] = res;
             if (res) lastuser[di.producer] = std::max(lastuser[di.producer], t);
@@ -184,6 +187,11 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         bool first_chunk = true;
         std::vector<size_t> chunk_deps;  // deps (indices into w.dep) of the open chunk
         auto close_chunk = [&]() {
+            if (ch.cps.empty() && first_chunk) {  // a global step with nothing staged: no op
+                rec.op = -1;
+                first_chunk = false;
+                return;
+            }
             const int32_t op = push_chunk(ch);
             if (first_chunk)
                 rec.op = op;
@@ -192,10 +200,21 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
             first_chunk = false;
             chunk_deps.clear();
         };
+        if (si.global) {
+            ++w.global_steps;
+            w.scratch_rows = std::max(w.scratch_rows, si.global_rows);
+        }
         for (size_t d = 0; d < si.deps.size(); ++d) {
             DepIn& di = si.deps[d];
             WDep dr = di.rec;
             dr.op = -1;
+            if (di.global) {
+                dr.src = dr.ysrc = -1;
+                dr.global = 1;
+                ++w.global_deps;
+                w.dep.push_back(dr);
+                continue;
+            }
             if (resident[t][d]) {
                 dr.src = di.ring_src >= 0 ? RB + ring[di.producer] + di.ring_src : -1;
                 dr.ysrc = di.ring_ysrc >= 0 ? RB + ring[di.producer] + di.ring_ysrc : -1;
@@ -256,6 +275,7 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         for (int32_t t = 0; t < T; ++t) {
             need[t] = std::max(need[t], ev_done(t));
             for (int32_t d = 0; d < w.step[t].ndep; ++d) {
+                if (steps[t].deps[d].global) continue;
                 const int32_t p = steps[t].deps[d].producer;
                 const int32_t g = resident[t][d] ? p : T + dep_tag0[t] + d;
                 need[g] = std::max(need[g], ev_dep(t, d));
@@ -292,11 +312,18 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         int32_t waited = -1;
         for (int32_t t = 0; t < T; ++t) {
             const WStep& st = w.step[t];
-            if (size_t(st.op) >= next) throw Error(3, "walk waits on an unissued op");
-            waited = std::max(waited, st.op);
-            expect(st.ring, t);
+            if (st.op >= 0 && size_t(st.op) >= next) throw Error(3, "walk waits on an unissued op");
+            if (!steps[t].global) {
+                if (st.op < 0) throw Error(3, "walk step block without an op");
+                waited = std::max(waited, st.op);
+                expect(st.ring, t);
+            }
             for (int32_t d = 0; d < st.ndep; ++d) {
                 const WDep& dr = w.dep[st.dep0 + d];
+                if (dr.global) {
+                    issue_upto(ev_dep(t, d));
+                    continue;
+                }
                 if (dr.op >= 0) {
                     if (size_t(dr.op) >= next) throw Error(3, "walk waits on an unissued fetch");
                     waited = std::max(waited, dr.op);
@@ -446,6 +473,27 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         int32_t need = 0;
         for (const DepIn& di : si.deps) need = std::max(need, di.fetch_rows);
         int32_t aft = -1, at = -1;
+        if (si.global) {  // nothing of the step in the pool (its deps are global too)
+            WStep grec = si.rec;
+            grec.ring = 0;
+            grec.op = -1;
+            grec.dep0 = static_cast<int32_t>(w.dep.size());
+            grec.ndep = static_cast<int32_t>(si.deps.size());
+            resident[t].assign(si.deps.size(), 0);
+            ++w.global_steps;
+            w.scratch_rows = std::max(w.scratch_rows, si.global_rows);
+            for (const DepIn& di : si.deps) {
+                if (!di.global) throw Error(3, "walk: a global step with a staged dependency");
+                WDep dr = di.rec;
+                dr.op = -1;
+                dr.src = dr.ysrc = -1;
+                dr.global = 1;
+                ++w.global_deps;
+                w.dep.push_back(dr);
+            }
+            w.step.push_back(grec);
+            continue;
+        }
         // producers this step could read from the pool (still intact)
         std::vector<int32_t> prods;
         for (const DepIn& di : si.deps)
@@ -505,6 +553,13 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
             WDep dr = di.rec;
             dr.op = -1;
             const int32_t pr = di.producer;
+            if (di.global) {
+                dr.src = dr.ysrc = -1;
+                dr.global = 1;
+                ++w.global_deps;
+                w.dep.push_back(dr);
+                continue;
+            }
             if (pr >= 0 && intact[pr] && (di.ring_src >= 0 || di.ring_ysrc >= 0)) {
                 resident[t][d] = 1;
                 for (Reg& r : live)
@@ -560,6 +615,7 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         for (int32_t t = 0; t < T; ++t) {
             need[t] = std::max(need[t], ev_done(t));
             for (int32_t d = 0; d < w.step[t].ndep; ++d) {
+                if (steps[t].deps[d].global) continue;
                 const int32_t p = steps[t].deps[d].producer;
                 const int32_t g = resident[t][d] ? p : T + dep_tag0[t] + d;
                 need[g] = std::max(need[g], ev_dep(t, d));
@@ -596,11 +652,18 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         int32_t waited = -1;
         for (int32_t t = 0; t < T; ++t) {
             const WStep& st = w.step[t];
-            if (size_t(st.op) >= next) throw Error(3, "walk waits on an unissued op");
-            waited = std::max(waited, st.op);
-            expect(st.ring, t);
+            if (st.op >= 0 && size_t(st.op) >= next) throw Error(3, "walk waits on an unissued op");
+            if (!steps[t].global) {
+                if (st.op < 0) throw Error(3, "walk step block without an op");
+                waited = std::max(waited, st.op);
+                expect(st.ring, t);
+            }
             for (int32_t d = 0; d < st.ndep; ++d) {
                 const WDep& dr = w.dep[st.dep0 + d];
+                if (dr.global) {
+                    issue_upto(ev_dep(t, d));
+                    continue;
+                }
                 if (dr.op >= 0) {
                     if (size_t(dr.op) >= next) throw Error(3, "walk waits on an unissued fetch");
                     waited = std::max(waited, dr.op);
@@ -644,7 +707,9 @@ struct Emitter {
 // pair when L(:,k) is row k+1 followed by exactly the rows of L(:,k+1) (so the
 // destinations of k are kpos(k+1) then those of k+1).  Every x element still
 // sees k's update before k+1's.
-bool pairable(const Walk& w, const WDep& e, const WDep& f, int64_t ev_e, int32_t op_base) {
+bool pairable(const Walk& w, const WDep& e, const WDep& f, int64_t ev_e, int32_t op_base, int32_t W) {
+    if (e.global || f.global) return false;
+    if (6 + ((f.nrows + 3) & ~3) / 2 > W - 1) return false;  // the pair record must fit a page
     if (e.nrows <= 0 || f.nrows < 0 || e.nrows != f.nrows + 1) return false;
     // a second wait is hoisted to the pair's start: its op must already be issued
     // there (issue event before e's) and its number must fit the record
@@ -693,16 +758,61 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
         }
     };
     auto opn = [&](int32_t op) { return op >= 0 ? op_base + op : -1; };
+    const int32_t W = em.W;
+    // a global-source dependency in records of at most W - 1 words: rows split
+    // into chunks (each re-reads the multiplier; only the first carries the FS role)
+    auto emit_dep_global = [&](const WDep& e, int32_t len) {
+        (void)len;
+        const int32_t max_rows = 2 * (W - 1 - 5);
+        int32_t q0 = 0;
+        bool first = true;
+        do {
+            const int32_t n = std::min(e.nrows - q0, max_rows);
+            const int32_t kpos = e.kpos_fs & 0xffff;
+            const int32_t fs = first ? int32_t(unsigned(e.kpos_fs) >> 16) : 0xffff;
+            std::vector<int32_t> rec{kRecDepG | ((first ? opn(e.op) + 1 : 0) << 4), kpos | (fs << 16), n,
+                                     e.gslot + q0, e.gnl - q0};
+            for (int32_t r = 0; r < n; r += 2) {
+                const int32_t a = int32_t(w.dst[e.u0 + q0 + r]);
+                const int32_t b = r + 1 < n ? int32_t(w.dst[e.u0 + q0 + r + 1]) : 0;
+                rec.push_back(a | (b << 16));
+            }
+            em.emit(rec);
+            q0 += n;
+            first = false;
+        } while (q0 < e.nrows);
+    };
     issue_upto(-1);
     int64_t ev = 0;
     for (const WStep& s : w.step) {
         if (forward) {
             const int32_t len = s.len_dp & 0xffff, dp = s.len_dp >> 16;
+            if (s.global) {
+                em.emit({kRecStepG | (s.ndep << 4), len | (dp << 16), s.gslot, s.lslot, s.brow});
+                for (int32_t d = 0; d < s.ndep; ++d) {
+                    emit_dep_global(w.dep[s.dep0 + d], len);
+                    issue_upto(ev++);
+                }
+                for (int32_t z0 = 0; z0 < dp; z0 += W - 3) {  // the U part -> its row-major slots
+                    const int32_t cnt = std::min(dp - z0, W - 3);
+                    std::vector<int32_t> rec{kRecEndU | (cnt << 4), z0};
+                    for (int32_t z = z0; z < z0 + cnt; ++z) rec.push_back(w.ut[s.ut0 + z]);
+                    em.emit(rec);
+                }
+                em.emit({kRecEndG});
+                issue_upto(ev++);
+                continue;
+            }
             em.emit({kRecStep | (s.ndep << 4), s.ring | (len << 16), dp, s.lslot, s.brow, opn(s.op)});
             for (int32_t d = 0; d < s.ndep; ++d) {
                 const WDep& e = w.dep[s.dep0 + d];
+                if (e.global) {
+                    emit_dep_global(e, len);
+                    issue_upto(ev++);
+                    continue;
+                }
                 if (e.src >= 65536 || e.nrows >= 65536) throw Error(3, "walk dependency too large to encode");
-                if (d + 1 < s.ndep && pairable(w, e, w.dep[s.dep0 + d + 1], ev, op_base)) {
+                if (d + 1 < s.ndep && pairable(w, e, w.dep[s.dep0 + d + 1], ev, op_base, W)) {
                     // supernode pair: dep k's rows are row k+1 (x position kpos2) then
                     // exactly dep k+1's rows; one pass applies both in order
                     const WDep& f = w.dep[s.dep0 + d + 1];
@@ -735,6 +845,19 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
             std::vector<int32_t> end{kRecEnd | (dp << 4)};
             for (int32_t z = 0; z < dp; ++z) end.push_back(w.ut[s.ut0 + z]);
             em.emit(end);
+            issue_upto(ev++);
+        } else if (s.global) {
+            // a row block read in place from the LU tape, x_k from the b tape
+            em.emit({kRecStepG | (s.ndep << 4), s.len_dp, s.gslot, s.brow});
+            for (int32_t d = 0; d < s.ndep;) {
+                const int32_t n = std::min(s.ndep - d, W - 2);
+                std::vector<int32_t> rec{kRecDepNG | (n << 4)};
+                for (int32_t i = 0; i < n; ++i) rec.push_back(w.dep[s.dep0 + d + i].gslot);
+                em.emit(rec);
+                for (int32_t i = 0; i < n; ++i) issue_upto(ev++);
+                d += n;
+            }
+            em.emit({kRecEndG});
             issue_upto(ev++);
         } else {
             em.emit({kRecStep | (s.ndep << 4), s.ring | (s.len_dp << 16), 0, s.lslot, s.brow, opn(s.op)});
@@ -781,7 +904,8 @@ Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
         longest = std::max(longest, 2 + (s.dpos[k] - s.cp[k]));           // END
         longest = std::max(longest, 6 + (s.cp[k + 1] - s.dpos[k]) / 2);  // DEP (rows padded to 4)
     }
-    const int32_t W = std::max(cfg.page_words, 4 * ((longest + 1 + 3) / 4));
+    // longer records than a page of kMaxPageWords go global (their forms split)
+    const int32_t W = std::min(std::max(cfg.page_words, 4 * ((longest + 1 + 3) / 4)), kMaxPageWords);
     const int64_t fixed = int64_t(walkers) * (int64_t(cfg.pages) * W * 4 + int64_t(cfg.barriers + cfg.pages) * 8);
     const int64_t rows = (int64_t(cfg.smem_budget) - fixed) / 256;
     return Geometry{W, int32_t(std::max<int64_t>(rows, 0))};
@@ -797,6 +921,62 @@ void split_share(const WalkConfig& cfg, int32_t share, int32_t& ring, int32_t& s
 struct Phase {
     std::vector<std::vector<int32_t>> lists;  // per walker: steps (column / row ids) in walk order
 };
+
+// Global-memory fallback: blocks larger than gb rows (and every dependency of
+// such a step) and fetches larger than gf rows are read from global memory
+// instead of staged; so are records that would not fit a program page.  The
+// per-element operation order is unchanged, only where the operands live.
+void apply_global(Program& pr, int32_t gb, int32_t gf, int32_t W, bool forward) {
+    for (StepIn& si : pr.steps) {
+        const int32_t dp = forward ? (si.rec.len_dp >> 16) : 0;
+        if (si.blk_rows > gb || (forward && 1 + dp > W - 1)) {
+            si.global = true;
+            si.global_rows = forward ? si.blk_rows : 0;
+            si.blk_rows = 0;
+            si.copies.clear();
+            si.rec.global = 1;
+        }
+        for (DepIn& di : si.deps) {
+            const int32_t n4 = (di.rec.nrows + 3) & ~3;
+            if (si.global || di.fetch_rows > gf || (forward && 4 + n4 / 2 > W - 1)) {
+                di.global = true;
+                di.fetch.clear();
+                di.fetch_rows = 0;
+                di.ring_src = di.ring_ysrc = -1;
+                di.rec.global = 1;
+            }
+        }
+    }
+}
+
+// Plan one walker's program: shared memory only if it fits, else with the
+// largest blocks / fetches moved to global memory, halving the limits until the
+// plan is feasible (everything global always is: no copies at all).
+Walk plan_walker(const Program& base, const PlanCfg& pc, const WalkConfig& cfg, int32_t W, bool forward) {
+    const int32_t PR = pc.ring_rows + pc.stage_rows;
+    int32_t gb = kInf, gf = kInf;
+    if (cfg.global_frac > 0.0) {
+        gb = std::max(1, int32_t(cfg.global_frac * PR));
+        gf = std::max(1, gb / 2);
+    }
+    for (;;) {
+        Program pr = base;
+        apply_global(pr, gb, gf, W, forward);
+        if (cfg.unified) {
+            try {
+                return plan_unified(pr.steps, pc);
+            } catch (const Error&) {  // infeasible: the split ring / staging plan
+            }
+        }
+        try {
+            return plan(pr.steps, pc);
+        } catch (const Error&) {
+            if (gb == 0) throw;
+        }
+        gb = gb == kInf ? PR / 2 : gb / 2;
+        gf = gb / 2;
+    }
+}
 
 // Plan and encode every (phase, walker) program of a walk set.
 template <class MakeProgram>
@@ -829,15 +1009,7 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
                 pc.headroom = cfg.headroom;
                 pc.max_copies = (g.W - 5) / 2;
                 Program pr = make_program(list);
-                bool done = false;
-                if (cfg.unified) {
-                    try {
-                        part = plan_unified(pr.steps, pc);
-                        done = true;
-                    } catch (const Error&) {  // infeasible: the split ring / staging plan
-                    }
-                }
-                if (!done) part = plan(pr.steps, pc);
+                part = plan_walker(pr, pc, cfg, g.W, forward);
                 part.dst = std::move(pr.dst);
                 part.ut = std::move(pr.ut);
                 encode(em[w], part, forward, op_base[w]);
@@ -850,6 +1022,9 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
             ws.fetched_rows += part.fetched_rows;
             ws.n_ops += int64_t(part.op.size());
             ws.n_copies += int64_t(part.copies.size());
+            ws.global_steps += part.global_steps;
+            ws.global_deps += part.global_deps;
+            ws.scratch_rows = std::max(ws.scratch_rows, part.scratch_rows);
             ws.parts.push_back(std::move(part));
         }
         if (ph + 1 < phases.size())
@@ -1081,6 +1256,7 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
             si.rec.lslot = lay.lslot[m];
             si.rec.ut0 = static_cast<int32_t>(pr.ut.size());
             si.rec.brow = lay.ucrs0[m + 1] - 2;  // y_m, U(m,m) of the backward block
+            si.rec.gslot = a_slot(c0, m);        // the column in the A tape (global form)
             for (int32_t z = c0; z < s.dpos[m]; ++z) pr.ut.push_back(lay.tape_of_ccs[z]);
             for (int32_t z = c0; z < c0 + len; ++z) posmap[s.ri[z]] = z - c0;
             std::vector<int32_t> ks;
@@ -1114,6 +1290,8 @@ WalkSet build_forward_walk(const Symbolic& s, const LuLayout& lay, bool with_fs,
                 const int32_t klen = s.cp[k + 1] - s.cp[k], kdp = s.dpos[k] - s.cp[k];
                 di.ring_src = kdp + 1;
                 di.ring_ysrc = with_fs ? klen : -1;
+                di.rec.gslot = lay.lslot[k];  // L(:,k) then y_k in the LU tape (global form)
+                di.rec.gnl = nl;
                 di.fetch.push_back(copy(kTapeLU, lay.lslot[k], with_fs ? nl + 1 : nl, 0));  // L rows (+ y_k)
                 di.stage_src = 0;
                 di.fetch_rows = nl;
@@ -1159,11 +1337,13 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
             si.rec.len_dp = ne;
             si.rec.lslot = lay.lslot[i];
             si.rec.brow = nJ - 1 - i;  // x_i's b-tape row: descending k re-fetches ascending rows
+            si.rec.gslot = lay.ucrs0[i];  // the row block in the LU tape (global form)
             for (int32_t k : urow[i]) {
                 DepIn di;
                 di.producer = local[k] >= 0 && local[k] < int32_t(t) ? local[k] : -1;
                 di.ring_ysrc = static_cast<int32_t>(urow[k].size());
                 di.fetch.push_back(copy(kTapeB, nJ - 1 - k, 1, 0));
+                di.rec.gslot = nJ - 1 - k;  // x_k's b-tape row (global form)
                 di.stage_ysrc = 0;
                 di.fetch_rows = 1;
                 si.deps.push_back(std::move(di));

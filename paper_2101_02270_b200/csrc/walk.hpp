@@ -34,7 +34,7 @@ namespace gbnr {
 
 enum : int32_t { kTapeA = 0, kTapeLU = 1, kTapeB = 2 };
 
-// One step (LU column / BS row).  32 B, two uniform int4 loads.
+// One step (LU column / BS row).
 struct WStep {
     int32_t ring;    // smem row of the step's block
     int32_t len_dp;  // forward: len | dp << 16; backward: number of U entries
@@ -44,6 +44,8 @@ struct WStep {
     int32_t ut0;     // forward: first index into the U-scatter list (dp entries)
     int32_t op;      // op carrying the block
     int32_t brow;    // b-tape row of the step (LU row / column index)
+    int32_t global = 0;  // block in global memory (too large for the walker's pool)
+    int32_t gslot = 0;   // global step: A-tape slot of the column (fwd) / LU-tape slot of the row (bwd)
 };
 // One dependency of a step.  32 B.
 struct WDep {
@@ -53,7 +55,9 @@ struct WDep {
     int32_t ysrc;     // smem row of y_k (forward) / x_k (backward)
     int32_t u0;       // forward: first destination record
     int32_t op;       // op to wait on, -1 = resident in the ring
-    int32_t pad0, pad1;
+    int32_t global;   // source read from global memory (too large to stage)
+    int32_t gslot;    // global source: LU-tape slot of L(:,k) (fwd) / b-tape row of x_k (bwd)
+    int32_t gnl;      // global source (fwd): rows of L(:,k) (y_k follows them)
 };
 // One TMA bulk copy: nrows 256 B rows of tape `tape` from slot/row `slot`.
 struct WCopy {
@@ -83,6 +87,10 @@ struct WalkConfig {
     double stage_frac = 0.3;      // staging share of a walker's rows (split plan; the
                                   // subtree partition sizes columns against it too)
     double stage_frac_up = 0.3;   // staging share above level 0 (< 0: stage_frac)
+    double global_frac = 0.0;     // > 0: also stage in global memory every block larger than
+                                  // this share of the pool and every fetch larger than half
+                                  // of it (tests; columns that cannot be planned in shared
+                                  // memory go global regardless)
     std::vector<int32_t> levels;  // walkers per level (empty: walkers, walkers/2, ..., 1)
     bool unified = true;          // blocks and fetches share one pool (plan_unified;
                                   // the split ring / staging plan where it is infeasible)
@@ -109,11 +117,28 @@ enum : int32_t {
     // bwd: n consecutive dependencies, only the first may wait:
     // 9 | (op + 1) << 4, n, ysrc u16 pairs
     kRecDepN = 9,
+    // Global-memory forms for columns / rows too large for a walker's pool (the
+    // same operation order per element, data in the tile's global scratch / tapes):
+    // fwd: 10 | ndep << 4, len | dp << 16, A slot, lslot, brow       (column -> scratch)
+    // bwd: 10 | ndep << 4, ne, LU slot of the row block, brow
+    kRecStepG = 10,
+    // fwd: 11 | (op + 1) << 4, kpos_fs, nrows, src, nl, dst u16 pairs (padded to 2);
+    //      src < 0: L(:,k) at LU-tape slot -src-1 (y_k nl rows further), else a shared
+    //      row (y_k at src + nl); x = the step's block (shared or scratch).  A dependency
+    //      may continue in further records (kpos only, no FS role).
+    kRecDepG = 11,
+    kRecEndG = 12,   // fwd: 12 (normalise the L part, flag, y); bwd: 12
+    // fwd: 13 | cnt << 4, z0, U-CRS slots [cnt]: scatter U entries z0.. of a global step
+    kRecEndU = 13,
+    // bwd: 14 | n << 4, b-tape rows of x_k [n] (global row block, x_k from the b tape)
+    kRecDepNG = 14,
 };
+constexpr int32_t kMaxPageWords = 256;  // longer records are split (global forms)
 
 // One verified single-walker program (one walker in one phase).
 struct Walk {
     int32_t ring_base = 0, ring_rows = 0, stage_rows = 0, barriers = 0, n_steps = 0;
+    int32_t global_steps = 0, global_deps = 0, scratch_rows = 0;
     std::vector<WStep> step;
     std::vector<WDep> dep;
     std::vector<uint16_t> dst;  // forward: destination position per applied L row
@@ -131,6 +156,8 @@ struct WalkSet {
     std::vector<int32_t> wpage0;    // [walkers + 1] first page of each walker
     std::vector<int32_t> owner;     // column / row -> level * 16 + walker
     int64_t steps = 0, events = 0, ring_dep_rows = 0, fetched_rows = 0, n_ops = 0, n_copies = 0;
+    int64_t global_steps = 0, global_deps = 0;
+    int32_t scratch_rows = 0;       // per-tile global scratch rows (forward global steps)
     size_t smem_bytes() const {
         return size_t(rows) * 256 + size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages) * 8);
     }

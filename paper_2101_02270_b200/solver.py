@@ -361,10 +361,11 @@ class NrPlan:
 
     WALK_KEYS = ("steps", "walkers", "phases", "rows", "page_words", "pages", "barriers",
                  "stream_words", "events", "ring_dep_rows", "fetched_rows", "n_ops", "n_copies",
-                 "smem_bytes", "ring_rows", "stage_rows")
+                 "smem_bytes", "ring_rows", "stage_rows", "global_steps", "global_deps",
+                 "scratch_rows")
 
     def walk_info(self, which: int) -> dict:
-        out = np.zeros(17, np.int64)
+        out = np.zeros(20, np.int64)
         _check(lib().gbnr_walk_info(self.h, int(which), out))
         return {k: int(out[i]) for i, k in enumerate(self.WALK_KEYS)}
 

@@ -329,3 +329,55 @@ def test_nonfinite_task_isolated():
     _compare(r, o)
     assert r.status[10] != 0 and r.status[41] != 0
     assert (np.delete(r.status, [10, 41]) == 0).all()
+
+
+def _setup_case(gc, **opts):
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    vm0, va0 = gc.v_start()
+    plan = S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, device=0, **opts)
+    oplan = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
+    return plan, oplan, vm0, va0
+
+
+@pytest.mark.parametrize("name,extra,T", [("synth9241x", 0, 64), ("synth9241", 50, 64), ("synth9241", 100, 64),
+                                          ("synth9241", 200, 64), ("synth9241", 1000, 32)])
+def test_dense_grids_plan_and_match_oracle(name, extra, T):
+    """execute_schedule for ANY frozen pattern: denser grids whose
+    LU columns outgrow a walker's shared-memory pool (synth9241x: 250 long tie
+    lines, nnzLU 341k, max_col 462; synth9241 + 50..1000 random branches, up to
+    nnzLU 1.6M, max_col 1321) plan -- the too-large blocks and fetches run from
+    global memory -- and solve bit-identically to the oracle."""
+    from gen_cases import add_random_branches
+    gc = load_case(util.case_path(name))
+    if extra:
+        gc = add_random_branches(gc, extra)
+    plan, oplan, vm0, va0 = _setup_case(gc)
+    p0, q0 = montecarlo(gc, T)
+    r = plan.solve(p0, q0, vm0, va0, n_tasks=T)
+    o = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T)
+    assert (r.status == 0).mean() > 0.9
+    _compare(r, o)
+    if extra >= 100 or name == "synth9241x":
+        assert plan.walk_info(0)["global_steps"] > 0
+
+
+@pytest.mark.parametrize("frac", ["0.3", "0.05"])
+def test_global_forms_match_oracle(frac, monkeypatch):
+    """Blocks / fetches forced into global memory on a grid that fits (the
+    fallback's code paths, GBNR_GLOBAL_FRAC): NR solve and the LU-only
+    refactorization stay bit-identical to the oracle."""
+    monkeypatch.setenv("GBNR_GLOBAL_FRAC", frac)
+    gc = load_case(util.case_path("synth2383"))
+    plan, oplan, vm0, va0 = _setup_case(gc)
+    assert plan.walk_info(0)["global_steps"] > 0 and plan.walk_info(2)["global_steps"] > 0
+    T = 100
+    p0, q0 = montecarlo(gc, T)
+    _compare(plan.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
+    rng = np.random.default_rng(3)
+    vm = vm0[:, None] * (1 + 0.02 * rng.standard_normal((gc.n_bus, 40)))
+    va = va0[:, None] + 0.05 * rng.standard_normal((gc.n_bus, 40))
+    plan.stage(p0[:, :40], q0[:, :40], vm, va)
+    lu, flags, _ = plan.refactor(reps=2)
+    olu, oflags = oplan.refactor(vm, va)
+    np.testing.assert_array_equal(flags, oflags)
+    np.testing.assert_array_equal(lu, olu)

@@ -83,6 +83,7 @@ def sequential(ex, A, b):
 
 
 REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC, REC_DEP2, REC_DEPN = 1, 2, 3, 4, 5, 6, 7, 8, 9
+REC_STEPG, REC_DEPG, REC_ENDG, REC_ENDU, REC_DEPNG = 10, 11, 12, 13, 14
 
 
 class Machine:
@@ -168,6 +169,45 @@ def replay_forward(w, A_tape, nrows, fs=True):
     def step(M, r, t, S):
         R = M.R
         h = int(r[0])
+        if t == REC_STEPG:  # column too large for the pool: its A rows + F in a global scratch
+            ln, dp = int(r[1]) & 0xFFFF, int(r[1]) >> 16
+            a0 = int(r[2])
+            S.update(ring=None, ln=ln, dp=dp, lslot=int(r[3]), uy=int(r[4]), gmax=0.0)
+            S["x"] = A_tape[a0:a0 + ln + 1].copy()  # the scratch (the A tape stays intact)
+            S["acc"] = S["x"][ln].copy() if fs else None
+            return 5
+        if t == REC_DEPG:  # dependency read from the LU tape
+            op = (h >> 4) - 1
+            if op >= 0:
+                M.wait(op)
+            kpos_fs, n, slot, nl = int(r[1]), int(r[2]), int(r[3]), int(r[4])
+            x = S["x"]
+            if n > 0:
+                mult = x[kpos_fs & 0xFFFF].copy()
+                for q in range(n):
+                    wq = int(r[5 + q // 2])
+                    d = (wq >> 16) & 0xFFFF if q & 1 else wq & 0xFFFF
+                    x[d] = x[d] - mult * LU[slot + q]
+            fsp = (kpos_fs >> 16) & 0xFFFF
+            if fs and fsp != 0xFFFF:
+                S["acc"] = S["acc"] - LU[slot + fsp] * LU[slot + nl]
+            return 5 + (n + 1) // 2
+        if t == REC_ENDU:
+            cnt, z0 = (h >> 4) & 0xFFFFF, int(r[1])
+            for i in range(cnt):
+                LU[int(r[2 + i])] = S["x"][z0 + i]
+            return 2 + cnt
+        if t == REC_ENDG:
+            x, dp, ln, lslot = S["x"], S["dp"], S["ln"], S["lslot"]
+            piv = x[dp].copy()
+            inv = 1.0 / piv
+            for z in range(dp + 1, ln):
+                LU[lslot + z - dp - 1] = x[z] * inv
+            LU[S["uy"] + 1] = piv
+            if fs:
+                LU[lslot + ln - dp - 1] = S["acc"]
+                LU[S["uy"]] = S["acc"]
+            return 1
         if t == REC_DEP:
             op = (h >> 4) - 1
             kpos_fs, nrows, src, ysrc = int(r[1]), int(r[2]) & 0xFFFF, (int(r[2]) >> 16) & 0xFFFF, int(r[3])
@@ -240,6 +280,20 @@ def replay_backward(w, LU, b_tape):
     def step(M, r, t, S):
         R = M.R
         h = int(r[0])
+        if t == REC_STEPG:  # row block read in place from the LU tape
+            ne, slot = int(r[1]), int(r[2])
+            S.update(ring=None, ne=ne, brow=int(r[3]), gslot=slot, e=0)
+            S["acc"] = LU[slot + ne].copy()
+            return 4
+        if t == REC_DEPNG:
+            n = (h >> 4) & 0xFFFFF
+            for i in range(n):
+                S["acc"] = S["acc"] - LU[S["gslot"] + S["e"]] * b_tape[int(r[1 + i])]
+                S["e"] += 1
+            return 1 + n
+        if t == REC_ENDG:
+            b_tape[S["brow"]] = S["acc"] / LU[S["gslot"] + S["ne"] + 1]
+            return 1
         if t == REC_DEPN:
             op = (h >> 4) - 1
             if op >= 0:
@@ -280,6 +334,30 @@ def test_walk_replay_bitwise(name, opts, unified, monkeypatch):
     monkeypatch.setenv("GBNR_UNIFIED", unified)
     gc = load_case(util.case_path(name))
     plan = S.NrPlan.from_case(gc, device=-1, **opts)
+    check_replay(gc, plan)
+
+
+@pytest.mark.parametrize("name,frac,opts", [("synth118", "0.1", {}), ("synth300", "0.05", {}),
+                                            ("synth300", "0.2", dict(walkers=2)),
+                                            ("synth300", "0.001", dict(walkers=1)),
+                                            ("synth2383", "0.08", {})])
+@pytest.mark.parametrize("unified", ["1", "0"])
+def test_walk_replay_global_forms(name, frac, opts, unified, monkeypatch):
+    """Blocks / fetches moved to global memory (the fallback for columns too large
+    for a walker's shared-memory pool, forced here on small grids by
+    GBNR_GLOBAL_FRAC) keep every element's operation order: bitwise equal."""
+    monkeypatch.setenv("GBNR_UNIFIED", unified)
+    monkeypatch.setenv("GBNR_GLOBAL_FRAC", frac)
+    gc = load_case(util.case_path(name))
+    plan = S.NrPlan.from_case(gc, device=-1, **opts)
+    infos = [plan.walk_info(w) for w in (0, 1, 2)]
+    assert infos[0]["global_steps"] > 0 and infos[0]["scratch_rows"] > 0
+    if frac == "0.001":  # everything global: no copies at all
+        assert all(i["global_steps"] == i["steps"] and i["n_copies"] == 0 for i in infos)
+    check_replay(gc, plan)
+
+
+def check_replay(gc, plan):
     ex, A, b = jacobian_tape(gc, plan)
     lu_ref, y_ref, x_ref = sequential(ex, A, b)
     wf, wl, wb = plan.walk_export(0), plan.walk_export(1), plan.walk_export(2)
