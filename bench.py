@@ -122,79 +122,105 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
-def lu_traffic_per_task():
-    """DRAM bytes per task per LU launch from the committed ncu capture, or None."""
+def ncu_lu_summary():
+    """The LU walk's ncu figures from the committed capture (profiles/ncu_summary.json):
+    DRAM bytes per task per launch, DRAM throughput fraction, FP64 pipe %."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             d = json.load(fh)
-        return float(d["lu_kernel"]["dram_bytes_per_task"])
+        lu = d["lu_kernel"]
+        return {"dram_bytes_per_task": float(lu["dram_bytes_per_task"]),
+                "dram_frac": lu.get("dram_frac"), "fp64_pipe_pct": lu.get("fp64_pipe_pct"),
+                "source": d.get("source")}
     except Exception:
-        return None
+        return {}
 
 
-def cpu_baseline(gc, case, p_fn, budget_s, threads):
-    """Oracle (CPU restatement of the reference path) on a bounded sample."""
+def host_info():
+    """Host cores and CPU model of the box (reported beside every CPU number)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def workload_config(case, nJ, T, world):
+    """The `config` object of both arms (same workload, same keys)."""
+    return {"workload": f"{case} (case9241pegase-sized synthetic grid, {nJ}-dim Jacobian), "
+                        "Monte-Carlo loads U(0.8,1.2)",
+            "case": case, "tasks_per_gpu": T, "global_batch": T * world,
+            "parallelism": f"scenario-sharded x{world}, no collective", "tol": 1e-8, "max_iter": 10}
+
+
+def oracle_plan(gc):
+    """The CPU restatement (test oracle) on the case's representative task; Ybus
+    from the oracle's own build_ybus (nothing of the product on this path)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
-    from paper_2101_02270_b200 import solver as S
-    ip, ix, _, yr, yi = S.build_ybus(gc)
+    orc = po.Oracle()
+    ip, ix, _, yr, yi = orc.build_ybus(gc)
     vm0, va0 = gc.v_start()
-    oplan = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
-    chunk = max(64 * threads, 256)  # large calls: the pool start-up is amortised as in --impl reference
+    return orc.plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0), vm0, va0
+
+
+def cpu_baseline(gc, case, p0, q0, budget_s, threads):
+    """Oracle (CPU restatement of the reference path) on the SAME pre-generated
+    batch the GPU arm solves: whole-batch calls repeated until budget_s, input
+    generation outside the timed region (as in --impl reference)."""
+    oplan, vm0, va0 = oracle_plan(gc)
+    T = p0.shape[1]
     done = conv = 0
     t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        p0, q0 = p_fn(done, chunk)
-        r = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=chunk, n_threads=threads)
+    while True:
+        r = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T, n_threads=threads)
         conv += int((r["status"] == 0).sum())
-        done += chunk
+        done += T
+        if time.perf_counter() - t0 >= budget_s:
+            break
     dt = time.perf_counter() - t0
     return {"value": conv / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{done} tasks (ids 0..{done - 1}) of the {case} Monte-Carlo workload, "
-                      f"{dt:.1f} s on {threads} threads"}
+            "sample": f"{done // T} x the GPU arm's batch ({T} tasks, ids 0..{T - 1}) of the {case} "
+                      f"Monte-Carlo workload, inputs pre-generated, {dt:.1f} s on {threads} threads",
+            **host_info()}
 
 
 def run_reference(a, rk):
-    """--impl reference: the oracle port with all host threads, rank 0 only."""
+    """--impl reference: the oracle port with all host threads on the same
+    workload as our arm (same case, same tasks per step, same scenario ids),
+    rank 0 only.  Inputs are generated once, before warm-up."""
     from paper_2101_02270_b200.case import load_case
     from paper_2101_02270_b200.scenarios import montecarlo
     if not rk.is_root:
         return None
     gc = load_case(os.path.join(ROOT, "cases", a.case + ".m"))
     threads = os.cpu_count() or 1
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle as po
-    from paper_2101_02270_b200 import solver as S
-    ip, ix, _, yr, yi = S.build_ybus(gc)
-    vm0, va0 = gc.v_start()
-    oplan = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
-    # one step = a bounded sample sized to ~cpu-seconds/steps of work
-    probe = max(4 * threads, 32)
-    p0, q0 = montecarlo(gc, probe)
-    t0 = time.perf_counter()
-    oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=probe, n_threads=threads)
-    rate = probe / (time.perf_counter() - t0)
-    per_step = int(max(probe, min(a.tasks, rate * max(2.0, 60.0 / max(a.steps + a.warmup, 1)))))
-    per_step = (per_step + threads - 1) // threads * threads
-    p0, q0 = montecarlo(gc, per_step)
+    oplan, vm0, va0 = oracle_plan(gc)
+    T = a.tasks
+    p0, q0 = montecarlo(gc, T)
     for _ in range(a.warmup):
-        oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=per_step, n_threads=threads)
+        oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T, n_threads=threads)
     conv = 0
     t0 = time.perf_counter()
     for _ in range(a.steps):
-        r = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=per_step, n_threads=threads)
+        r = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T, n_threads=threads)
         conv += int((r["status"] == 0).sum())
     dt = time.perf_counter() - t0
     value = conv / dt
-    sample = f"{per_step} tasks (ids 0..{per_step - 1}) per step of the {a.case} workload"
+    sample = (f"the full {T}-task batch (ids 0..{T - 1}) of the {a.case} workload per step, "
+              "inputs pre-generated")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{a.case} Monte-Carlo load scenarios, CPU oracle port",
-                       "case": a.case, "tasks_per_step": per_step, "threads": threads},
+            "config": {**workload_config(a.case, oplan.stats()["nJ"], T, 1), "same_config": True,
+                       "threads": threads},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, **host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -224,7 +250,10 @@ def main():
     else:
         task0, T = rk.rank * a.tasks, a.tasks
         scaling = "weak"
-    plan = S.NrPlan.from_case(gc, device=dev, profile=1)
+    torch.cuda.init()
+    i0 = time.perf_counter()
+    plan = S.NrPlan.from_case(gc, device=dev, profile=1)  # one-time init
+    init_ms = (time.perf_counter() - i0) * 1e3
     st = plan.stats()
     vm0, va0 = gc.v_start()
     p0, q0 = montecarlo(gc, T, task0=task0)
@@ -235,7 +264,7 @@ def main():
     dist.barrier(rk)
     torch.cuda.synchronize(dev)
     dev_ms = lu_ms = 0.0
-    conv = launches = lu_launches = lu_tasks = 0
+    conv = launches = lu_launches = lu_tasks = npm_tasks = 0
     iters = []
     with ClockSampler(dev) as clk:
         w0 = time.perf_counter()
@@ -247,6 +276,7 @@ def main():
             conv += tm["converged"]
             lu_launches += tm["lu_launches"]
             lu_tasks += tm["lu_task_launches"]
+            npm_tasks += tm["tasks"] + tm["lu_task_launches"]  # the V0 check + one per update
             launches += tm["kernels"]
             iters.append(tm["iterations"])
         wall = time.perf_counter() - w0
@@ -297,7 +327,15 @@ def main():
     b_lu_task = 8 * (2 * st["nnzLU"] + st["D"]) + 16 * st["nJ"]
     peak, peak_kind = measured_peaks()
     achieved = b_lu_task * lu_tasks / (lu_ms / 1e3) / 1e9 if lu_ms > 0 else None
-    tr = lu_traffic_per_task()
+    ncu = ncu_lu_summary()
+    tr = ncu.get("dram_bytes_per_task")
+    # whole solve: every kernel's algorithmic bytes (DESIGN.md §5 table) over the
+    # whole device time -- mismatch sweeps for every check, the rest per LU launch
+    n_, nJ_, zLU_, zL_ = gc.n_bus, st["nJ"], st["nnzLU"], st["nnzL"]
+    b_npm = 32 * n_ + 8 * nJ_
+    b_iter = (16 * n_ + 8 * zLU_) + b_lu_task + (8 * (zLU_ - zL_) + 16 * nJ_) + (8 * nJ_ + 32 * n_)
+    solve_bytes = b_npm * npm_tasks + b_iter * lu_tasks
+    solve_gbs = solve_bytes / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
             "traffic": tr * (lu_tasks / max(lu_launches, 1)) if tr else None,
@@ -307,27 +345,32 @@ def main():
             # also against the nominal HBM3e figure (7.7 TB/s HGX B200)
             "peak_nominal": 7700.0, "frac_nominal": achieved / 7700.0 if achieved else None,
             "lu_ms_per_launch": lu_ms / max(lu_launches, 1),
-            "lu_share_of_step": lu_ms / dev_ms if dev_ms else None}
+            "lu_share_of_step": lu_ms / dev_ms if dev_ms else None,
+            # ncu (profiles/ncu_summary.json): DRAM bytes actually moved by one LU launch
+            # and its rate over the ncu-timed launch, FP64 pipe utilisation
+            "ncu_dram_frac": ncu.get("dram_frac"), "ncu_fp64_pipe_pct": ncu.get("fp64_pipe_pct"),
+            "ncu_source": ncu.get("source"),
+            "whole_solve": {"achieved": solve_gbs, "peak": peak, "unit": "GB/s",
+                            "frac": solve_gbs / peak if solve_gbs else None,
+                            "bytes_per_task_iteration": b_iter + b_npm,
+                            "note": "algorithmic bytes of every kernel (DESIGN.md §5) over the whole "
+                                    "device time of the solve"}}
 
     cpu = None
     if rk.is_root and rk.world == 1 and not a.no_cpu:
-        cpu = cpu_baseline(gc, a.case, lambda t0_, k: montecarlo(gc, k, task0=t0_),
-                           a.cpu_seconds, os.cpu_count() or 1)
+        cpu = cpu_baseline(gc, a.case, p0, q0, a.cpu_seconds, os.cpu_count() or 1)
 
     if rk.is_root:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world,
                "steps": a.steps, "warmup": a.warmup, "ms_per_step": job_ms / a.steps,
                "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
                "dtype": "f64", "data": "synthetic",
-               "config": {"workload": f"{a.case} (case9241pegase-sized synthetic grid, "
-                                      f"{st['nJ']}-dim Jacobian), Monte-Carlo loads U(0.8,1.2)",
-                          "case": a.case, "tasks_per_gpu": T, "global_batch": T * rk.world,
-                          "parallelism": f"scenario-sharded x{rk.world}, no collective",
-                          "tol": 1e-8, "max_iter": 10,
+               "config": {**workload_config(a.case, st["nJ"], T, rk.world),
                           "newton_iterations_per_step": iters,
                           "l2": "inputs larger than L2 (LU tape "
                                 f"{st['nnzLU'] * 8 * T / 1e9:.1f} GB per GPU)",
                           "wall_s_timed": wall},
+               "init_ms": init_ms,
                "clocks": clk.summary(),
                "e2e": {"value": e2e_conv / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "steps": K, "jobs_timed": 3, "statistic": "median",

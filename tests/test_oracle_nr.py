@@ -49,7 +49,8 @@ def test_case14_published_solution():
     np.testing.assert_allclose(flat["vm"], r["vm"], atol=1e-8)
 
 
-@pytest.mark.parametrize("name,T", [("case14", 40), ("synth118", 12), ("synth300", 8)])
+@pytest.mark.parametrize("name,T", [("case14", 40), ("synth118", 12), ("synth300", 8),
+                                    ("synth2383", 6), ("synth9241", 4)])
 def test_matches_scipy_newtonpf(name, T):
     gc, plan, Y, vm0, va0 = setup(name)
     p0, q0 = montecarlo(gc, T)

@@ -1,7 +1,7 @@
 """Every BASELINE.json config on one B200 (not the driver's bench line).
 
   configs[0] case14, 1000 scenarios      -- GPU solve and the CPU oracle port
-  configs[1] synth300 (case300-sized), 10k scenarios
+  configs[1] synth300 (case300-sized), 10k Monte-Carlo load/PV scenarios
   configs[2] synth2383 (case2383wp-sized), 10k: batched LU refactorization microbenchmark
   configs[3] synth9241 (case9241pegase-sized), 10k (the headline; bench.py)
   configs[4] synth9241, 100k over N GPUs -- per-GPU 12.5k slice at N = 8 (weak-scaled here)
@@ -25,10 +25,10 @@ from paper_2101_02270_b200.case import load_case  # noqa: E402
 from paper_2101_02270_b200.scenarios import montecarlo  # noqa: E402
 
 
-def gpu_solve(name, T):
+def gpu_solve(name, T, mode="load"):
     gc = load_case(os.path.join(ROOT, "cases", name + ".m"))
     vm0, va0 = gc.v_start()
-    p0, q0 = montecarlo(gc, T)
+    p0, q0 = montecarlo(gc, T, mode=mode)
     plan = S.NrPlan.from_case(gc, device=0, profile=1)
     st = plan.stats()
     plan.stage(p0, q0, vm0, va0)
@@ -38,7 +38,7 @@ def gpu_solve(name, T):
         plan.run()
         tm = plan.timing()
         best = tm if best is None or tm["total_ms"] < best["total_ms"] else best
-    out = {"case": name, "tasks": T, "nJ": st["nJ"], "nnzLU": st["nnzLU"], "D": st["D"],
+    out = {"case": name, "tasks": T, "scenario_mode": mode, "nJ": st["nJ"], "nnzLU": st["nnzLU"], "D": st["D"],
            "ms": best["total_ms"], "pf_per_s": best["converged"] / (best["total_ms"] / 1e3),
            "iterations": best["iterations"], "converged": best["converged"],
            "per_launch_ms": {k: best[k + "_ms"] / max(best[k + "_launches"], 1)
@@ -46,11 +46,12 @@ def gpu_solve(name, T):
     return gc, plan, out
 
 
-def cpu_solve(gc, T, threads):
-    ip, ix, _, yr, yi = S.build_ybus(gc)
+def cpu_solve(gc, T, threads, mode="load"):
+    orc = po.Oracle()
+    ip, ix, _, yr, yi = orc.build_ybus(gc)
     vm0, va0 = gc.v_start()
-    op = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
-    p0, q0 = montecarlo(gc, T)
+    op = orc.plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0)
+    p0, q0 = montecarlo(gc, T, mode=mode)
     t = time.perf_counter()
     r = op.solve(p0, q0, vm0[:, None], va0[:, None], n_threads=threads)
     dt = time.perf_counter() - t
@@ -63,8 +64,9 @@ def main():
     gc, plan, res["config0_case14_1000"] = gpu_solve("case14", 1000)
     res["config0_case14_1000"]["cpu_oracle"] = cpu_solve(gc, 1000, threads)
     plan.close()
-    gc, plan, res["config1_synth300_10k"] = gpu_solve("synth300", 10000)
-    res["config1_synth300_10k"]["cpu_oracle"] = cpu_solve(gc, 2000, threads)
+    # configs[1]: 10k Monte-Carlo load/PV scenarios (PV set-points drawn per task too)
+    gc, plan, res["config1_synth300_10k_loadpv"] = gpu_solve("synth300", 10000, mode="loadpv")
+    res["config1_synth300_10k_loadpv"]["cpu_oracle"] = cpu_solve(gc, 10000, threads, mode="loadpv")
     plan.close()
     # configs[2]: LU-only microbenchmark, J frozen at each task's start voltages
     gc = load_case(os.path.join(ROOT, "cases", "synth2383.m"))

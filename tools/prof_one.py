@@ -1,4 +1,6 @@
-"""One staged solve (for ncu): prof_one.py CASE TASKS [key=val ...]"""
+"""The ncu capture target of tools/gpu_round.sh and gpu_full.sh: one staged solve.
+
+usage: prof_one.py CASE TASKS [key=val ...]  (key=val are gbnr_options fields)"""
 import os
 import sys
 
