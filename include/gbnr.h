@@ -34,8 +34,13 @@
  *    4 singular initial factorization, 5 CUDA.  No C++ exception crosses the
  *    ABI.  Per-task numerical failure goes to status_out, never to the return
  *    code (core.hpp:33-34).
- *  - A plan is immutable after creation; calls on one plan serialize.  One plan
- *    per device; multi-GPU = one host thread (or process) per device.
+ *  - A plan is immutable after creation; calls on one plan serialize.  A plan
+ *    with n_devices > 1 holds one device plan per GPU and drives them from one
+ *    host thread each inside gbnr_solve / gbnr_solve_batches; the split form
+ *    (gbnr_stage / gbnr_run / gbnr_fetch), gbnr_refactor and gbnr_branch_flows
+ *    use the first device.  A batch larger than a device's memory is solved in
+ *    chunks (gbnr_options.chunk_tasks); results never depend on the sharding or
+ *    the chunking (tasks are independent).
  *  - There is no CPU fallback: a plan created with device >= 0 runs only on the
  *    GPU; gbnr_solve on a host-only plan (device = -1) returns 3.
  */
@@ -80,13 +85,22 @@ typedef struct gbnr_options {
                               check (a wrong guess adds a Jacobian-only launch);
                               1 = always inside the sweep; 2 = always after the check
                               (the reference's order).  Results are identical.        */
-    int32_t second_chance; /* up to this many tasks per solve (default 16) whose
-                              frozen pivot collapsed are re-planned alone with fresh
-                              pivoting at their current voltages and continue
-                              (SPEC.md:337-345); status 3 on convergence.  0 = off.
-                              With a shared Ybus, >5% of the tasks failing at their
-                              first solve restarts the batch once from the worst
-                              task's pivots (SPEC.md design decisions).               */
+    int32_t second_chance; /* 1 (default): every task whose frozen pivot collapsed is
+                              re-planned alone with fresh pivoting at its current
+                              voltages and continues; status 3
+                              on convergence.  The re-plans run concurrently (host
+                              threads, one stream each).  0 = off.  With a shared
+                              Ybus, >5% of the tasks failing at their first solve
+                              restarts the batch once from the worst task's pivots
+                              (SPEC.md design decisions).                           */
+    int32_t n_devices;     /* gbnr_solve / gbnr_solve_batches shard the tasks over this
+                              many GPUs (0 or 1 = one): contiguous slices, one plan,
+                              host thread and stream per device, results gathered
+                              straight into the caller's buffers.  No collective.   */
+    int32_t device_step;   /* device of shard i = device + i * device_step (default 1;
+                              0 = every shard on `device`, e.g. tests on one GPU)    */
+    int32_t chunk_tasks;   /* most tasks per device launch; larger slices are solved in
+                              chunks (0 = automatic, from the free device memory)    */
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);
@@ -177,7 +191,8 @@ int gbnr_solve_batches(gbnr_plan* plan, int32_t n_batches, int32_t n_tasks, cons
                        int32_t* const* status_out, double* const* max_mismatch_out);
 
 /* calc_branch_flows on the voltages of the last solve of
- * `plan` (still on the device): S_from = V_f conj(Yff V_f + Yft V_t), S_to =
+ * `plan` (still on the device; GBNR_ECONFIG if that solve was sharded over
+ * devices or chunked, i.e. the device no longer holds every task): S_from = V_f conj(Yff V_f + Yft V_t), S_to =
  * V_t conj(Ytf V_f + Ytt V_t) per branch and task, zero for the task's outaged
  * branch (outage_branch [n_tasks] or NULL); outputs [n_branch][n_tasks]
  * element-major (any may be NULL).  Computed for every task (diverged ones

@@ -151,7 +151,7 @@ class OraclePlan:
         return dict(row_fwd=rf, col_fwd=cf, col_ptr=cp, row_ix=ri, level=lev)
 
     def solve(self, p0, q0, vm0, va0, n_tasks=None, y=None, tol=1e-8, max_iter=10,
-              singular_tol=1e-14, n_threads=None, second_chance=16, _rederive=True):
+              singular_tol=1e-14, n_threads=None, second_chance=True, _rederive=True):
         p0 = _f64(p0); q0 = _f64(q0); vm0 = _f64(vm0); va0 = _f64(va0)
         if n_tasks is None:
             n_tasks = max(p0.shape[1] if p0.ndim == 2 else 1, vm0.shape[1] if vm0.ndim == 2 else 1)
@@ -169,7 +169,7 @@ class OraclePlan:
         nt = n_threads or os.cpu_count() or 1
         self.o._check(self.o.lib.orc_solve(self.h, n_tasks, yre, yim, ny, p0, q0, ns, vm0, va0, nv,
                                            tol, max_iter, singular_tol, vm, va, it, cv, st, mm, nt))
-        second_chance = int(second_chance)  # re-plans per solve (True = 1)
+        second_chance = bool(second_chance)
         if second_chance and _rederive and ny == 1 and int(((st == 2) & (it == 1)).sum()) * 20 > n_tasks:
             # representative re-derivation (SPEC.md DESIGN DECISIONS): the frozen
             # pivots failed for more than 5% of the tasks at their first solve ->
@@ -195,27 +195,25 @@ class OraclePlan:
                                  _rederive=False)
         if second_chance:
             self._second_chance(n_tasks, yre, yim, ny, p0, q0, ns, tol, max_iter, singular_tol,
-                                vm, va, it, cv, st, mm, second_chance)
+                                vm, va, it, cv, st, mm)
         return dict(vm=vm, va=va, iterations=it, converged=cv, status=st, max_mismatch=mm)
 
     def _second_chance(self, n_tasks, yre, yim, ny, p0, q0, ns, tol, max_iter, singular_tol,
-                       vm, va, it, cv, st, mm, cap):
+                       vm, va, it, cv, st, mm):
         """second_chance_refactorize (open question :436): a task
         whose frozen pivot collapsed (status singular after `it` linear solves) is
         re-planned alone -- a fresh threshold-pivoting factorization at its current
         voltages, kept for the rest of its Newton loop -- and continues with the
         remaining budget max_iter - (it - 1).  Converged -> status 3
         (fallback_converged); otherwise the re-run's status.  A fresh
-        factorization that is itself singular leaves the task singular.  At most
-        `cap` tasks (in task order) get the re-plan."""
+        factorization that is itself singular leaves the task singular.  Every
+        flagged task gets its re-plan (tasks flagged for the fallback
+        are re-run)."""
         ip, ix, _, _, pv, pq = self._keep
         for t in np.nonzero(st == 2)[0]:
             budget = max_iter - (int(it[t]) - 1)
             if budget < 1:
                 continue
-            if cap <= 0:  # at most `cap` re-plans per solve (gbnr_options.second_chance)
-                break
-            cap -= 1
             yr = yre[:, t] if ny > 1 else (yre[:, 0] if yre.ndim == 2 else yre)
             yi = yim[:, t] if ny > 1 else (yim[:, 0] if yim.ndim == 2 else yim)
             pp = p0[:, t] if ns > 1 else (p0[:, 0] if p0.ndim == 2 else p0)

@@ -678,7 +678,25 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             if (nrows > 0) {
                 const double mult = xg[size_t(kpos_fs & 0xffff) * kTile];
                 const int32_t* dw = r + 5;
-                for (int q = 0; q < nrows; ++q) {
+                int q = 0;
+#pragma unroll 1
+                for (; q + 8 <= nrows; q += 8) {  // 16 independent loads in flight per group
+                    int d[8];
+                    double l[8], a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        const int32_t wq = dw[(q + u) >> 1];
+                        d[u] = wq & 0xffff;
+                        d[u + 1] = int(unsigned(wq) >> 16);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) l[u] = src[size_t(q + u) * kTile];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = xg[size_t(d[u]) * kTile];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) xg[size_t(d[u]) * kTile] = fma(-mult, l[u], a[u]);
+                }
+                for (; q < nrows; ++q) {
                     const int32_t wq = dw[q >> 1];
                     const int d = (q & 1) ? int(unsigned(wq) >> 16) : (wq & 0xffff);
                     xg[size_t(d) * kTile] = fma(-mult, src[size_t(q) * kTile], xg[size_t(d) * kTile]);
@@ -697,14 +715,35 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             P.cur += 5;
             xg = v.scratch + (size_t(tile) * 8 + warp) * size_t(v.scratch_rows) * kTile + lane;
             const double* at = v.A + size_t(tile) * v.tstride + lane + size_t(a0) * kTile;
-            for (int z = 0; z <= len; ++z) xg[size_t(z) * kTile] = at[size_t(z) * kTile];
+            int z = 0;
+#pragma unroll 1
+            for (; z + 8 <= len + 1; z += 8) {  // loads grouped ahead of the stores
+                double a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = at[size_t(z + u) * kTile];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) xg[size_t(z + u) * kTile] = a[u];
+            }
+            for (; z <= len; ++z) xg[size_t(z) * kTile] = at[size_t(z) * kTile];
             acc_y = FS ? xg[size_t(len) * kTile] : 0.0;
             gmax = 0.0;
         } else if (type == kRecEndU) {
             // U entries z0 .. z0+cnt-1 of a global step -> their row-major slots
             const int cnt = (h >> 4) & 0xfffff, z0 = r[1];
             h = r[2 + cnt];
-            for (int i = 0; i < cnt; ++i) {
+            int i = 0;
+#pragma unroll 1
+            for (; i + 8 <= cnt; i += 8) {
+                double u[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) u[k] = xg[size_t(z0 + i + k) * kTile];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    gmax = fmax(gmax, fabs(u[k]));
+                    lu_t[size_t(r[2 + i + k]) * kTile] = u[k];
+                }
+            }
+            for (; i < cnt; ++i) {
                 const double u = xg[size_t(z0 + i) * kTile];
                 gmax = fmax(gmax, fabs(u));
                 lu_t[size_t(r[2 + i]) * kTile] = u;
@@ -717,7 +756,19 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const double inv = 1.0 / piv;
             double c0 = fmax(gmax, fabs(piv));
             double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * kTile;
-            for (int z = dp + 1; z < len; ++z) {
+            int z = dp + 1;
+#pragma unroll 1
+            for (; z + 8 <= len; z += 8) {
+                double x[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x[k] = xg[size_t(z + k) * kTile];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    c0 = fmax(c0, fabs(x[k]));
+                    lcol[size_t(z + k) * kTile] = x[k] * inv;
+                }
+            }
+            for (; z < len; ++z) {
                 const double x0 = xg[size_t(z) * kTile];
                 c0 = fmax(c0, fabs(x0));
                 lcol[size_t(z) * kTile] = x0 * inv;
@@ -825,7 +876,20 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
         } else if (type == kRecDepNG) {
             const int n = (h >> 4) & 0xfffff;
             h = r[1 + n];
-            for (int i = 0; i < n; ++i) {  // acc -= U(i,k) x_k, k descending, x_k from the b tape
+            int i = 0;
+#pragma unroll 1
+            for (; i + 8 <= n; i += 8) {  // acc -= U(i,k) x_k, k descending, x_k from the b tape
+                double u[8], x[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    u[k] = e_g[size_t(k) * kTile];
+                    x[k] = b_t[size_t(r[1 + i + k]) * kTile];
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = fma(-u[k], x[k], acc);
+                e_g += 8 * kTile;
+            }
+            for (; i < n; ++i) {
                 acc = fma(-e_g[0], b_t[size_t(r[1 + i]) * kTile], acc);
                 e_g += kTile;
             }
@@ -904,8 +968,13 @@ __global__ void __launch_bounds__(256) flows_kernel(DevView v, int32_t nb, const
         }
         const int f = __ldg(bf + k), to = __ldg(bt + k);
         const double vmf = v.vm[f * bp + t], vmt = v.vm[to * bp + t];
-        const double vfr = vmf * v.c[f * bp + t], vfi = vmf * v.s[f * bp + t];
-        const double vtr = vmt * v.c[to * bp + t], vti = vmt * v.s[to * bp + t];
+        // unit phasors from the angles (the same gb_sincos that fills the c / s tapes,
+        // so voltages written back from the host -- second chance -- need no c / s)
+        double sf, cf, st, ct;
+        gb_sincos(v.va[f * bp + t], &sf, &cf);
+        gb_sincos(v.va[to * bp + t], &st, &ct);
+        const double vfr = vmf * cf, vfi = vmf * sf;
+        const double vtr = vmt * ct, vti = vmt * st;
         const double* a = adm + size_t(8) * k;
         double P, Q;
         branch_end_flow(__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3), vfr, vfi, vtr, vti, vfr, vfi, P, Q);

@@ -10,9 +10,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
+#include <atomic>
+#include <exception>
 #include <functional>
-#include <string>
 #include <memory>
+#include <string>
+#include <thread>
+#include <type_traits>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -65,6 +70,12 @@ enum Phase { kNpm = 0, kJac, kLu, kFsbs, kVupd, kPhases };
 
 }  // namespace
 
+// gbnr_plan_create with `sub`: a second-chance / re-derivation plan (no LU-only walk)
+static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indices, const double* y_re,
+                       const double* y_im, int32_t ref, const int32_t* pv, int32_t n_pv, const int32_t* pq,
+                       int32_t n_pq, const double* vm0, const double* va0, const gbnr_options* opt, gbnr_plan** out,
+                       bool sub);
+
 struct gbnr_plan {
     gbnr::Symbolic sym;
     std::vector<int32_t> in_pv, in_pq;  // creation inputs kept for second-chance re-plans
@@ -91,6 +102,11 @@ struct gbnr_plan {
     double* d_scratch = nullptr;  // [n] staging for broadcast sets
     std::vector<void*> batch;     // per-batch tapes
     int32_t cap_tiles = 0;        // allocated tile capacity
+    size_t batch_bytes = 0, pipe_bytes = 0;  // device bytes held by the batch tapes / the pipeline
+    std::vector<double> y_host_re, y_host_im;       // the plan's shared Ybus values (host copy)
+    std::vector<std::unique_ptr<gbnr_plan>> peers;  // device plans 2..n_devices (gbnr_options.n_devices)
+    bool sub_plan = false;         // a second-chance / re-derivation plan: no LU-only walk
+    bool whole_on_device = false;  // the device state holds every task of the last solve
     double *p0_own = nullptr, *q0_own = nullptr;  // [n][bpad] injections owned by the plan
     bool staged = false;
     bool solved = false;  // device voltages hold a finished solve
@@ -184,7 +200,7 @@ struct gbnr_plan {
             v.zcol_v = dev_upload(owned, zv);
         }
         vf = upload_walk(wf);
-        vl = upload_walk(wl);
+        if (!sub_plan) vl = upload_walk(wl);
         vb = upload_walk(wb);
         int32_t* itd = nullptr;
         CK(cudaMalloc(&itd, sizeof(int32_t)));
@@ -225,9 +241,10 @@ struct gbnr_plan {
     size_t y_task_cap = 0;
 
     void set_ybus(const double* re, const double* im) {
-        std::vector<double> a(re, re + sym.nnzY), b(im, im + sym.nnzY);
-        v.yre = y_shared_re = dev_upload(owned, a);
-        v.yim = y_shared_im = dev_upload(owned, b);
+        y_host_re.assign(re, re + sym.nnzY);
+        y_host_im.assign(im, im + sym.nnzY);
+        v.yre = y_shared_re = dev_upload(owned, y_host_re);
+        v.yim = y_shared_im = dev_upload(owned, y_host_im);
         v.y_ld = 1;
         v.y_inc = 0;
     }
@@ -235,7 +252,21 @@ struct gbnr_plan {
     // Ybus values for the next solve: NULL = the plan's shared set; otherwise the
     // caller's set(s) are staged into a per-call buffer (one shared set, y_inc = 0,
     // or one per task, [nnzY][n_tasks]) and the plan's own set is never touched.
-    void stage_ybus(const double* y_re, const double* y_im, int32_t n_ysets, int32_t n_tasks) {
+    // ld_y > 0: per-task sets, columns [0, n_tasks) of a host array [nnzY][ld_y]
+    // (a slice of a larger batch; the caller offsets the pointers)
+    void stage_ybus(const double* y_re, const double* y_im, int32_t n_ysets, int32_t n_tasks, int64_t ld_y = 0) {
+        if (ld_y > 0 && y_re && y_im) {
+            const size_t bytes = size_t(sym.nnzY) * size_t(n_tasks) * 8;
+            ensure_ytask(bytes);
+            for (auto [dst, src] : {std::pair{y_task_re, y_re}, {y_task_im, y_im}})
+                CK(cudaMemcpy2DAsync(dst, size_t(n_tasks) * 8, src, size_t(ld_y) * 8, size_t(n_tasks) * 8,
+                                     size_t(sym.nnzY), cudaMemcpyHostToDevice, stream));
+            v.yre = y_task_re;
+            v.yim = y_task_im;
+            v.y_ld = n_tasks;
+            v.y_inc = 1;
+            return;
+        }
         if (!y_re || !y_im) {
             if (n_ysets != 1) throw Error(GBNR_ECONFIG, "per-task Ybus sets need y_re and y_im");
             v.yre = y_shared_re;
@@ -248,16 +279,7 @@ struct gbnr_plan {
         if (!shared && n_ysets != n_tasks) throw Error(GBNR_ECONFIG, "n_ysets must be 1 or n_tasks");
         const size_t sets = shared ? 1 : size_t(n_tasks);
         const size_t bytes = size_t(sym.nnzY) * sets * 8;
-        if (bytes > y_task_cap) {
-            CK(cudaStreamSynchronize(stream));
-            if (y_task_re) cudaFree(y_task_re);
-            if (y_task_im) cudaFree(y_task_im);
-            y_task_re = y_task_im = nullptr;
-            y_task_cap = 0;
-            CK(cudaMalloc(&y_task_re, bytes));
-            CK(cudaMalloc(&y_task_im, bytes));
-            y_task_cap = bytes;
-        }
+        ensure_ytask(bytes);
         CK(cudaMemcpyAsync(y_task_re, y_re, bytes, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(y_task_im, y_im, bytes, cudaMemcpyHostToDevice, stream));
         v.yre = y_task_re;
@@ -266,16 +288,56 @@ struct gbnr_plan {
         v.y_inc = shared ? 0 : 1;
     }
 
+    void ensure_ytask(size_t bytes) {
+        if (bytes <= y_task_cap) return;
+        CK(cudaStreamSynchronize(stream));
+        if (y_task_re) cudaFree(y_task_re);
+        if (y_task_im) cudaFree(y_task_im);
+        y_task_re = y_task_im = nullptr;
+        y_task_cap = 0;
+        CK(cudaMalloc(&y_task_re, bytes));
+        CK(cudaMalloc(&y_task_im, bytes));
+        y_task_cap = bytes;
+    }
+
+    // Device bytes one tile (32 tasks) of a solve needs: the A / LU / b block, the
+    // [n][bpad] voltage / injection tapes, per-task state, walk scratch, and the
+    // per-task Ybus sets when the batch has them.
+    size_t bytes_per_tile(bool per_task_y) const {
+        const size_t lanes = gbnr::kTile;
+        size_t b = v.tstride * 8 + 8 * size_t(sym.n) * lanes * 8 + lanes * 64 +
+                   size_t(8) * size_t(std::max(wf.scratch_rows, wl.scratch_rows)) * lanes * 8;
+        if (per_task_y) b += 2 * size_t(sym.nnzY) * lanes * 8;
+        return b;
+    }
+
+    // Tasks one launch of this plan can hold: gbnr_options.chunk_tasks, else what
+    // the free device memory (plus what this plan already holds) allows, keeping a
+    // reserve for the second-chance re-plans and the driver.
+    int32_t chunk_capacity(bool per_task_y) {
+        if (opt.chunk_tasks > 0) return opt.chunk_tasks;
+        CK(cudaSetDevice(opt.device));
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t held = batch_bytes + pipe_bytes + y_task_cap;
+        const size_t reserve = (size_t(4) << 30) + total_b / 50;
+        const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
+        const size_t tiles = avail / bytes_per_tile(per_task_y);
+        return int32_t(std::max<size_t>(1, std::min<size_t>(tiles, (size_t(1) << 26))) * gbnr::kTile);
+    }
+
     void ensure_capacity(int32_t n_tiles) {
         if (n_tiles <= cap_tiles) return;
         CK(cudaStreamSynchronize(stream));
         for (void* p : batch) cudaFree(p);
         batch.clear();
         const size_t bpad = size_t(n_tiles) * gbnr::kTile;
+        batch_bytes = 0;
         auto alloc = [&](size_t bytes) {
             void* p = nullptr;
             CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
             batch.push_back(p);
+            batch_bytes += bytes;
             return p;
         };
         const size_t nb = size_t(sym.n) * bpad * sizeof(double);
@@ -334,12 +396,26 @@ struct gbnr_plan {
         }
     }
 
+    // ld_s / ld_v > 0: the injections / start voltages are per task, columns
+    // [0, n_tasks) of host arrays [n][ld] (a slice of a larger batch; the caller
+    // offsets the pointers; n_ssets / n_vsets are then ignored)
     void stage(int32_t n_tasks, const double* p0, const double* q0, int32_t n_ssets,
-               const double* vm0, const double* va0, int32_t n_vsets) {
+               const double* vm0, const double* va0, int32_t n_vsets, int64_t ld_s = 0, int64_t ld_v = 0) {
         if (!on_device) throw Error(GBNR_ECONFIG, "host-only plan (device = -1) cannot solve");
         if (n_tasks <= 0) throw Error(GBNR_ECONFIG, "n_tasks must be positive");
+        if (ld_s > 0) n_ssets = n_tasks;
+        if (ld_v > 0) n_vsets = n_tasks;
         if ((n_ssets != 0 && n_ssets != 1 && n_ssets != n_tasks) || (n_vsets != 1 && n_vsets != n_tasks))
             throw Error(GBNR_ECONFIG, "set counts must be 1 or n_tasks");
+        // host [n][ld] columns [0, n_tasks) -> device [n][n_tasks], one linear copy when unsliced
+        auto h2d_cols = [&](const double* dst, const double* src, int64_t ld) {
+            const size_t w = size_t(n_tasks) * 8;
+            if (ld <= 0 || ld == n_tasks)
+                CK(cudaMemcpyAsync(const_cast<double*>(dst), src, size_t(sym.n) * w, cudaMemcpyHostToDevice, stream));
+            else
+                CK(cudaMemcpy2DAsync(const_cast<double*>(dst), w, src, size_t(ld) * 8, w, size_t(sym.n),
+                                     cudaMemcpyHostToDevice, stream));
+        };
         CK(cudaSetDevice(opt.device));
         const int32_t n_tiles = (n_tasks + gbnr::kTile - 1) / gbnr::kTile;
         ensure_capacity(n_tiles);
@@ -348,10 +424,15 @@ struct gbnr_plan {
         v.n_tasks = n_tasks;
         // start voltages as given: [n] shared or [n][n_tasks], one linear copy each
         // (init_kernel reads them through vin_ld / vin_inc)
-        const bool vshared = n_vsets == 1;
-        const size_t vbytes = size_t(sym.n) * (vshared ? 1 : size_t(n_tasks)) * sizeof(double);
-        CK(cudaMemcpyAsync(const_cast<double*>(v.vm_in), vm0, vbytes, cudaMemcpyHostToDevice, stream));
-        CK(cudaMemcpyAsync(const_cast<double*>(v.va_in), va0, vbytes, cudaMemcpyHostToDevice, stream));
+        const bool vshared = n_vsets == 1 && ld_v <= 0;
+        if (vshared) {
+            const size_t vbytes = size_t(sym.n) * sizeof(double);
+            CK(cudaMemcpyAsync(const_cast<double*>(v.vm_in), vm0, vbytes, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(const_cast<double*>(v.va_in), va0, vbytes, cudaMemcpyHostToDevice, stream));
+        } else {
+            h2d_cols(v.vm_in, vm0, ld_v);
+            h2d_cols(v.va_in, va0, ld_v);
+        }
         v.vin_ld = vshared ? 1 : n_tasks;
         v.vin_inc = vshared ? 0 : 1;
         if (n_ssets != 0) {
@@ -360,6 +441,11 @@ struct gbnr_plan {
         }
         if (n_ssets == 0) {
             // injections are placed by the caller (batch pipeline)
+        } else if (ld_s > 0) {
+            h2d_cols(v.p0, p0, ld_s);
+            h2d_cols(v.q0, q0, ld_s);
+            v.s_ld = n_tasks;
+            v.s_inc = 1;
         } else if (n_ssets == 1 && n_tasks > 1) {
             CK(cudaMemcpyAsync(const_cast<double*>(v.p0), p0, size_t(sym.n) * sizeof(double),
                                cudaMemcpyHostToDevice, stream));
@@ -382,6 +468,7 @@ struct gbnr_plan {
             v.s_inc = 1;
         }
         staged = true;
+        whole_on_device = true;
     }
 
     void timed(int phase, const std::function<void()>& launch) {
@@ -418,7 +505,10 @@ struct gbnr_plan {
 
     static int launches_per_iteration() { return 6; }  // lu+fs, bs, vupd, npm+jac, conv, bump
 
-    void run() {
+    // One batched Newton solve of the staged tasks.  finish: also the second chance
+    // of flagged tasks (and, inside gbnr_solve, the re-derivation decision);
+    // solve_general finishes chunks itself.
+    void run(bool finish = true) {
         if (!staged) throw Error(GBNR_ECONFIG, "gbnr_run before gbnr_stage");
         CK(cudaSetDevice(opt.device));
         std::memset(timing, 0, sizeof timing);
@@ -454,15 +544,8 @@ struct gbnr_plan {
         }
         timing[14] = tiles;
         timing[15] = tasks;
-        if (opt.second_chance && h_count[66] > 0) {
-            // representative re-derivation (SPEC.md DESIGN DECISIONS): the frozen
-            // pivot order failed for more than 5% of the tasks at their first
-            // solve -> gbnr_solve restarts the batch once from the worst task
-            if (allow_rederive && flagged_at_first_solve() * 20 > v.n_tasks)
-                rederive_pending = true;
-            else
-                second_chance();
-        }
+        first_flagged = h_count[66] > 0 ? flagged_at_first_solve() : 0;
+        if (finish && opt.second_chance && h_count[66] > 0) second_chance();
         count_statuses();
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -483,7 +566,7 @@ struct gbnr_plan {
     // converges, else the re-run's status.  A fresh factorization that is itself
     // singular leaves the task singular.  Host orchestration only: the re-run uses
     // the same kernels (oracle/pyoracle.py OraclePlan._second_chance is the checker).
-    bool allow_rederive = false, rederive_pending = false;
+    int32_t first_flagged = 0;  // tasks of the last run flagged at their first linear solve
 
     // converged (incl. second chance), diverged, singular; [20] the second-chance subset
     void count_statuses() {
@@ -504,116 +587,266 @@ struct gbnr_plan {
         return c;
     }
 
-    // The restart of gbnr_solve: a plan whose pivots come from the task with the
-    // worst mismatch at V0 (its V0 and Ybus values) solves the whole batch again,
-    // with second chance; results and device voltages come from it.
-    void rederive_and_solve(int32_t n_tasks, const double* y_re, const double* y_im, int32_t n_ysets,
-                            const double* p0, const double* q0, int32_t n_ssets, const double* vm0,
-                            const double* va0, int32_t n_vsets, double* vm_out, double* va_out,
-                            int32_t* it_out, uint8_t* conv_out, int32_t* st_out, double* mm_out) {
-        const int32_t nt = v.n_tasks, n = sym.n, nY = sym.nnzY;
-        std::vector<double> m0(nt);
-        CK(cudaMemcpy(m0.data(), v.mis0, size_t(nt) * 8, cudaMemcpyDeviceToHost));
-        int32_t w = 0;
-        for (int32_t t = 1; t < nt; ++t)
-            if (m0[t] > m0[w]) w = t;  // first of the largest
-        std::vector<double> vm(n), va(n), yr(nY), yi(nY);
-        const int32_t vw = n_vsets == 1 ? 0 : w;
-        for (int32_t b = 0; b < n; ++b) {
-            vm[b] = vm0[size_t(b) * n_vsets + vw];
-            va[b] = va0[size_t(b) * n_vsets + vw];
-        }
-        if (y_re && y_im) {
-            const int32_t yw = n_ysets == 1 ? 0 : w;
-            for (int32_t q = 0; q < nY; ++q) {
-                yr[q] = y_re[size_t(q) * n_ysets + yw];
-                yi[q] = y_im[size_t(q) * n_ysets + yw];
-            }
-        } else {
-            CK(cudaMemcpy(yr.data(), y_shared_re, size_t(nY) * 8, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(yi.data(), y_shared_im, size_t(nY) * 8, cudaMemcpyDeviceToHost));
-        }
-        gbnr_plan* alt = nullptr;
-        const int rc = gbnr_plan_create(n, sym.yp.data(), sym.yi.data(), yr.data(), yi.data(), sym.ref,
-                                        in_pv.data(), int32_t(in_pv.size()), in_pq.data(), int32_t(in_pq.size()),
-                                        vm.data(), va.data(), &opt, &alt);
-        if (rc == GBNR_ESINGULAR) {  // no better representative: per-task second chance
-            second_chance();
-            count_statuses();
-            fetch(vm_out, va_out, it_out, conv_out, st_out, mm_out);
-            return;
-        }
-        if (rc != GBNR_OK) throw Error(rc, std::string("re-derivation: ") + gbnr_last_error());
-        std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(alt, gbnr_plan_destroy);
-        alt->stage_ybus(y_re, y_im, n_ysets, n_tasks);
-        alt->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
-        alt->run();
-        alt->fetch(vm_out, va_out, it_out, conv_out, st_out, mm_out);
-        std::memcpy(timing, alt->timing, sizeof timing);
-        timing[21] = 1;  // restarted from a re-derived representative
-        // device state for gbnr_branch_flows: the restarted solve's voltages
-        CK(cudaSetDevice(opt.device));
-        const size_t nb = size_t(n) * size_t(v.bpad) * 8;
-        for (auto [dst, src] : {std::pair{v.vm, alt->v.vm}, {v.va, alt->v.va}, {v.c, alt->v.c}, {v.s, alt->v.s}})
-            CK(cudaMemcpy(dst, src, nb, cudaMemcpyDeviceToDevice));
-        CK(cudaMemcpy(v.status, alt->v.status, size_t(nt) * 4, cudaMemcpyDeviceToDevice));
-        CK(cudaMemcpy(v.iters, alt->v.iters, size_t(nt) * 4, cudaMemcpyDeviceToDevice));
-        CK(cudaMemcpy(v.maxmis, alt->v.maxmis, size_t(nt) * 8, cudaMemcpyDeviceToDevice));
+    // ---- second chance -------------------------------
+    // Every flagged task is re-planned alone: its own threshold-pivoting
+    // factorization at its current voltages (kept for the rest of its Newton loop),
+    // then it continues on this GPU with the remaining budget max_iter - (it - 1).
+    // The re-plans (host symbolic analysis + walk plans) and their one-task solves
+    // run concurrently, one host thread and stream per re-plan.
+    struct Chance {
+        int32_t t = 0, it = 0;
+        std::vector<double> vm, va, yr, yi, pp, qq;  // the task's state at the failure
+        bool ran = false;
+        int32_t status = GBNR_SINGULAR, iters = 0;
+        double mm = 0.0;
+    };
+
+    void run_chance(Chance& c) {
+        gbnr_options o = opt;
+        o.second_chance = 0;  // one chance
+        o.profile = 0;
+        o.n_devices = 1;
+        o.chunk_tasks = 0;
+        o.max_iter = opt.max_iter - (c.it - 1);
+        gbnr_plan* sub = nullptr;
+        const int rc = create_plan(sym.n, sym.yp.data(), sym.yi.data(), c.yr.data(), c.yi.data(), sym.ref,
+                                   in_pv.data(), int32_t(in_pv.size()), in_pq.data(), int32_t(in_pq.size()),
+                                   c.vm.data(), c.va.data(), &o, &sub, true);
+        if (rc == GBNR_ESINGULAR) return;  // still singular: the task stays failed
+        if (rc != GBNR_OK) throw Error(rc, std::string("second chance: ") + gbnr_last_error());
+        std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(sub, gbnr_plan_destroy);
+        sub->stage_ybus(nullptr, nullptr, 1, 1);
+        sub->stage(1, c.pp.data(), c.qq.data(), 1, c.vm.data(), c.va.data(), 1);
+        sub->run(false);
+        int32_t s2 = 0, i2 = 0;
+        sub->fetch(c.vm.data(), c.va.data(), &i2, nullptr, &s2, &c.mm);
+        c.status = s2 == GBNR_CONVERGED ? GBNR_FALLBACK_CONVERGED : s2;
+        c.iters = c.it - 1 + i2;
+        c.ran = true;
     }
 
     void second_chance() {
+        CK(cudaSetDevice(opt.device));
         const int32_t nt = v.n_tasks, n = sym.n, nY = sym.nnzY;
         std::vector<int32_t> st(nt), it(nt);
         CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
         CK(cudaMemcpyAsync(it.data(), v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
-        gbnr_options o = opt;
-        o.second_chance = 0;  // one chance
-        o.profile = 0;
-        std::vector<double> vm(n), va(n), yr(nY), yi(nY), pp(n), qq(n);
-        auto column = [&](double* dst, const double* src, size_t pitch, int32_t rows) {
-            CK(cudaMemcpy2DAsync(dst, 8, src, pitch * 8, 8, size_t(rows), cudaMemcpyDeviceToHost, stream));
+        std::vector<Chance> work;
+        const size_t bp = size_t(v.bpad);
+        auto column = [&](std::vector<double>& dst, const double* src, size_t pitch, int32_t rows) {
+            dst.resize(size_t(rows));
+            CK(cudaMemcpy2DAsync(dst.data(), 8, src, pitch * 8, 8, size_t(rows), cudaMemcpyDeviceToHost, stream));
         };
-        int32_t budget = opt.second_chance;  // re-plans per solve (each is a plan build)
-        for (int32_t t = 0; t < nt && budget > 0; ++t) {
-            if (st[t] != GBNR_SINGULAR) continue;
-            o.max_iter = opt.max_iter - (it[t] - 1);
-            if (o.max_iter < 1) continue;
-            --budget;
-            const size_t bp = size_t(v.bpad);
-            column(vm.data(), v.vm + t, bp, n);
-            column(va.data(), v.va + t, bp, n);
-            column(yr.data(), v.yre + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
-            column(yi.data(), v.yim + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
-            column(pp.data(), v.p0 + size_t(t) * v.s_inc, size_t(v.s_ld), n);
-            column(qq.data(), v.q0 + size_t(t) * v.s_inc, size_t(v.s_ld), n);
-            CK(cudaStreamSynchronize(stream));
-            gbnr_plan* sub = nullptr;
-            const int rc = gbnr_plan_create(n, sym.yp.data(), sym.yi.data(), yr.data(), yi.data(), sym.ref,
-                                            in_pv.data(), int32_t(in_pv.size()), in_pq.data(),
-                                            int32_t(in_pq.size()), vm.data(), va.data(), &o, &sub);
-            if (rc == GBNR_ESINGULAR) continue;  // still singular: the task stays failed
-            if (rc != GBNR_OK) throw Error(rc, std::string("second chance: ") + gbnr_last_error());
-            std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(sub, gbnr_plan_destroy);
-            sub->stage_ybus(nullptr, nullptr, 1, 1);
-            sub->stage(1, pp.data(), qq.data(), 1, vm.data(), va.data(), 1);
-            sub->run();
-            int32_t s2 = 0, i2 = 0;
-            CK(cudaMemcpy(&s2, sub->v.status, 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(&i2, sub->v.iters, 4, cudaMemcpyDeviceToHost));
-            const int32_t s_new = s2 == GBNR_CONVERGED ? GBNR_FALLBACK_CONVERGED : s2;
-            const int32_t i_new = it[t] - 1 + i2;
-            CK(cudaSetDevice(opt.device));
-            CK(cudaMemcpyAsync(v.status + t, &s_new, 4, cudaMemcpyHostToDevice, stream));
-            CK(cudaMemcpyAsync(v.iters + t, &i_new, 4, cudaMemcpyHostToDevice, stream));
-            CK(cudaMemcpyAsync(v.maxmis + t, sub->v.maxmis, 8, cudaMemcpyDeviceToDevice, stream));
-            const size_t sp = size_t(sub->v.bpad) * 8;
-            for (auto [dst, src] : {std::pair{v.vm, sub->v.vm}, {v.va, sub->v.va}, {v.c, sub->v.c}, {v.s, sub->v.s}})
-                CK(cudaMemcpy2DAsync(dst + t, bp * 8, src, sp, 8, size_t(n), cudaMemcpyDeviceToDevice, stream));
-            CK(cudaStreamSynchronize(stream));  // before the sub-plan's buffers go
+        for (int32_t t = 0; t < nt; ++t) {
+            if (st[t] != GBNR_SINGULAR || opt.max_iter - (it[t] - 1) < 1) continue;
+            Chance c;
+            c.t = t;
+            c.it = it[t];
+            column(c.vm, v.vm + t, bp, n);
+            column(c.va, v.va + t, bp, n);
+            column(c.yr, v.yre + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
+            column(c.yi, v.yim + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
+            column(c.pp, v.p0 + size_t(t) * v.s_inc, size_t(v.s_ld), n);
+            column(c.qq, v.q0 + size_t(t) * v.s_inc, size_t(v.s_ld), n);
+            work.push_back(std::move(c));
+        }
+        CK(cudaStreamSynchronize(stream));
+        if (work.empty()) return;
+        // workers: host threads, bounded by the cores and by the device memory a
+        // one-task plan needs next to this batch
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t per_plan = bytes_per_tile(false) + size_t(64) << 20;
+        const size_t by_mem = free_b > (size_t(1) << 30) ? (free_b - (size_t(1) << 30)) / per_plan : 1;
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const size_t W = std::max<size_t>(1, std::min({work.size(), size_t(std::min(hw, 16u)), by_mem}));
+        std::atomic<size_t> next{0};
+        std::vector<std::exception_ptr> errs(W);
+        auto worker = [&](size_t w) {
+            try {
+                for (size_t i; (i = next.fetch_add(1)) < work.size();) run_chance(work[i]);
+            } catch (...) {
+                errs[w] = std::current_exception();
+                next = work.size();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (size_t w = 1; w < W; ++w) pool.emplace_back(worker, w);
+        worker(0);
+        for (auto& th : pool) th.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        // results -> this batch's device state (statuses, iterations, mismatch, V)
+        CK(cudaSetDevice(opt.device));
+        for (const Chance& c : work) {
+            if (!c.ran) continue;
+            const int32_t t = c.t;
+            CK(cudaMemcpy(v.status + t, &c.status, 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(v.iters + t, &c.iters, 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(v.maxmis + t, &c.mm, 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy2D(v.vm + t, bp * 8, c.vm.data(), 8, 8, size_t(n), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy2D(v.va + t, bp * 8, c.va.data(), 8, 8, size_t(n), cudaMemcpyHostToDevice));
         }
         gbnr::launch_status_count(v, stream);
         CK(cudaStreamSynchronize(stream));
+    }
+
+    // ---- gbnr_solve: shards over devices, chunks, re-derivation ----------------
+    struct SolveIn {
+        int32_t n_tasks;
+        const double *y_re, *y_im;
+        int32_t n_ysets;
+        const double *p0, *q0;
+        int32_t n_ssets;
+        const double *vm0, *va0;
+        int32_t n_vsets;
+    };
+    struct SolveOut {
+        double *vm, *va;
+        int32_t* it;
+        uint8_t* conv;
+        int32_t* st;
+        double* mm;
+    };
+
+    // timing of one run -> a running total ([5] total device ms and counts add up,
+    // [12] Newton iterations is the maximum)
+    static void add_timing(double* acc, const double* t) {
+        for (int i = 0; i < 24; ++i) acc[i] = i == 12 ? std::max(acc[i], t[i]) : acc[i] + t[i];
+    }
+
+    // Tasks [t0, t0 + T) of `in` on this device plan, in chunks of at most
+    // chunk_capacity() tasks; results into the same columns of `out`; per-task
+    // mismatch at V0 into mis0 and the count of tasks flagged at their first
+    // linear solve (the re-derivation rule) into *first.
+    void solve_slice(const SolveIn& in, const SolveOut& out, int32_t t0, int32_t T, double* mis0, int64_t* first,
+                     double* acc) {
+        CK(cudaSetDevice(opt.device));
+        const int64_t N = in.n_tasks;
+        const bool per_y = in.y_re && in.n_ysets > 1, per_s = in.n_ssets > 1, per_v = in.n_vsets > 1;
+        const int32_t cap = chunk_capacity(per_y);
+        const int32_t nch = (T + cap - 1) / cap;
+        const bool sliced = T != N || nch > 1;
+        for (int32_t ch = 0; ch < nch; ++ch) {
+            const int32_t a = t0 + int32_t(int64_t(T) * ch / nch), b = t0 + int32_t(int64_t(T) * (ch + 1) / nch);
+            const int32_t m = b - a;
+            if (sliced) {
+                stage_ybus(per_y ? in.y_re + a : in.y_re, per_y ? in.y_im + a : in.y_im, per_y ? m : 1, m,
+                           per_y ? N : 0);
+                stage(m, per_s ? in.p0 + a : in.p0, per_s ? in.q0 + a : in.q0, 1, per_v ? in.vm0 + a : in.vm0,
+                      per_v ? in.va0 + a : in.va0, 1, per_s ? N : 0, per_v ? N : 0);
+            } else {
+                stage_ybus(in.y_re, in.y_im, in.n_ysets, m);
+                stage(m, in.p0, in.q0, in.n_ssets, in.vm0, in.va0, in.n_vsets);
+            }
+            run(false);
+            *first += first_flagged;
+            CK(cudaMemcpy(mis0 + a, v.mis0, size_t(m) * 8, cudaMemcpyDeviceToHost));
+            if (opt.second_chance && h_count[66] > 0) second_chance();
+            count_statuses();
+            add_timing(acc, timing);
+            auto at = [&](auto* p) { return p ? p + a : p; };
+            fetch(at(out.vm), at(out.va), at(out.it), at(out.conv), at(out.st), at(out.mm), sliced ? N : 0);
+        }
+        whole_on_device = !sliced;
+    }
+
+    void solve_general(const SolveIn& in, const SolveOut& out, bool allow_rd) {
+        const int32_t N = in.n_tasks;
+        if (N <= 0) throw Error(GBNR_ECONFIG, "n_tasks must be positive");
+        if ((in.n_ssets != 1 && in.n_ssets != N) || (in.n_vsets != 1 && in.n_vsets != N))
+            throw Error(GBNR_ECONFIG, "set counts must be 1 or n_tasks");
+        if (in.y_re && in.y_im && in.n_ysets != 1 && in.n_ysets != N)
+            throw Error(GBNR_ECONFIG, "n_ysets must be 1 or n_tasks");
+        if ((!in.y_re || !in.y_im) && in.n_ysets != 1) throw Error(GBNR_ECONFIG, "per-task Ybus sets need y_re and y_im");
+        std::vector<gbnr_plan*> dev{this};
+        for (auto& q : peers) dev.push_back(q.get());
+        const size_t D = dev.size();
+        std::vector<double> mis0(size_t(N), 0.0);
+        std::vector<int64_t> first(D, 0);
+        std::vector<std::array<double, 24>> acc(D);
+        std::vector<std::exception_ptr> errs(D);
+        auto shard = [&](size_t d) {
+            try {
+                acc[d].fill(0.0);
+                const int32_t a = int32_t(int64_t(N) * int64_t(d) / int64_t(D));
+                const int32_t b = int32_t(int64_t(N) * int64_t(d + 1) / int64_t(D));
+                if (b > a) dev[d]->solve_slice(in, out, a, b - a, mis0.data(), &first[d], acc[d].data());
+            } catch (...) {
+                errs[d] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> th;
+        for (size_t d = 1; d < D; ++d) th.emplace_back(shard, d);
+        shard(0);
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        // shards ran concurrently: the job's device time is the slowest shard's
+        double agg[24] = {0};
+        for (size_t d = 0; d < D; ++d) {
+            const double ms = agg[5];
+            add_timing(agg, acc[d].data());
+            agg[5] = std::max(ms, acc[d][5]);
+        }
+        agg[13] = N;
+        std::memcpy(timing, agg, sizeof timing);
+        if (D > 1) whole_on_device = false;
+        int64_t ff = 0;
+        for (int64_t f : first) ff += f;
+        if (allow_rd && opt.second_chance && ff * 20 > N) rederive(in, out, mis0);
+    }
+
+    // Representative re-derivation (SPEC.md DESIGN DECISIONS): the frozen pivot
+    // order failed for more than 5% of the tasks at their first solve -> solve the
+    // batch again, once, from a plan whose pivots come from the task with the worst
+    // mismatch at V0 (its V0 and Ybus values).  A representative that is itself
+    // singular keeps the first results (their second chances are done).
+    void rederive(const SolveIn& in, const SolveOut& out, const std::vector<double>& mis0) {
+        const int32_t N = in.n_tasks, n = sym.n, nY = sym.nnzY;
+        int32_t w = 0;
+        for (int32_t t = 1; t < N; ++t)
+            if (mis0[t] > mis0[w]) w = t;  // first of the largest
+        std::vector<double> vm(n), va(n), yr(nY), yi(nY);
+        const int32_t vw = in.n_vsets == 1 ? 0 : w;
+        for (int32_t b = 0; b < n; ++b) {
+            vm[b] = in.vm0[size_t(b) * in.n_vsets + vw];
+            va[b] = in.va0[size_t(b) * in.n_vsets + vw];
+        }
+        if (in.y_re && in.y_im) {
+            const int32_t yw = in.n_ysets == 1 ? 0 : w;
+            for (int32_t q = 0; q < nY; ++q) {
+                yr[q] = in.y_re[size_t(q) * in.n_ysets + yw];
+                yi[q] = in.y_im[size_t(q) * in.n_ysets + yw];
+            }
+        } else {
+            yr = y_host_re;
+            yi = y_host_im;
+        }
+        gbnr_plan* alt = nullptr;
+        const int rc = create_plan(n, sym.yp.data(), sym.yi.data(), yr.data(), yi.data(), sym.ref, in_pv.data(),
+                                   int32_t(in_pv.size()), in_pq.data(), int32_t(in_pq.size()), vm.data(), va.data(),
+                                   &opt, &alt, false);
+        if (rc == GBNR_ESINGULAR) return;
+        if (rc != GBNR_OK) throw Error(rc, std::string("re-derivation: ") + gbnr_last_error());
+        std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(alt, gbnr_plan_destroy);
+        alt->solve_general(in, out, false);
+        std::memcpy(timing, alt->timing, sizeof timing);
+        timing[21] = 1;  // restarted from a re-derived representative
+        whole_on_device = false;
+        if (alt->whole_on_device && peers.empty()) {
+            // device state for gbnr_branch_flows: the restarted solve's voltages
+            CK(cudaSetDevice(opt.device));
+            const size_t nb = size_t(n) * size_t(v.bpad) * 8;
+            for (auto [dst, src] : {std::pair{v.vm, alt->v.vm}, {v.va, alt->v.va}})
+                CK(cudaMemcpy(dst, src, nb, cudaMemcpyDeviceToDevice));
+            const size_t nt = size_t(v.n_tasks);
+            CK(cudaMemcpy(v.status, alt->v.status, nt * 4, cudaMemcpyDeviceToDevice));
+            CK(cudaMemcpy(v.iters, alt->v.iters, nt * 4, cudaMemcpyDeviceToDevice));
+            CK(cudaMemcpy(v.maxmis, alt->v.maxmis, nt * 8, cudaMemcpyDeviceToDevice));
+            whole_on_device = true;
+        }
     }
 
     void ensure_pipe(int32_t n_tiles) {
@@ -623,10 +856,12 @@ struct gbnr_plan {
         pipe.clear();
         const size_t nb = size_t(sym.n) * size_t(n_tiles) * gbnr::kTile * sizeof(double);
         const size_t tb = size_t(n_tiles) * gbnr::kTile;
+        pipe_bytes = 0;
         auto alloc = [&](size_t bytes) {
             void* q = nullptr;
             CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
             pipe.push_back(q);
+            pipe_bytes += bytes;
             return q;
         };
         for (int i = 0; i < 2; ++i) {
@@ -723,21 +958,26 @@ struct gbnr_plan {
         staged = false;  // the device tapes no longer hold a staged batch
     }
 
+    // Results to the host.  ld > 0: vm / va go to columns [0, n_tasks) of host
+    // arrays [n][ld] (a slice of a larger batch; the caller offsets the pointers).
     void fetch(double* vm, double* va, int32_t* iters, uint8_t* conv, int32_t* status,
-               double* maxmis) {
+               double* maxmis, int64_t ld = 0) {
         CK(cudaSetDevice(opt.device));
         const int32_t nt = v.n_tasks;
-        const size_t row = size_t(nt) * 8, bytes = size_t(sym.n) * row;
-        if (vm || va) ensure_pipe(v.n_tiles);
-        // pack [n][bpad] -> [n][n_tasks] on the device, then one linear D2H each
-        if (vm) {
-            gbnr::launch_pack(out_vm[0], v.vm, sym.n, nt, v.bpad, stream);
-            CK(cudaMemcpyAsync(vm, out_vm[0], bytes, cudaMemcpyDeviceToHost, stream));
-        }
-        if (va) {
-            gbnr::launch_pack(out_va[0], v.va, sym.n, nt, v.bpad, stream);
-            CK(cudaMemcpyAsync(va, out_va[0], bytes, cudaMemcpyDeviceToHost, stream));
-        }
+        const size_t row = size_t(nt) * 8;
+        // pack [n][bpad] -> [n][n_tasks] on the device into the phasor tapes (free
+        // after a solve: the next run recomputes them, flows read the angles), then
+        // one linear (or pitched, for a slice) D2H each
+        auto d2h = [&](double* dst, double* packed, const double* src) {
+            gbnr::launch_pack(packed, src, sym.n, nt, v.bpad, stream);
+            if (ld <= 0 || ld == nt)
+                CK(cudaMemcpyAsync(dst, packed, size_t(sym.n) * row, cudaMemcpyDeviceToHost, stream));
+            else
+                CK(cudaMemcpy2DAsync(dst, size_t(ld) * 8, packed, row, row, size_t(sym.n), cudaMemcpyDeviceToHost,
+                                     stream));
+        };
+        if (vm) d2h(vm, v.c, v.vm);
+        if (va) d2h(va, v.s, v.va);
         std::vector<int32_t> st(nt);
         CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
         if (iters) CK(cudaMemcpyAsync(iters, v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
@@ -752,6 +992,9 @@ struct gbnr_plan {
     void branch_flows(int32_t nb, const int32_t* bf, const int32_t* bt, const double* adm, const int32_t* outage,
                       double* sfr, double* sfi, double* str, double* sti) {
         if (!solved) throw Error(GBNR_ECONFIG, "gbnr_branch_flows before a solve");
+        if (!whole_on_device)
+            throw Error(GBNR_ECONFIG, "the last solve was sharded over devices or chunked: the device does not hold "
+                                      "every task's voltages (solve with n_devices = 1 and a batch that fits)");
         CK(cudaSetDevice(opt.device));
         const size_t T = size_t(v.n_tasks), out_bytes = size_t(nb) * T * 8;
         std::vector<void*> tmp;
@@ -828,13 +1071,14 @@ struct gbnr_plan {
         if (flags_out) CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
         if (lu_out) {
             // tile-blocked tape -> element-major CCS order [nnzLU][n_tasks]
-            const size_t z = size_t(v.nnzLU);
-            std::vector<double> tape(size_t(v.n_tiles) * v.tstride);
-            CK(cudaMemcpy(tape.data(), v.A, tape.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            const size_t z = size_t(v.nnzLU), tr = size_t(v.tape_rows) * gbnr::kTile;
+            std::vector<double> tape(size_t(v.n_tiles) * tr);  // the LU part of every tile's block
+            CK(cudaMemcpy2D(tape.data(), tr * 8, v.LU, v.tstride * 8, tr * 8, size_t(v.n_tiles),
+                            cudaMemcpyDeviceToHost));
             for (size_t c = 0; c < z; ++c) {
-                const size_t ts = size_t(v.tape_rows) + size_t(lay.tape_of_ccs[c]);  // LU rows follow the A rows
+                const size_t ts = size_t(lay.tape_of_ccs[c]);
                 for (int32_t t = 0; t < nt; ++t)
-                    lu_out[c * nt + t] = tape[size_t(t / gbnr::kTile) * v.tstride + ts * gbnr::kTile + t % gbnr::kTile];
+                    lu_out[c * nt + t] = tape[size_t(t / gbnr::kTile) * tr + ts * gbnr::kTile + t % gbnr::kTile];
             }
         }
     }
@@ -856,7 +1100,10 @@ void gbnr_default_options(gbnr_options* o) {
     o->headroom = 1;
     o->walkers = 8;
     o->jacobian = 0;
-    o->second_chance = 16;
+    o->second_chance = 1;
+    o->n_devices = 1;
+    o->device_step = 1;
+    o->chunk_tasks = 0;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -924,10 +1171,12 @@ int gbnr_amd_order(int32_t n, const int32_t* col_ptr, const int32_t* row_ix, int
     });
 }
 
-int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indices,
-                     const double* y_re, const double* y_im, int32_t ref, const int32_t* pv,
-                     int32_t n_pv, const int32_t* pq, int32_t n_pq, const double* vm0,
-                     const double* va0, const gbnr_options* opt, gbnr_plan** out) {
+}  // extern "C"
+
+static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indices, const double* y_re,
+                       const double* y_im, int32_t ref, const int32_t* pv, int32_t n_pv, const int32_t* pq,
+                       int32_t n_pq, const double* vm0, const double* va0, const gbnr_options* opt, gbnr_plan** out,
+                       bool sub) {
     *out = nullptr;
     gbnr_plan* p = new (std::nothrow) gbnr_plan();
     if (!p) {
@@ -946,6 +1195,9 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             throw Error(GBNR_ECONFIG, "negative walk parameter");
         if (p->opt.jacobian < 0 || p->opt.jacobian > 2) throw Error(GBNR_ECONFIG, "jacobian policy must be 0, 1 or 2");
         if (p->opt.second_chance < 0) throw Error(GBNR_ECONFIG, "second_chance must be >= 0");
+        if (p->opt.n_devices < 0 || p->opt.n_devices > 64 || p->opt.device_step < 0 || p->opt.chunk_tasks < 0)
+            throw Error(GBNR_ECONFIG, "need 0 <= n_devices <= 64, device_step >= 0, chunk_tasks >= 0");
+        p->sub_plan = sub;
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
         p->in_pv.assign(pv, pv + n_pv);
@@ -976,7 +1228,7 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
         }
         auto build_walks = [&] {
             p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
-            p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
+            if (!sub) p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
             gbnr::WalkConfig wcb = wc;
             if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
             p->wb = gbnr::build_backward_walk(p->sym, p->lay, wcb);
@@ -999,6 +1251,32 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
             p->on_device = true;
             p->upload_structure();
             p->set_ybus(y_re, y_im);
+            // n_devices > 1: the same frozen symbolic state and walk programs on
+            // devices device + i * device_step, one plan each
+            const int32_t nd = std::max(1, p->opt.n_devices);
+            for (int32_t i = 1; i < nd; ++i) {
+                const int32_t d = p->opt.device + i * p->opt.device_step;
+                if (d >= ndev) throw Error(GBNR_ECUDA, "n_devices: CUDA device ordinal out of range");
+                auto q = std::make_unique<gbnr_plan>();
+                q->sym = p->sym;
+                q->in_pv = p->in_pv;
+                q->in_pq = p->in_pq;
+                q->lay = p->lay;
+                q->wf = p->wf;
+                q->wl = p->wl;
+                q->wb = p->wb;
+                q->opt = p->opt;
+                q->opt.device = d;
+                q->opt.n_devices = 1;
+                q->sub_plan = sub;
+                CK(cudaSetDevice(d));
+                gbnr::configure_kernels();
+                q->on_device = true;
+                q->upload_structure();
+                q->set_ybus(y_re, y_im);
+                p->peers.push_back(std::move(q));
+            }
+            CK(cudaSetDevice(p->opt.device));
         }
     });
     if (rc != GBNR_OK) {
@@ -1007,6 +1285,15 @@ int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indice
     }
     *out = p;
     return GBNR_OK;
+}
+
+extern "C" {
+
+int gbnr_plan_create(int32_t n_bus, const int32_t* indptr, const int32_t* indices,
+                     const double* y_re, const double* y_im, int32_t ref, const int32_t* pv,
+                     int32_t n_pv, const int32_t* pq, int32_t n_pq, const double* vm0,
+                     const double* va0, const gbnr_options* opt, gbnr_plan** out) {
+    return create_plan(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0, opt, out, false);
 }
 
 void gbnr_plan_destroy(gbnr_plan* plan) { delete plan; }
@@ -1061,27 +1348,12 @@ int gbnr_solve(gbnr_plan* p, int32_t n_tasks, const double* y_re, const double* 
                double* va_out, int32_t* iterations_out, uint8_t* converged_out,
                int32_t* status_out, double* max_mismatch_out) {
     return guarded([&] {
-        if (n_ssets < 1) throw Error(GBNR_ECONFIG, "n_ssets must be 1 or n_tasks");
         if (!p->on_device) throw Error(GBNR_ECONFIG, "host-only plan (device = -1) cannot solve");
-        CK(cudaSetDevice(p->opt.device));
-        p->stage_ybus(y_re, y_im, n_ysets, n_tasks);
-        p->stage(n_tasks, p0, q0, n_ssets, vm0, va0, n_vsets);
-        p->allow_rederive = !y_re || n_ysets == 1;  // N-1 batches: islanded tasks dominate the flags
-        p->rederive_pending = false;
-        try {
-            p->run();
-        } catch (...) {
-            p->allow_rederive = false;
-            throw;
-        }
-        p->allow_rederive = false;
-        if (p->rederive_pending) {
-            p->rederive_pending = false;
-            p->rederive_and_solve(n_tasks, y_re, y_im, n_ysets, p0, q0, n_ssets, vm0, va0, n_vsets, vm_out,
-                                  va_out, iterations_out, converged_out, status_out, max_mismatch_out);
-            return;
-        }
-        p->fetch(vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out);
+        const gbnr_plan::SolveIn in{n_tasks, y_re, y_im, n_ysets, p0, q0, n_ssets, vm0, va0, n_vsets};
+        const gbnr_plan::SolveOut out{vm_out, va_out, iterations_out, converged_out, status_out, max_mismatch_out};
+        // N-1 batches (per-task Ybus sets): islanded tasks dominate the flags, no re-derivation
+        p->solve_general(in, out, !y_re || n_ysets == 1);
+        p->solved = true;
     });
 }
 
@@ -1092,8 +1364,45 @@ int gbnr_solve_batches(gbnr_plan* p, int32_t n_batches, int32_t n_tasks, const d
     return guarded([&] {
         for (int32_t i = 0; i < n_batches; ++i)
             if (!p0 || !q0 || !p0[i] || !q0[i]) throw Error(GBNR_ECONFIG, "every batch needs p0 and q0");
-        p->solve_batches(n_batches, n_tasks, p0, q0, vm0, va0, vm_out, va_out, iterations_out, converged_out,
-                         status_out, max_mismatch_out);
+        if (p->peers.empty()) {
+            p->solve_batches(n_batches, n_tasks, p0, q0, vm0, va0, vm_out, va_out, iterations_out, converged_out,
+                             status_out, max_mismatch_out);
+            return;
+        }
+        // n_devices > 1: batches dealt round-robin, each device pipelines its own
+        // share from its own host thread
+        std::vector<gbnr_plan*> dev{p};
+        for (auto& q : p->peers) dev.push_back(q.get());
+        const size_t D = dev.size();
+        std::vector<std::exception_ptr> errs(D);
+        auto pick = [&](auto* const* a, size_t d) {
+            std::vector<std::remove_const_t<std::remove_pointer_t<decltype(a)>>> o;
+            for (int32_t j = int32_t(d); j < n_batches; j += int32_t(D)) o.push_back(a ? a[j] : nullptr);
+            return o;
+        };
+        auto shard = [&](size_t d) {
+            try {
+                auto P = pick(p0, d);
+                auto Q = pick(q0, d);
+                auto VM = pick(vm_out, d);
+                auto VA = pick(va_out, d);
+                auto IT = pick(iterations_out, d);
+                auto CV = pick(converged_out, d);
+                auto ST = pick(status_out, d);
+                auto MM = pick(max_mismatch_out, d);
+                if (!P.empty())
+                    dev[d]->solve_batches(int32_t(P.size()), n_tasks, P.data(), Q.data(), vm0, va0, VM.data(),
+                                          VA.data(), IT.data(), CV.data(), ST.data(), MM.data());
+            } catch (...) {
+                errs[d] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> th;
+        for (size_t d = 1; d < D; ++d) th.emplace_back(shard, d);
+        shard(0);
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
     });
 }
 

@@ -49,7 +49,8 @@ class Options(C.Structure):
                 ("singular_tol", C.c_double), ("device", C.c_int32), ("ring_rows", C.c_int32),
                 ("profile", C.c_int32), ("stage_rows", C.c_int32),
                 ("prefetch", C.c_int32), ("headroom", C.c_int32), ("walkers", C.c_int32),
-                ("jacobian", C.c_int32), ("second_chance", C.c_int32)]
+                ("jacobian", C.c_int32), ("second_chance", C.c_int32),
+                ("n_devices", C.c_int32), ("device_step", C.c_int32), ("chunk_tasks", C.c_int32)]
 
 
 _lib = None

@@ -86,3 +86,85 @@ def test_newtonpf_batch_matches_scipy_newtonpf(name, T):
         p0, q0, vm0[:, None], va0[:, None], n_tasks=T)
     np.testing.assert_array_equal(it, o["iterations"])
     np.testing.assert_array_equal(V, o["vm"] * np.exp(1j * o["va"]))
+
+
+def _plan(gc, **opts):
+    ip, ix, _, yr, yi = S.build_ybus(gc)
+    vm0, va0 = gc.v_start()
+    return S.NrPlan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0, device=0, **opts), vm0, va0
+
+
+def _same(a, b):
+    for k in ("vm", "va", "iterations", "converged", "status", "max_mismatch"):
+        np.testing.assert_array_equal(getattr(a, k), getattr(b, k), err_msg=k)
+
+
+@pytest.mark.parametrize("opts", [dict(n_devices=2, device_step=0), dict(chunk_tasks=64),
+                                  dict(n_devices=3, device_step=0, chunk_tasks=40)])
+def test_sharded_and_chunked_solves_match_single(opts):
+    """gbnr_options.n_devices / chunk_tasks (one batch slice and
+    stream per device, chunk a batch that does not fit): contiguous shards (here
+    several plans on device 0 standing in for several GPUs) and chunks return
+    exactly what one launch returns -- Monte-Carlo, per-task start voltages, N-1
+    per-task Ybus sets, and the batch pipeline."""
+    gc = load_case(util.case_path("synth300"))
+    base, vm0, va0 = _plan(gc)
+    multi, _, _ = _plan(gc, **opts)
+    T = 250
+    p0, q0 = montecarlo(gc, T)
+    _same(multi.solve(p0, q0, vm0, va0), base.solve(p0, q0, vm0, va0))
+    rng = np.random.default_rng(2)
+    vmT = vm0[:, None] * (1 + 0.001 * rng.standard_normal((gc.n_bus, T)))
+    vaT = va0[:, None] + 0.001 * rng.standard_normal((gc.n_bus, T))
+    _same(multi.solve(p0, q0, vmT, vaT), base.solve(p0, q0, vmT, vaT))
+    outages = rng.integers(0, gc.n_branch, T).astype(np.int32)
+    yre, yim, _ = S.contingency_values(gc, outages)
+    _same(multi.solve(p0, q0, vm0, va0, y=(yre, yim)), base.solve(p0, q0, vm0, va0, y=(yre, yim)))
+    batches = [montecarlo(gc, 96, task0=i * 96) for i in range(3)]
+    outs_m = multi.solve_batches([b[0] for b in batches], [b[1] for b in batches], vm0, va0)
+    outs_b = base.solve_batches([b[0] for b in batches], [b[1] for b in batches], vm0, va0)
+    for a, b in zip(outs_m, outs_b):
+        _same(a, b)
+    if opts.get("n_devices", 1) > 1 or opts.get("chunk_tasks", 0) < T:
+        with pytest.raises(S.GbnrError):  # the device holds only the last shard / chunk
+            multi.solve(p0, q0, vm0, va0)
+            multi.branch_flows(gc)
+
+
+@pytest.mark.parametrize("opts", [dict(chunk_tasks=16), dict(n_devices=2, device_step=0, chunk_tasks=3)])
+def test_second_chance_and_rederivation_survive_chunking(opts):
+    """The second chance is per task and the >5% re-derivation rule is decided over
+    the whole batch, so chunked / sharded solves equal the one-launch solve and
+    the oracle (DESIGN DECISIONS)."""
+    from test_oracle_nr import _two_bus_instability
+    for T in (40, 8):  # 40: one flagged task (second chance); 8: 1/8 > 5% (re-derivation)
+        args, p0, q0, vm, va = _two_bus_instability(T=T, special=3)
+        ip, ix, yr, yi, ref, pv, pq, vm0, va0 = args
+        base = S.NrPlan(2, ip, ix, yr, yi, ref, pv, pq, vm0, va0, device=0)
+        multi = S.NrPlan(2, ip, ix, yr, yi, ref, pv, pq, vm0, va0, device=0, **opts)
+        r = multi.solve(p0, q0, vm, va, n_tasks=T)
+        _same(r, base.solve(p0, q0, vm, va, n_tasks=T))
+        _compare(r, po.Oracle().plan(2, *args).solve(p0, q0, vm, va, n_tasks=T))
+        if T == 8:
+            assert multi.timing()["rederived"] == 1
+
+
+def test_50k_synth9241_solve_on_one_gpu():
+    """A 50k-task synth9241 batch (one GPU's half of configs[4]'s 100k at N = 2) is
+    more than one B200's HBM holds as tapes (about 139 MB per 32 tasks): gbnr_solve
+    chunks it automatically.  Tasks repeat a 2,000-task Monte-Carlo batch 25 times,
+    so every task must equal its copy in a direct 2,000-task solve bit for bit."""
+    gc = load_case(util.case_path("synth9241"))
+    plan, vm0, va0 = _plan(gc)
+    B, K = 2000, 25
+    pb, qb = montecarlo(gc, B)
+    one = plan.solve(pb, qb, vm0, va0)
+    p0, q0 = np.tile(pb, (1, K)), np.tile(qb, (1, K))
+    r = plan.solve(p0, q0, vm0, va0, n_tasks=B * K)
+    del p0, q0
+    assert (r.status == 0).all()
+    for k in range(K):
+        sl = slice(k * B, (k + 1) * B)
+        np.testing.assert_array_equal(r.vm[:, sl], one.vm)
+        np.testing.assert_array_equal(r.va[:, sl], one.va)
+        np.testing.assert_array_equal(r.iterations[sl], one.iterations)

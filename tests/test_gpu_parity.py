@@ -361,7 +361,7 @@ def test_dense_grids_plan_and_match_oracle(name, extra, T):
         assert plan.walk_info(0)["global_steps"] > 0
 
 
-@pytest.mark.parametrize("frac", ["0.3", "0.05"])
+@pytest.mark.parametrize("frac", ["0.2", "0.05"])
 def test_global_forms_match_oracle(frac, monkeypatch):
     """Blocks / fetches forced into global memory on a grid that fits (the
     fallback's code paths, GBNR_GLOBAL_FRAC): NR solve and the LU-only
