@@ -25,8 +25,13 @@ oracle:
 ref:
 	$(MAKE) -s -C oracle ref
 
+# walker time breakdown build (GBNR_DBG=8 prints per-phase cycle shares; tools/gpu_quick.py)
+prof: $(PKG)/libgbnr_prof.so
+$(PKG)/libgbnr_prof.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -DGBNR_PROF -shared -o $@ $(SRCS) 2> $(PKG)/build_prof.log || (cat $(PKG)/build_prof.log; false)
+
 clean:
-	rm -f $(LIB) $(PKG)/build.log
+	rm -f $(LIB) $(PKG)/libgbnr_prof.so $(PKG)/build.log $(PKG)/build_prof.log
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref prof clean

@@ -82,8 +82,11 @@ def test_newtonpf_batch_matches_scipy_newtonpf(name, T):
         assert oks == bool(ok[t]) and its == int(it[t])
         assert np.abs(np.abs(Vs) - np.abs(V[:, t])).max() <= 1e-8
         assert np.abs(np.angle(Vs) - np.angle(V[:, t])).max() <= 1e-8
-    o = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vm0, va0).solve(
-        p0, q0, vm0[:, None], va0[:, None], n_tasks=T)
+    # the oracle on the same inputs: the start voltages as the call sees them, |V0| and angle(V0)
+    # (one ulp off vm0 / va0 after the round trip through complex V0)
+    vs, as_ = np.abs(V0), np.angle(V0)
+    o = po.Oracle().plan(gc.n_bus, ip, ix, yr, yi, gc.slack, gc.pv, gc.pq, vs, as_).solve(
+        p0, q0, vs[:, None], as_[:, None], n_tasks=T)
     np.testing.assert_array_equal(it, o["iterations"])
     np.testing.assert_array_equal(V, o["vm"] * np.exp(1j * o["va"]))
 
