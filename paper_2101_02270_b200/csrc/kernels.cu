@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.y * kSuper + warp;
     if (tile >= v.n_tiles) return;
-    const int t = tile * kTile + lane;
+    const int t = tile * v.tw + min(lane, v.tw - 1);
     const bool real = t < v.n_tasks;
     const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
     for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
         v.mis_prev[t] = INFINITY;
         v.jskip[t] = 0;
         v.norm_bits[t] = 0ull;
-        const int cnt = __popc(__ballot_sync(kFull, real));
+        const int cnt = __popc(__ballot_sync(kFull, real && lane < v.tw));
         if (lane == 0) v.tile_active[tile] = cnt;
         if (t == 0) *v.it_dev = 0;
     }
@@ -96,14 +96,17 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
     return isfinite(n2) && n1 * n1 * n1 < v.tol * n2 * n2;
 }
 
-template <bool NPM, int JMODE>
+// TW_: the tile width as a compile-time constant (8 / 16 / 24 / 32: no register
+// for it under the 5-blocks-per-SM budget), 0 = read from the view.
+template <bool NPM, int JMODE, int TW_>
 __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = my_tile(v, blockIdx.y, warp);
     if (tile < 0) return;
-    const int t = tile * kTile + lane;
+    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);
+    const int t = tile * TW + le;
     const size_t bp = v.bpad;
-    double* a_t = v.A + size_t(tile) * v.tstride + lane;  // tile-blocked A tape
+    double* a_t = v.A + size_t(tile) * v.tstride + le;  // tile-blocked A tape
     const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
     bool act = JMODE != kJacNone && v.active[t] != 0;
     if (JMODE == kJacSpec) {
@@ -134,12 +137,12 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
         if (NPM) {
             const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
             const double fp = P - __ldg(v.p0 + size_t(r) * v.s_ld + ts);
-            a_t[size_t(__ldg(v.fslot_p + r)) * kTile] = fp;  // F beside its A column
+            a_t[size_t(__ldg(v.fslot_p + r)) * TW] = fp;  // F beside its A column
             nrm = fmax(nrm, nan_as_inf_abs(fp));
             const int fq_slot = __ldg(v.fslot_q + r);
             if (fq_slot >= 0) {
                 const double fq = Q - __ldg(v.q0 + size_t(r) * v.s_ld + ts);
-                a_t[size_t(fq_slot) * kTile] = fq;
+                a_t[size_t(fq_slot) * TW] = fq;
                 nrm = fmax(nrm, nan_as_inf_abs(fq));
             }
         }
@@ -151,10 +154,10 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
                 jac_z(__ldg(v.yre + size_t(q) * v.y_ld + yt), __ldg(v.yim + size_t(q) * v.y_ld + yt), vre, vim, ck, sk, zre, zim);
                 jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
                 const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
-                if (l.x >= 0) a_t[size_t(l.x) * kTile] = j[0];
-                if (l.y >= 0) a_t[size_t(l.y) * kTile] = j[1];
-                if (l.z >= 0) a_t[size_t(l.z) * kTile] = j[2];
-                if (l.w >= 0) a_t[size_t(l.w) * kTile] = j[3];
+                if (l.x >= 0) a_t[size_t(l.x) * TW] = j[0];
+                if (l.y >= 0) a_t[size_t(l.y) * TW] = j[1];
+                if (l.z >= 0) a_t[size_t(l.z) * TW] = j[2];
+                if (l.w >= 0) a_t[size_t(l.w) * TW] = j[3];
             }
         }
     }
@@ -166,7 +169,8 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.x * kSuper + warp;
     if (tile >= v.n_tiles) return;
-    const int t = tile * kTile + lane;
+    const bool in = lane < v.tw;  // lanes >= tw shadow lane tw - 1: counted once
+    const int t = tile * v.tw + min(lane, v.tw - 1);
     const int it = *v.it_dev;
     const double m = __longlong_as_double(static_cast<long long>(v.norm_bits[t]));
     v.norm_bits[t] = 0ull;
@@ -187,8 +191,8 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
             act = false;
         }
     }
-    const int cnt = __popc(__ballot_sync(kFull, act));
-    const int nj = __popc(__ballot_sync(kFull, act && v.jskip[t] != 0));
+    const int cnt = __popc(__ballot_sync(kFull, act && in));
+    const int nj = __popc(__ballot_sync(kFull, act && in && v.jskip[t] != 0));
     if (lane == 0) {
         v.tile_active[tile] = cnt;
         if (cnt) {
@@ -309,6 +313,7 @@ struct Prog {
     const int32_t* cur;         // next record
     const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
     int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
+    int RB;                     // bytes per row: tile width x 8
     int W, n_pages, page;
 };
 
@@ -353,7 +358,7 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
                                            int lane) {
     extern __shared__ __align__(128) unsigned char walk_smem[];
     P.R = reinterpret_cast<double*>(walk_smem);
-    unsigned char* mine = walk_smem + size_t(w.rows) * kTile * 8 +
+    unsigned char* mine = walk_smem + size_t(w.rows) * size_t(w.tw) * 8 +
                           size_t(warp) * (size_t(kWalkPages) * w.page_words * 4 + (kWalkBars + kWalkPages) * 8);
     P.pg = reinterpret_cast<int32_t*>(mine);
     P.bar = reinterpret_cast<unsigned long long*>(mine + size_t(kWalkPages) * w.page_words * 4);
@@ -365,6 +370,7 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.cur = P.pg;
     P.tb = reinterpret_cast<const char*>(v.A + size_t(tile) * v.tstride);
     P.tape_rows = v.tape_rows;
+    P.RB = v.tw * 8;
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
     __syncwarp();  // every lane's barrier is initialised before lane 0 arms the page barriers
@@ -399,18 +405,19 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
     fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
     unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
     __syncwarp();
-    if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]));
+    const unsigned RB = unsigned(P.RB);
+    if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]) * RB);  // rows -> bytes
     // one copy per lane; a copy may complete before lane 0's arrive.expect_tx (the
     // barrier's tx-count dips below zero, its phase cannot complete without the arrive)
     const unsigned rbase = smem_u32(P.R), ubar = smem_u32(bar);
     for (int i = lane; i < ncopy; i += 32) {
         const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
         const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
-        const char* src = P.tb + size_t(unsigned((c & 3) * P.tape_rows + slot)) * (kTile * 8);
+        const char* src = P.tb + size_t(unsigned((c & 3) * P.tape_rows + slot)) * RB;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                rbase + smem * (kTile * 8u)),
-            "l"(src), "r"(rows * (kTile * 8u)), "r"(ubar)
+                rbase + smem * RB),
+            "l"(src), "r"(rows * RB), "r"(ubar)
             : "memory");
     }
     return 3 + 2 * ncopy;
@@ -430,10 +437,11 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    double* lu_t = v.LU + size_t(tile) * v.tstride + lane;
+    const int TW = v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
+    double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const double stol = v.singular_tol;
-    constexpr unsigned RB = kTile * 8;  // bytes per shared row
-    const unsigned R0 = smem_u32(P.R) + unsigned(lane) * 8u;
+    const unsigned RB = unsigned(TW) * 8u;  // bytes per shared / tape row
+    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
     bool flagged = false;
     unsigned xs = R0;  // this step's block
     int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
@@ -603,7 +611,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             PROF_MARK(0)
             PROF_CNT(3)
             xs = R0 + unsigned(ring) * RB;
-            xg = P.R + size_t(ring) * kTile + lane;
+            xg = P.R + size_t(ring) * TW + le;
             acc_y = FS ? lds(xs + unsigned(len) * RB) : 0.0;
         } else if (type == kRecEnd) {
             h = r[1 + dp];
@@ -613,7 +621,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const double piv = lds(xs + unsigned(dp) * RB);
             const double inv = 1.0 / piv;
             double c0 = fabs(piv), c1 = 0.0;
-            double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * kTile;  // L row z of x at lcol[z], y at lcol[len]
+            double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * TW;  // L row z of x at lcol[z], y at lcol[len]
             int z = dp + 1;
             for (; z + 2 <= len; z += 2) {
                 const double x0 = lds(xs + unsigned(z) * RB), x1 = lds(xs + unsigned(z + 1) * RB);
@@ -622,15 +630,15 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 const double l0 = x0 * inv, l1 = x1 * inv;
                 sts(xs + unsigned(z) * RB, l0);
                 sts(xs + unsigned(z + 1) * RB, l1);
-                lcol[size_t(z) * kTile] = l0;
-                lcol[size_t(z + 1) * kTile] = l1;
+                lcol[size_t(z) * TW] = l0;
+                lcol[size_t(z + 1) * TW] = l1;
             }
             if (z < len) {
                 const double x0 = lds(xs + unsigned(z) * RB);
                 c0 = fmax(c0, fabs(x0));
                 const double l0 = x0 * inv;
                 sts(xs + unsigned(z) * RB, l0);
-                lcol[size_t(z) * kTile] = l0;
+                lcol[size_t(z) * TW] = l0;
             }
             z = 0;
             for (; z + 4 <= dp; z += 4) {  // U part -> its row-major slots
@@ -641,23 +649,23 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 c1 = fmax(c1, fabs(u1));
                 c0 = fmax(c0, fabs(u2));
                 c1 = fmax(c1, fabs(u3));
-                lu_t[size_t(s0) * kTile] = u0;
-                lu_t[size_t(s1) * kTile] = u1;
-                lu_t[size_t(s2) * kTile] = u2;
-                lu_t[size_t(s3) * kTile] = u3;
+                lu_t[size_t(s0) * TW] = u0;
+                lu_t[size_t(s1) * TW] = u1;
+                lu_t[size_t(s2) * TW] = u2;
+                lu_t[size_t(s3) * TW] = u3;
             }
             for (; z < dp; ++z) {
                 const double u0 = lds(xs + unsigned(z) * RB);
                 c0 = fmax(c0, fabs(u0));
-                lu_t[size_t(r[1 + z]) * kTile] = u0;
+                lu_t[size_t(r[1 + z]) * TW] = u0;
             }
             const double cmax = fmax(c0, c1);
             flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
-            lu_t[size_t(brow + 1) * kTile] = piv;  // U(m,m) closing the backward block
+            lu_t[size_t(brow + 1) * TW] = piv;  // U(m,m) closing the backward block
             if (FS) {  // y_m after the L rows (forward re-fetches) and in the backward block
                 sts(xs + unsigned(len) * RB, acc_y);
-                lcol[size_t(len) * kTile] = acc_y;
-                lu_t[size_t(brow) * kTile] = acc_y;
+                lcol[size_t(len) * TW] = acc_y;
+                lu_t[size_t(brow) * TW] = acc_y;
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1 + dp;
@@ -673,10 +681,10 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             const int kpos_fs = r[1], nrows = r[2], slot = r[3], nl = r[4];
             h = r[5 + ((nrows + 1) >> 1)];
             if (op >= 0) prog_wait(P, op);
-            const double* src = lu_t + size_t(slot) * kTile;
+            const double* src = lu_t + size_t(slot) * TW;
             const int fspos = int(unsigned(kpos_fs) >> 16);
             if (nrows > 0) {
-                const double mult = xg[size_t(kpos_fs & 0xffff) * kTile];
+                const double mult = xg[size_t(kpos_fs & 0xffff) * TW];
                 const int32_t* dw = r + 5;
                 int q = 0;
 #pragma unroll 1
@@ -690,19 +698,19 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                         d[u + 1] = int(unsigned(wq) >> 16);
                     }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) l[u] = src[size_t(q + u) * kTile];
+                    for (int u = 0; u < 8; ++u) l[u] = src[size_t(q + u) * TW];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) a[u] = xg[size_t(d[u]) * kTile];
+                    for (int u = 0; u < 8; ++u) a[u] = xg[size_t(d[u]) * TW];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) xg[size_t(d[u]) * kTile] = fma(-mult, l[u], a[u]);
+                    for (int u = 0; u < 8; ++u) xg[size_t(d[u]) * TW] = fma(-mult, l[u], a[u]);
                 }
                 for (; q < nrows; ++q) {
                     const int32_t wq = dw[q >> 1];
                     const int d = (q & 1) ? int(unsigned(wq) >> 16) : (wq & 0xffff);
-                    xg[size_t(d) * kTile] = fma(-mult, src[size_t(q) * kTile], xg[size_t(d) * kTile]);
+                    xg[size_t(d) * TW] = fma(-mult, src[size_t(q) * TW], xg[size_t(d) * TW]);
                 }
             }
-            if (FS && fspos != 0xffff) acc_y = fma(-src[size_t(fspos) * kTile], src[size_t(nl) * kTile], acc_y);
+            if (FS && fspos != 0xffff) acc_y = fma(-src[size_t(fspos) * TW], src[size_t(nl) * TW], acc_y);
             P.cur += 5 + ((nrows + 1) >> 1);
         } else if (type == kRecStepG) {
             // a column too large for the pool: A rows + F into this walker's scratch
@@ -713,19 +721,19 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             brow = r[4];
             h = r[5];
             P.cur += 5;
-            xg = v.scratch + (size_t(tile) * 8 + warp) * size_t(v.scratch_rows) * kTile + lane;
-            const double* at = v.A + size_t(tile) * v.tstride + lane + size_t(a0) * kTile;
+            xg = v.scratch + (size_t(tile) * 8 + warp) * size_t(v.scratch_rows) * TW + le;
+            const double* at = v.A + size_t(tile) * v.tstride + le + size_t(a0) * TW;
             int z = 0;
 #pragma unroll 1
             for (; z + 8 <= len + 1; z += 8) {  // loads grouped ahead of the stores
                 double a[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) a[u] = at[size_t(z + u) * kTile];
+                for (int u = 0; u < 8; ++u) a[u] = at[size_t(z + u) * TW];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) xg[size_t(z + u) * kTile] = a[u];
+                for (int u = 0; u < 8; ++u) xg[size_t(z + u) * TW] = a[u];
             }
-            for (; z <= len; ++z) xg[size_t(z) * kTile] = at[size_t(z) * kTile];
-            acc_y = FS ? xg[size_t(len) * kTile] : 0.0;
+            for (; z <= len; ++z) xg[size_t(z) * TW] = at[size_t(z) * TW];
+            acc_y = FS ? xg[size_t(len) * TW] : 0.0;
             gmax = 0.0;
         } else if (type == kRecEndU) {
             // U entries z0 .. z0+cnt-1 of a global step -> their row-major slots
@@ -736,48 +744,48 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             for (; i + 8 <= cnt; i += 8) {
                 double u[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) u[k] = xg[size_t(z0 + i + k) * kTile];
+                for (int k = 0; k < 8; ++k) u[k] = xg[size_t(z0 + i + k) * TW];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     gmax = fmax(gmax, fabs(u[k]));
-                    lu_t[size_t(r[2 + i + k]) * kTile] = u[k];
+                    lu_t[size_t(r[2 + i + k]) * TW] = u[k];
                 }
             }
             for (; i < cnt; ++i) {
-                const double u = xg[size_t(z0 + i) * kTile];
+                const double u = xg[size_t(z0 + i) * TW];
                 gmax = fmax(gmax, fabs(u));
-                lu_t[size_t(r[2 + i]) * kTile] = u;
+                lu_t[size_t(r[2 + i]) * TW] = u;
             }
             P.cur += 2 + cnt;
         } else if (type == kRecEndG) {
             // END of a global step (the U part went out in kRecEndU records)
             h = r[1];
-            const double piv = xg[size_t(dp) * kTile];
+            const double piv = xg[size_t(dp) * TW];
             const double inv = 1.0 / piv;
             double c0 = fmax(gmax, fabs(piv));
-            double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * kTile;
+            double* lcol = lu_t + ptrdiff_t(lslot - dp - 1) * TW;
             int z = dp + 1;
 #pragma unroll 1
             for (; z + 8 <= len; z += 8) {
                 double x[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) x[k] = xg[size_t(z + k) * kTile];
+                for (int k = 0; k < 8; ++k) x[k] = xg[size_t(z + k) * TW];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     c0 = fmax(c0, fabs(x[k]));
-                    lcol[size_t(z + k) * kTile] = x[k] * inv;
+                    lcol[size_t(z + k) * TW] = x[k] * inv;
                 }
             }
             for (; z < len; ++z) {
-                const double x0 = xg[size_t(z) * kTile];
+                const double x0 = xg[size_t(z) * TW];
                 c0 = fmax(c0, fabs(x0));
-                lcol[size_t(z) * kTile] = x0 * inv;
+                lcol[size_t(z) * TW] = x0 * inv;
             }
             flagged |= isfinite(c0) && (piv == 0.0 || fabs(piv) < stol * c0);
-            lu_t[size_t(brow + 1) * kTile] = piv;
+            lu_t[size_t(brow + 1) * TW] = piv;
             if (FS) {
-                lcol[size_t(len) * kTile] = acc_y;
-                lu_t[size_t(brow) * kTile] = acc_y;
+                lcol[size_t(len) * TW] = acc_y;
+                lu_t[size_t(brow) * TW] = acc_y;
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1;
@@ -799,7 +807,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             break;
         }
     }
-    if (flagged && v.active[tile * kTile + lane]) v.flag[tile * kTile + lane] = 1;
+    if (flagged && v.active[tile * TW + le]) v.flag[tile * TW + le] = 1;
 }
 
 // Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
@@ -809,10 +817,11 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    double* b_t = v.b + size_t(tile) * v.tstride + lane;
-    const double* lu_t = v.LU + size_t(tile) * v.tstride + lane;
-    constexpr unsigned RB = kTile * 8;
-    const unsigned R0 = smem_u32(P.R) + unsigned(lane) * 8u;
+    const int TW = v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
+    double* b_t = v.b + size_t(tile) * v.tstride + le;
+    const double* lu_t = v.LU + size_t(tile) * v.tstride + le;
+    const unsigned RB = unsigned(TW) * 8u;
+    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
     unsigned blk = R0, e = R0;  // this step's block; its next U entry
     const double *blk_g = lu_t, *e_g = lu_t;  // a global step's row block in the LU tape
     int ne = 0, brow = 0;
@@ -859,7 +868,7 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             h = r[1];
             const double xi = acc / lds(blk + unsigned(ne + 1) * RB);
             sts(blk + unsigned(ne) * RB, xi);
-            b_t[size_t(brow) * kTile] = xi;
+            b_t[size_t(brow) * TW] = xi;
             fence_proxy_async_global();
             P.cur += 1;
         } else if (type == kRecPage) {
@@ -868,11 +877,11 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
         } else if (type == kRecStepG) {
             // a row too long for the pool: its block read in place from the LU tape
             ne = r[1];
-            blk_g = e_g = lu_t + size_t(r[2]) * kTile;
+            blk_g = e_g = lu_t + size_t(r[2]) * TW;
             brow = r[3];
             h = r[4];
             P.cur += 4;
-            acc = blk_g[size_t(ne) * kTile];
+            acc = blk_g[size_t(ne) * TW];
         } else if (type == kRecDepNG) {
             const int n = (h >> 4) & 0xfffff;
             h = r[1 + n];
@@ -882,21 +891,21 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
                 double u[8], x[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    u[k] = e_g[size_t(k) * kTile];
-                    x[k] = b_t[size_t(r[1 + i + k]) * kTile];
+                    u[k] = e_g[size_t(k) * TW];
+                    x[k] = b_t[size_t(r[1 + i + k]) * TW];
                 }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) acc = fma(-u[k], x[k], acc);
-                e_g += 8 * kTile;
+                e_g += 8 * TW;
             }
             for (; i < n; ++i) {
-                acc = fma(-e_g[0], b_t[size_t(r[1 + i]) * kTile], acc);
-                e_g += kTile;
+                acc = fma(-e_g[0], b_t[size_t(r[1 + i]) * TW], acc);
+                e_g += TW;
             }
             P.cur += 1 + n;
         } else if (type == kRecEndG) {
             h = r[1];
-            b_t[size_t(brow) * kTile] = acc / blk_g[size_t(ne + 1) * kTile];
+            b_t[size_t(brow) * TW] = acc / blk_g[size_t(ne + 1) * TW];
             fence_proxy_async_global();
             P.cur += 1;
         } else if (type == kRecSync) {
@@ -919,7 +928,8 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = my_tile(v, blockIdx.y, warp);
     if (tile < 0) return;
-    const int t = tile * kTile + lane;
+    const int TW = v.tw, le = min(lane, TW - 1);
+    const int t = tile * TW + le;
     if (!v.active[t]) return;
     if (v.flag[t]) {  // frozen pivot collapsed: stop, never update V
         if (blockIdx.x == 0) {
@@ -930,16 +940,16 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
         return;
     }
     const size_t bp = v.bpad;
-    const double* b_t = v.b + size_t(tile) * v.tstride + lane;  // tile-blocked b tape
+    const double* b_t = v.b + size_t(tile) * v.tstride + le;  // tile-blocked b tape
     const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
     for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
         const int zt = __ldg(v.zcol_t + bus);
         if (zt < 0) continue;
         const size_t o = size_t(bus) * bp + t;
-        const double va = v.va[o] - b_t[size_t(zt) * kTile];
+        const double va = v.va[o] - b_t[size_t(zt) * TW];
         v.va[o] = va;
         const int zv = __ldg(v.zcol_v + bus);
-        if (zv >= 0) v.vm[o] = v.vm[o] - b_t[size_t(zv) * kTile];
+        if (zv >= 0) v.vm[o] = v.vm[o] - b_t[size_t(zv) * TW];
         double s, c;
         gb_sincos(va, &s, &c);
         v.s[o] = s;
@@ -955,7 +965,7 @@ __global__ void __launch_bounds__(256) flows_kernel(DevView v, int32_t nb, const
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.y * kSuper + warp;
     if (tile >= v.n_tiles) return;
-    const int t = tile * kTile + lane;
+    const int t = tile * v.tw + min(lane, v.tw - 1);
     if (t >= v.n_tasks) return;
     const size_t bp = v.bpad, T = size_t(v.n_tasks);
     const int out = outage ? outage[t] : -1;
@@ -1006,7 +1016,7 @@ unsigned n_super(const DevView& v) { return unsigned((v.n_tiles + kSuper - 1) / 
 }  // namespace
 
 size_t walk_smem_bytes(const WalkView& w) {
-    return size_t(w.rows) * kTile * 8 +
+    return size_t(w.rows) * size_t(w.tw) * 8 +
            size_t(w.walkers) * (size_t(kWalkPages) * w.page_words * 4 + size_t(kWalkBars + kWalkPages) * 8);
 }
 
@@ -1031,12 +1041,23 @@ void launch_init(const DevView& v, cudaStream_t st) {
     init_kernel<<<dim3(unsigned((v.n + 31) / 32), n_super(v)), 256, 0, st>>>(v);
 }
 
+template <bool NPM, int JMODE>
+void launch_npm_tw(const DevView& v, dim3 grid, cudaStream_t st) {
+    switch (v.tw) {
+        case 8: npm_kernel<NPM, JMODE, 8><<<grid, 256, 0, st>>>(v); break;
+        case 16: npm_kernel<NPM, JMODE, 16><<<grid, 256, 0, st>>>(v); break;
+        case 24: npm_kernel<NPM, JMODE, 24><<<grid, 256, 0, st>>>(v); break;
+        case 32: npm_kernel<NPM, JMODE, 32><<<grid, 256, 0, st>>>(v); break;
+        default: npm_kernel<NPM, JMODE, 0><<<grid, 256, 0, st>>>(v); break;
+    }
+}
+
 void launch_npm(const DevView& v, bool jac, cudaStream_t st) {
     const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v));
     if (jac)
-        npm_kernel<true, kJacSpec><<<grid, 256, 0, st>>>(v);
+        launch_npm_tw<true, kJacSpec>(v, grid, st);
     else
-        npm_kernel<true, kJacNone><<<grid, 256, 0, st>>>(v);
+        launch_npm_tw<true, kJacNone>(v, grid, st);
     conv_kernel<<<n_super(v), 256, 0, st>>>(v);
     bump_kernel<<<1, 1, 0, st>>>(v);
 }
@@ -1046,9 +1067,9 @@ void launch_status_count(const DevView& v, cudaStream_t st) { status_count_kerne
 void launch_jacobian(const DevView& v, bool all, cudaStream_t st) {
     const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v));
     if (all)
-        npm_kernel<false, kJacAll><<<grid, 256, 0, st>>>(v);
+        launch_npm_tw<false, kJacAll>(v, grid, st);
     else
-        npm_kernel<false, kJacFix><<<grid, 256, 0, st>>>(v);
+        launch_npm_tw<false, kJacFix>(v, grid, st);
 }
 
 void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {

@@ -10,7 +10,7 @@
 
 namespace gbnr {
 
-constexpr int kTile = 32;      // tasks per tile = lanes of a warp
+constexpr int kTile = 32;      // most tasks per tile = lanes of a warp (DevView::tw: the batch's tile width)
 constexpr int kSuper = 8;      // tiles per super-tile = warps per block (2 KB access runs)
 constexpr int kRowChunk = 4;  // Ybus rows per warp in the NPM / Jacobian kernels
 
@@ -18,6 +18,10 @@ constexpr int kRowChunk = 4;  // Ybus rows per warp in the NPM / Jacobian kernel
 // tapes are element-major: value(elem, task) at elem * bpad + task.
 struct DevView {
     int32_t n, nJ, nnzY, n_rows, nnzLU, bpad, n_tiles, n_tasks;
+    // tasks per tile (even, 2..32): lane l < tw of a tile's warps owns task
+    // tile * tw + l; lanes >= tw shadow lane tw - 1 (same task, same addresses,
+    // same values: their loads and stores are duplicates, never a second task)
+    int32_t tw;
     // shared structure (read-only, L2-resident)
     const int32_t *yp, *yi;
     const double *yre, *yim;      // Ybus values: slot q of task t at q * y_ld + t * y_inc
@@ -31,7 +35,7 @@ struct DevView {
     const double *p0, *q0;
     int32_t s_ld, s_inc;          // p0[bus * s_ld + task * s_inc]
     // tile-blocked tapes, one block per tile of tstride doubles:
-    //   [A: tape_rows][LU: tape_rows][b: nJ rows] x 32 lanes   (layouts: walk.hpp LuLayout)
+    //   [A: tape_rows][LU: tape_rows][b: nJ rows] x tw lanes   (layouts: walk.hpp LuLayout)
     // A = the Jacobian columns, each followed by F_m; LU = the factors with y;
     // b = dx, row nJ-1-k for J column k (backward walk).
     double *A, *LU, *b;           // tile 0's tapes; tile t's at + t * tstride
@@ -66,6 +70,7 @@ struct DevView {
 struct WalkView {
     const int32_t* stream;  // program words (walk.hpp kRec*), walker-major pages
     int32_t walkers, page_words, rows;
+    int32_t tw;             // tile width the program's row budget was planned for
     int32_t wpage0[9];      // first page of each walker's program
 };
 

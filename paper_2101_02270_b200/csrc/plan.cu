@@ -80,8 +80,18 @@ struct gbnr_plan {
     gbnr::Symbolic sym;
     std::vector<int32_t> in_pv, in_pq;  // creation inputs kept for second-chance re-plans
     gbnr::LuLayout lay;
-    gbnr::WalkSet wf, wl, wb;        // forward LU+FS, LU-only, backward walks
-    gbnr::WalkView vf{}, vl{}, vb{};
+    // The walk programs depend on the tile width only through each walker's row
+    // budget (a row is one value per task of a tile): one set per tile width,
+    // planned on first use (tile width).
+    struct TileWalks {
+        int32_t tw = gbnr::kTile;
+        gbnr::WalkSet wf, wl, wb;        // forward LU+FS, LU-only, backward walks
+        gbnr::WalkView vf{}, vl{}, vb{};
+    };
+    std::vector<std::unique_ptr<TileWalks>> walks;
+    TileWalks* cur = nullptr;    // the walks of the staged batch's tile width
+    gbnr::WalkConfig wcfg;       // planning configuration (row bytes set per width)
+    int32_t n_sm = 148, ctas_per_sm = 3;
     gbnr_options opt{};
     bool on_device = false;
     cudaStream_t stream = nullptr;
@@ -89,7 +99,7 @@ struct gbnr_plan {
     // two result sets, so batch i+1's H2D and batch i-1's D2H overlap batch i
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<void*> pipe;
-    int32_t pipe_tiles = 0;
+    size_t pipe_lanes = 0;
     double *p0_set[2] = {nullptr, nullptr}, *q0_set[2] = {nullptr, nullptr};
     double *out_vm[2] = {nullptr, nullptr}, *out_va[2] = {nullptr, nullptr}, *out_mm[2] = {nullptr, nullptr};
     int32_t *out_it[2] = {nullptr, nullptr}, *out_st[2] = {nullptr, nullptr};
@@ -101,7 +111,10 @@ struct gbnr_plan {
     std::vector<void*> owned;     // structure buffers
     double* d_scratch = nullptr;  // [n] staging for broadcast sets
     std::vector<void*> batch;     // per-batch tapes
-    int32_t cap_tiles = 0;        // allocated tile capacity
+    size_t cap_lanes = 0;         // allocated task slots (tiles x tile width)
+    int32_t cap_scratch = 0;      // allocated global-step scratch rows per walker
+    size_t a_bytes = 0;           // A + LU + b tape bytes
+    int32_t a_tw = 0;             // tile width whose Jacobian slots the A tape holds (0: all zero)
     size_t batch_bytes = 0, pipe_bytes = 0;  // device bytes held by the batch tapes / the pipeline
     std::vector<double> y_host_re, y_host_im;       // the plan's shared Ybus values (host copy)
     std::vector<std::unique_ptr<gbnr_plan>> peers;  // device plans 2..n_devices (gbnr_options.n_devices)
@@ -199,9 +212,6 @@ struct gbnr_plan {
             v.zcol_t = dev_upload(owned, zt);
             v.zcol_v = dev_upload(owned, zv);
         }
-        vf = upload_walk(wf);
-        if (!sub_plan) vl = upload_walk(wl);
-        vb = upload_walk(wb);
         int32_t* itd = nullptr;
         CK(cudaMalloc(&itd, sizeof(int32_t)));
         owned.push_back(itd);
@@ -219,19 +229,83 @@ struct gbnr_plan {
         v.jpolicy = opt.jacobian;
     }
 
-    gbnr::WalkView upload_walk(const gbnr::WalkSet& w) {
+    gbnr::WalkView upload_walk(const gbnr::WalkSet& w, int32_t tw) {
         gbnr::WalkView x{};
         x.stream = dev_upload(owned, w.stream);
         x.walkers = w.walkers;
         x.page_words = w.page_words;
         x.rows = w.rows;
+        x.tw = tw;
         if (w.walkers < 1 || w.walkers > 8) throw Error(GBNR_ECONFIG, "1..8 walkers per tile");
         for (int32_t i = 0; i <= w.walkers; ++i) x.wpage0[i] = w.wpage0[i];
         if (w.barriers != 32 || w.pages != 2) throw Error(GBNR_ECONFIG, "walk kernels use 32 barriers, 2 pages");
-        if (gbnr::walk_smem_bytes(x) != w.smem_bytes()) throw Error(GBNR_ECONFIG, "walk smem layout mismatch");
+        if (w.row_bytes != tw * 8 || gbnr::walk_smem_bytes(x) != w.smem_bytes())
+            throw Error(GBNR_ECONFIG, "walk smem layout mismatch");
         if (gbnr::walk_smem_bytes(x) > 227 * 1024)
             throw Error(GBNR_ECONFIG, "walk needs more shared memory than a B200 CTA has");
         return x;
+    }
+
+    // The walks of tile width tw, planned (and on a device plan uploaded) on first
+    // use.  On the device the row budget shrinks until ctas_per_sm walk CTAs really
+    // co-reside on an SM.
+    TileWalks* walks_for(int32_t tw) {
+        for (auto& w : walks)
+            if (w->tw == tw) return w.get();
+        auto tws = std::make_unique<TileWalks>();
+        tws->tw = tw;
+        gbnr::WalkConfig wc = wcfg;
+        wc.row_bytes = tw * 8;
+        auto build = [&] {
+            tws->wf = gbnr::build_forward_walk(sym, lay, true, wc);
+            if (!sub_plan) tws->wl = gbnr::build_forward_walk(sym, lay, false, wc);
+            gbnr::WalkConfig wcb = wc;
+            if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
+            tws->wb = gbnr::build_backward_walk(sym, lay, wcb);
+        };
+        build();
+        if (on_device) {
+            CK(cudaSetDevice(opt.device));
+            while (gbnr::walk_ctas_per_sm(tws->wf.smem_bytes(), 32 * tws->wf.walkers) < ctas_per_sm &&
+                   wc.smem_budget > 65536) {
+                wc.smem_budget -= 1024;
+                build();
+            }
+            tws->vf = upload_walk(tws->wf, tw);
+            if (!sub_plan) tws->vl = upload_walk(tws->wl, tw);
+            tws->vb = upload_walk(tws->wb, tw);
+        }
+        walks.push_back(std::move(tws));
+        return walks.back().get();
+    }
+
+    // A copy of another device plan's walks (same programs), uploaded here.
+    void adopt_walks(const TileWalks& src) {
+        auto tws = std::make_unique<TileWalks>();
+        tws->tw = src.tw;
+        tws->wf = src.wf;
+        tws->wl = src.wl;
+        tws->wb = src.wb;
+        CK(cudaSetDevice(opt.device));
+        tws->vf = upload_walk(tws->wf, src.tw);
+        if (!sub_plan) tws->vl = upload_walk(tws->wl, src.tw);
+        tws->vb = upload_walk(tws->wb, src.tw);
+        walks.push_back(std::move(tws));
+    }
+
+    // Tile width of a batch of T tasks: the narrowest of 8/16/24/32 lanes whose
+    // tiles all fit one resident wave (n_sm x ctas_per_sm CTAs), so that the smem
+    // rows of a walker -- its prefetch depth and its resident dependencies -- grow
+    // as the batch shrinks below a full wave of 32-task tiles (gbnr_options
+    // tile_width / GBNR_TW override).
+    int32_t choose_tw(int32_t T) const {
+        int32_t tw = opt.tile_width;
+        if (const char* e = std::getenv("GBNR_TW")) tw = std::atoi(e);
+        if (tw > 0) return std::min(gbnr::kTile, std::max(2, tw + (tw & 1)));
+        const int64_t slots = int64_t(n_sm) * ctas_per_sm;
+        for (int32_t c : {8, 16, 24})
+            if (int64_t(T) <= slots * c) return c;
+        return gbnr::kTile;
     }
 
     // the plan's shared Ybus value set (one for every task)
@@ -300,14 +374,14 @@ struct gbnr_plan {
         y_task_cap = bytes;
     }
 
-    // Device bytes one tile (32 tasks) of a solve needs: the A / LU / b block, the
-    // [n][bpad] voltage / injection tapes, per-task state, walk scratch, and the
-    // per-task Ybus sets when the batch has them.
-    size_t bytes_per_tile(bool per_task_y) const {
-        const size_t lanes = gbnr::kTile;
-        size_t b = v.tstride * 8 + 8 * size_t(sym.n) * lanes * 8 + lanes * 64 +
-                   size_t(8) * size_t(std::max(wf.scratch_rows, wl.scratch_rows)) * lanes * 8;
-        if (per_task_y) b += 2 * size_t(sym.nnzY) * lanes * 8;
+    // Device bytes one task of a solve needs: its lane of the A / LU / b blocks, of
+    // the [n][bpad] voltage / injection tapes, per-task state, walk scratch, and its
+    // Ybus set when the batch has per-task sets.
+    size_t bytes_per_task(bool per_task_y) const {
+        int32_t scr = 0;
+        for (const auto& w : walks) scr = std::max({scr, w->wf.scratch_rows, w->wl.scratch_rows});
+        size_t b = (2 * size_t(lay.rows) + size_t(sym.nJ)) * 8 + 8 * size_t(sym.n) * 8 + 64 + size_t(8) * scr * 8;
+        if (per_task_y) b += 2 * size_t(sym.nnzY) * 8;
         return b;
     }
 
@@ -322,16 +396,20 @@ struct gbnr_plan {
         const size_t held = batch_bytes + pipe_bytes + y_task_cap;
         const size_t reserve = (size_t(4) << 30) + total_b / 50;
         const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
-        const size_t tiles = avail / bytes_per_tile(per_task_y);
-        return int32_t(std::max<size_t>(1, std::min<size_t>(tiles, (size_t(1) << 26))) * gbnr::kTile);
+        const size_t tasks = avail / bytes_per_task(per_task_y) / gbnr::kTile * gbnr::kTile;
+        return int32_t(std::max<size_t>(gbnr::kTile, std::min<size_t>(tasks, size_t(1) << 30)));
     }
 
-    void ensure_capacity(int32_t n_tiles) {
-        if (n_tiles <= cap_tiles) return;
+    // Device tapes for `lanes` = n_tiles x tile width task slots.  Every buffer is
+    // sized by lanes, so one allocation serves any tile width; the tile geometry
+    // (tstride, the LU / b offsets) is set per batch by set_geometry.
+    void ensure_capacity(size_t lanes, int32_t scratch_rows) {
+        if (lanes <= cap_lanes && scratch_rows <= cap_scratch) return;
         CK(cudaStreamSynchronize(stream));
         for (void* p : batch) cudaFree(p);
         batch.clear();
-        const size_t bpad = size_t(n_tiles) * gbnr::kTile;
+        lanes = std::max(lanes, cap_lanes);
+        scratch_rows = std::max(scratch_rows, cap_scratch);
         batch_bytes = 0;
         auto alloc = [&](size_t bytes) {
             void* p = nullptr;
@@ -340,7 +418,7 @@ struct gbnr_plan {
             batch_bytes += bytes;
             return p;
         };
-        const size_t nb = size_t(sym.n) * bpad * sizeof(double);
+        const size_t nb = size_t(sym.n) * lanes * sizeof(double);
         v.vm = static_cast<double*>(alloc(nb));
         v.va = static_cast<double*>(alloc(nb));
         v.vm_in = static_cast<double*>(alloc(nb));
@@ -353,32 +431,46 @@ struct gbnr_plan {
         v.q0 = q0_own = static_cast<double*>(alloc(nb));
         // one block per tile: A, LU and b rows adjacent, so a walk copy's source is
         // tile base + (tape * tape_rows + slot) rows
-        v.tstride = (2 * size_t(v.tape_rows) + size_t(v.nJ)) * gbnr::kTile;
-        const size_t tb = v.tstride * size_t(n_tiles) * sizeof(double);
-        v.A = static_cast<double*>(alloc(tb));
+        a_bytes = (2 * size_t(v.tape_rows) + size_t(v.nJ)) * lanes * sizeof(double);
+        v.A = static_cast<double*>(alloc(a_bytes));
         // fill slots of the A tape are never written by the Jacobian kernel and
-        // must read zero; tile-blocked addresses do not depend on the batch size
-        CK(cudaMemsetAsync(v.A, 0, tb, stream));
-        v.LU = v.A + size_t(v.tape_rows) * gbnr::kTile;
-        v.b = v.LU + size_t(v.tape_rows) * gbnr::kTile;
-        v.status = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
-        v.iters = static_cast<int32_t*>(alloc(bpad * sizeof(int32_t)));
-        v.active = static_cast<uint8_t*>(alloc(bpad));
-        v.flag = static_cast<uint8_t*>(alloc(bpad));
-        v.maxmis = static_cast<double*>(alloc(bpad * sizeof(double)));
-        v.mis_prev = static_cast<double*>(alloc(bpad * sizeof(double)));
-        v.mis0 = static_cast<double*>(alloc(bpad * sizeof(double)));
-        v.jskip = static_cast<uint8_t*>(alloc(bpad));
-        v.norm_bits = static_cast<unsigned long long*>(alloc(bpad * sizeof(unsigned long long)));
-        v.tile_active = static_cast<int32_t*>(alloc(size_t(n_tiles) * sizeof(int32_t)));
+        // must read zero (re-zeroed when the tile width changes, set_geometry)
+        CK(cudaMemsetAsync(v.A, 0, a_bytes, stream));
+        a_tw = 0;
+        v.status = static_cast<int32_t*>(alloc(lanes * sizeof(int32_t)));
+        v.iters = static_cast<int32_t*>(alloc(lanes * sizeof(int32_t)));
+        v.active = static_cast<uint8_t*>(alloc(lanes));
+        v.flag = static_cast<uint8_t*>(alloc(lanes));
+        v.maxmis = static_cast<double*>(alloc(lanes * sizeof(double)));
+        v.mis_prev = static_cast<double*>(alloc(lanes * sizeof(double)));
+        v.mis0 = static_cast<double*>(alloc(lanes * sizeof(double)));
+        v.jskip = static_cast<uint8_t*>(alloc(lanes));
+        v.norm_bits = static_cast<unsigned long long*>(alloc(lanes * sizeof(unsigned long long)));
+        v.tile_active = static_cast<int32_t*>(alloc(lanes * sizeof(int32_t)));  // >= tiles at any width
         // global scratch of the forward walks' global steps (columns too large for
         // a walker's shared-memory pool), 8 walkers per tile
-        v.scratch_rows = std::max(wf.scratch_rows, wl.scratch_rows);
-        v.scratch = v.scratch_rows > 0
-                        ? static_cast<double*>(alloc(size_t(n_tiles) * 8 * size_t(v.scratch_rows) * gbnr::kTile * 8))
-                        : nullptr;
+        v.scratch = scratch_rows > 0 ? static_cast<double*>(alloc(lanes * 8 * size_t(scratch_rows) * 8)) : nullptr;
         v.active_count = static_cast<int32_t*>(alloc(128 * sizeof(int32_t)));
-        cap_tiles = n_tiles;
+        cap_lanes = lanes;
+        cap_scratch = scratch_rows;
+    }
+
+    // Tile geometry of a batch of n_tasks tasks at tile width tw (its walks current).
+    void set_geometry(int32_t n_tasks, int32_t tw) {
+        cur = walks_for(tw);
+        const int32_t n_tiles = (n_tasks + tw - 1) / tw;
+        const int32_t scr = std::max(cur->wf.scratch_rows, cur->wl.scratch_rows);
+        ensure_capacity(size_t(n_tiles) * tw, scr);
+        if (a_tw != 0 && a_tw != tw) CK(cudaMemsetAsync(v.A, 0, a_bytes, stream));  // J slots move with tw
+        a_tw = tw;
+        v.tw = tw;
+        v.n_tiles = n_tiles;
+        v.bpad = n_tiles * tw;
+        v.n_tasks = n_tasks;
+        v.tstride = (2 * size_t(v.tape_rows) + size_t(v.nJ)) * size_t(tw);
+        v.LU = v.A + size_t(v.tape_rows) * tw;
+        v.b = v.LU + size_t(v.tape_rows) * tw;
+        v.scratch_rows = scr;
     }
 
     // Element-major host [n][sets] -> device [n][bpad] (broadcast when sets == 1).
@@ -417,11 +509,7 @@ struct gbnr_plan {
                                      cudaMemcpyHostToDevice, stream));
         };
         CK(cudaSetDevice(opt.device));
-        const int32_t n_tiles = (n_tasks + gbnr::kTile - 1) / gbnr::kTile;
-        ensure_capacity(n_tiles);
-        v.n_tiles = n_tiles;
-        v.bpad = n_tiles * gbnr::kTile;
-        v.n_tasks = n_tasks;
+        set_geometry(n_tasks, choose_tw(n_tasks));
         // start voltages as given: [n] shared or [n][n_tasks], one linear copy each
         // (init_kernel reads them through vin_ld / vin_inc)
         const bool vshared = n_vsets == 1 && ld_v <= 0;
@@ -500,8 +588,8 @@ struct gbnr_plan {
 
     // LU refactorization fused with the forward substitution, then the
     // backward substitution: one launch each (tile walks, walk.hpp)
-    void launch_lu_all() { gbnr::launch_lu_walk(v, vf, true, stream); }
-    void launch_fsbs_all() { gbnr::launch_bs_walk(v, vb, stream); }
+    void launch_lu_all() { gbnr::launch_lu_walk(v, cur->vf, true, stream); }
+    void launch_fsbs_all() { gbnr::launch_bs_walk(v, cur->vb, stream); }
 
     static int launches_per_iteration() { return 6; }  // lu+fs, bs, vupd, npm+jac, conv, bump
 
@@ -657,7 +745,7 @@ struct gbnr_plan {
         // one-task plan needs next to this batch
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
-        const size_t per_plan = bytes_per_tile(false) + size_t(64) << 20;
+        const size_t per_plan = bytes_per_task(false) * gbnr::kTile + (size_t(64) << 20);
         const size_t by_mem = free_b > (size_t(1) << 30) ? (free_b - (size_t(1) << 30)) / per_plan : 1;
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const size_t W = std::max<size_t>(1, std::min({work.size(), size_t(std::min(hw, 16u)), by_mem}));
@@ -849,13 +937,13 @@ struct gbnr_plan {
         }
     }
 
-    void ensure_pipe(int32_t n_tiles) {
-        if (n_tiles <= pipe_tiles) return;
+    void ensure_pipe(size_t lanes) {
+        if (lanes <= pipe_lanes) return;
         CK(cudaDeviceSynchronize());
         for (void* q : pipe) cudaFree(q);
         pipe.clear();
-        const size_t nb = size_t(sym.n) * size_t(n_tiles) * gbnr::kTile * sizeof(double);
-        const size_t tb = size_t(n_tiles) * gbnr::kTile;
+        const size_t nb = size_t(sym.n) * lanes * sizeof(double);
+        const size_t tb = lanes;
         pipe_bytes = 0;
         auto alloc = [&](size_t bytes) {
             void* q = nullptr;
@@ -879,7 +967,7 @@ struct gbnr_plan {
             out_it[i] = static_cast<int32_t*>(alloc(tb * sizeof(int32_t)));
             out_st[i] = static_cast<int32_t*>(alloc(tb * sizeof(int32_t)));
         }
-        pipe_tiles = n_tiles;
+        pipe_lanes = lanes;
     }
 
     // Pipelined sequence of batches (all of n_tasks tasks, injections per task,
@@ -914,7 +1002,7 @@ struct gbnr_plan {
         stage_ybus(nullptr, nullptr, 1, n_tasks);
         stage(n_tasks, nullptr, nullptr, 0, vm0, va0, 1);
         CK(cudaStreamSynchronize(stream));
-        ensure_pipe(v.n_tiles);
+        ensure_pipe(size_t(v.bpad));
         const size_t nt = size_t(n_tasks), row = nt * sizeof(double);
         const size_t bytes = size_t(sym.n) * row;  // host layout [n][n_tasks], copied linearly
         auto issue_h2d = [&](int32_t j) {
@@ -1053,13 +1141,13 @@ struct gbnr_plan {
         gbnr::launch_init(v, stream);
         gbnr::launch_jacobian(v, true, stream);
         CK(cudaGetLastError());
-        gbnr::launch_lu_walk(v, vl, false, stream);  // warm-up
+        gbnr::launch_lu_walk(v, cur->vl, false, stream);  // warm-up
         if (v.prof) {
             CK(cudaStreamSynchronize(stream));
             CK(cudaMemset(v.prof, 0, 4 * 8 * 16 * 8));
         }
         CK(cudaEventRecord(ev0, stream));
-        for (int32_t r = 0; r < reps; ++r) gbnr::launch_lu_walk(v, vl, false, stream);
+        for (int32_t r = 0; r < reps; ++r) gbnr::launch_lu_walk(v, cur->vl, false, stream);
         CK(cudaEventRecord(ev1, stream));
         CK(cudaGetLastError());
         CK(cudaEventSynchronize(ev1));
@@ -1071,14 +1159,14 @@ struct gbnr_plan {
         if (flags_out) CK(cudaMemcpy(flags_out, v.flag, size_t(nt), cudaMemcpyDeviceToHost));
         if (lu_out) {
             // tile-blocked tape -> element-major CCS order [nnzLU][n_tasks]
-            const size_t z = size_t(v.nnzLU), tr = size_t(v.tape_rows) * gbnr::kTile;
+            const size_t TW = size_t(v.tw), z = size_t(v.nnzLU), tr = size_t(v.tape_rows) * TW;
             std::vector<double> tape(size_t(v.n_tiles) * tr);  // the LU part of every tile's block
             CK(cudaMemcpy2D(tape.data(), tr * 8, v.LU, v.tstride * 8, tr * 8, size_t(v.n_tiles),
                             cudaMemcpyDeviceToHost));
             for (size_t c = 0; c < z; ++c) {
                 const size_t ts = size_t(lay.tape_of_ccs[c]);
                 for (int32_t t = 0; t < nt; ++t)
-                    lu_out[c * nt + t] = tape[size_t(t / gbnr::kTile) * tr + ts * gbnr::kTile + t % gbnr::kTile];
+                    lu_out[c * nt + t] = tape[size_t(t) / TW * tr + ts * TW + size_t(t) % TW];
             }
         }
     }
@@ -1104,6 +1192,7 @@ void gbnr_default_options(gbnr_options* o) {
     o->n_devices = 1;
     o->device_step = 1;
     o->chunk_tasks = 0;
+    o->tile_width = 0;
 }
 
 const char* gbnr_last_error(void) { return g_err.c_str(); }
@@ -1197,6 +1286,8 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         if (p->opt.second_chance < 0) throw Error(GBNR_ECONFIG, "second_chance must be >= 0");
         if (p->opt.n_devices < 0 || p->opt.n_devices > 64 || p->opt.device_step < 0 || p->opt.chunk_tasks < 0)
             throw Error(GBNR_ECONFIG, "need 0 <= n_devices <= 64, device_step >= 0, chunk_tasks >= 0");
+        if (p->opt.tile_width < 0 || p->opt.tile_width > gbnr::kTile || (p->opt.tile_width & 1))
+            throw Error(GBNR_ECONFIG, "tile_width must be 0 (automatic) or even in 2..32");
         p->sub_plan = sub;
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
@@ -1226,31 +1317,21 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
             if (wc.levels.empty() || wc.levels.front() != wc.walkers || wc.levels.back() != 1)
                 throw Error(GBNR_ECONFIG, "GBNR_LEVELS must start at the walker count and end at 1");
         }
-        auto build_walks = [&] {
-            p->wf = gbnr::build_forward_walk(p->sym, p->lay, true, wc);
-            if (!sub) p->wl = gbnr::build_forward_walk(p->sym, p->lay, false, wc);
-            gbnr::WalkConfig wcb = wc;
-            if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
-            p->wb = gbnr::build_backward_walk(p->sym, p->lay, wcb);
-        };
-        build_walks();
-        if (p->opt.device >= 0) {
+        p->wcfg = wc;
+        if (const char* e = std::getenv("GBNR_CTAS")) p->ctas_per_sm = std::max(1, std::atoi(e));
+        if (p->opt.device < 0) {
+            p->cur = p->walks_for(gbnr::kTile);  // host-only plan: the full-width programs (inspection, tests)
+        } else {
             int ndev = 0;
             CK(cudaGetDeviceCount(&ndev));
             if (p->opt.device >= ndev) throw Error(GBNR_ECUDA, "CUDA device ordinal out of range");
             CK(cudaSetDevice(p->opt.device));
+            CK(cudaDeviceGetAttribute(&p->n_sm, cudaDevAttrMultiProcessorCount, p->opt.device));
             gbnr::configure_kernels();
-            // three tiles per SM: shrink the shared-memory budget until the
-            // device really co-schedules three walk CTAs
-            int ctas = 3;
-            if (const char* e = std::getenv("GBNR_CTAS")) ctas = std::max(1, std::atoi(e));
-            while (gbnr::walk_ctas_per_sm(p->wf.smem_bytes(), 32 * p->wf.walkers) < ctas && wc.smem_budget > 65536) {
-                wc.smem_budget -= 1024;
-                build_walks();
-            }
             p->on_device = true;
             p->upload_structure();
             p->set_ybus(y_re, y_im);
+            p->cur = p->walks_for(gbnr::kTile);
             // n_devices > 1: the same frozen symbolic state and walk programs on
             // devices device + i * device_step, one plan each
             const int32_t nd = std::max(1, p->opt.n_devices);
@@ -1262,18 +1343,20 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
                 q->in_pv = p->in_pv;
                 q->in_pq = p->in_pq;
                 q->lay = p->lay;
-                q->wf = p->wf;
-                q->wl = p->wl;
-                q->wb = p->wb;
+                q->wcfg = p->wcfg;
+                q->ctas_per_sm = p->ctas_per_sm;
                 q->opt = p->opt;
                 q->opt.device = d;
                 q->opt.n_devices = 1;
                 q->sub_plan = sub;
                 CK(cudaSetDevice(d));
+                CK(cudaDeviceGetAttribute(&q->n_sm, cudaDevAttrMultiProcessorCount, d));
                 gbnr::configure_kernels();
                 q->on_device = true;
                 q->upload_structure();
                 q->set_ybus(y_re, y_im);
+                for (const auto& w : p->walks) q->adopt_walks(*w);
+                q->cur = q->walks.front().get();
                 p->peers.push_back(std::move(q));
             }
             CK(cudaSetDevice(p->opt.device));
@@ -1411,9 +1494,9 @@ int gbnr_last_timing(const gbnr_plan* p, double* out) {
 }
 
 static const gbnr::WalkSet& pick_walk(const gbnr_plan* p, int32_t which) {
-    if (which == 0) return p->wf;
-    if (which == 1) return p->wl;
-    if (which == 2) return p->wb;
+    if (which == 0) return p->cur->wf;
+    if (which == 1) return p->cur->wl;
+    if (which == 2) return p->cur->wb;
     throw Error(GBNR_ECONFIG, "walk index must be 0, 1 or 2");
 }
 

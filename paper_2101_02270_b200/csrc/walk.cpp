@@ -158,7 +158,7 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         o.ncopy = static_cast<int32_t>(c.cps.size());
         o.c0 = static_cast<int32_t>(w.copies.size());
         for (size_t i = 0; i < c.cps.size(); ++i) {
-            o.bytes += copy_rows(c.cps[i]) * 256;
+            o.bytes += copy_rows(c.cps[i]);
             w.copies.push_back(c.cps[i]);
             tag_of_copy.push_back(c.tags[i]);
             if (c.tags[i] >= T) op_of_tag[c.tags[i] - T] = s;
@@ -452,7 +452,7 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         o.ncopy = static_cast<int32_t>(c.cps.size());
         o.c0 = static_cast<int32_t>(w.copies.size());
         for (size_t i = 0; i < c.cps.size(); ++i) {
-            o.bytes += copy_rows(c.cps[i]) * 256;
+            o.bytes += copy_rows(c.cps[i]);
             w.copies.push_back(c.cps[i]);
             tag_of_copy.push_back(c.tags[i]);
             if (c.tags[i] >= T) op_of_tag[c.tags[i] - T] = s;
@@ -907,7 +907,7 @@ Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
     // longer records than a page of kMaxPageWords go global (their forms split)
     const int32_t W = std::min(std::max(cfg.page_words, 4 * ((longest + 1 + 3) / 4)), kMaxPageWords);
     const int64_t fixed = int64_t(walkers) * (int64_t(cfg.pages) * W * 4 + int64_t(cfg.barriers + cfg.pages) * 8);
-    const int64_t rows = (int64_t(cfg.smem_budget) - fixed) / 256;
+    const int64_t rows = (int64_t(cfg.smem_budget) - fixed) / cfg.row_bytes;
     return Geometry{W, int32_t(std::max<int64_t>(rows, 0))};
 }
 
@@ -989,6 +989,7 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
     ws.pages = cfg.pages;
     ws.barriers = cfg.barriers;
     ws.rows = g.rows;
+    ws.row_bytes = cfg.row_bytes;
     std::vector<Emitter> em(walkers, Emitter{{}, g.W});
     std::vector<int32_t> op_base(walkers, 0);
     for (size_t ph = 0; ph < phases.size(); ++ph) {

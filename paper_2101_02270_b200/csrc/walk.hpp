@@ -59,7 +59,8 @@ struct WDep {
     int32_t gslot;    // global source: LU-tape slot of L(:,k) (fwd) / b-tape row of x_k (bwd)
     int32_t gnl;      // global source (fwd): rows of L(:,k) (y_k follows them)
 };
-// One TMA bulk copy: nrows 256 B rows of tape `tape` from slot/row `slot`.
+// One TMA bulk copy: nrows rows of tape `tape` from slot/row `slot` (a row is one
+// value per task of a tile: tile width x 8 bytes).
 struct WCopy {
     int32_t tape_rows;  // tape | nrows << 8
     int32_t slot;
@@ -69,13 +70,14 @@ struct WCopy {
 struct WOp {
     int32_t after;  // issue once the consumer has passed this event (-1 = prologue)
     int32_t ncopy;
-    int32_t bytes;  // expect_tx total
+    int32_t bytes;  // expect_tx total in rows (the kernel multiplies by its row bytes)
     int32_t c0;     // first copy in Walk::copies
 };
 
 struct WalkConfig {
     int32_t walkers = 8;          // K: warps per tile walking disjoint etree subtrees
     int32_t smem_budget = 76800;  // bytes per CTA: three tiles per SM (228 KB - 3 x 1 KB reserved)
+    int32_t row_bytes = 256;      // bytes per shared / tape row: tile width x 8
     int32_t ring_rows = 0;        // per-walker ring override (0 = from the budget)
     int32_t stage_rows = 0;       // per-walker staging override (0 = from the budget)
     int32_t barriers = 32;        // mbarriers per walker (op i uses barrier i % 32)
@@ -150,7 +152,7 @@ struct Walk {
 
 // All walkers of one tile, all phases: what a kernel launch runs.
 struct WalkSet {
-    int32_t walkers = 1, phases = 1, rows = 0, page_words = 0, pages = 0, barriers = 0;
+    int32_t walkers = 1, phases = 1, rows = 0, page_words = 0, pages = 0, barriers = 0, row_bytes = 256;
     std::vector<Walk> parts;        // [phase * walkers + w]
     std::vector<int32_t> stream;    // every walker's pages, walker-major
     std::vector<int32_t> wpage0;    // [walkers + 1] first page of each walker
@@ -159,7 +161,8 @@ struct WalkSet {
     int64_t global_steps = 0, global_deps = 0;
     int32_t scratch_rows = 0;       // per-tile global scratch rows (forward global steps)
     size_t smem_bytes() const {
-        return size_t(rows) * 256 + size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages) * 8);
+        return size_t(rows) * size_t(row_bytes) +
+               size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages) * 8);
     }
 };
 

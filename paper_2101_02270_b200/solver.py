@@ -50,7 +50,8 @@ class Options(C.Structure):
                 ("profile", C.c_int32), ("stage_rows", C.c_int32),
                 ("prefetch", C.c_int32), ("headroom", C.c_int32), ("walkers", C.c_int32),
                 ("jacobian", C.c_int32), ("second_chance", C.c_int32),
-                ("n_devices", C.c_int32), ("device_step", C.c_int32), ("chunk_tasks", C.c_int32)]
+                ("n_devices", C.c_int32), ("device_step", C.c_int32), ("chunk_tasks", C.c_int32),
+                ("tile_width", C.c_int32)]
 
 
 _lib = None

@@ -381,3 +381,28 @@ def test_global_forms_match_oracle(frac, monkeypatch):
     olu, oflags = oplan.refactor(vm, va)
     np.testing.assert_array_equal(flags, oflags)
     np.testing.assert_array_equal(lu, olu)
+
+
+@pytest.mark.parametrize("tw", [2, 8, 16, 24, 32, 14])
+def test_tile_width_invariance(tw):
+    """gbnr_options.tile_width (tasks per tile; the walk programs re-planned for the
+    row budget of that width, lanes >= width shadowing the last real lane) never
+    changes a bit: NR solve, N-1 per-task Ybus sets and the LU-only refactorization
+    against the oracle.  14 is not one of the automatic widths (generic kernels)."""
+    gc = load_case(util.case_path("synth2383"))
+    plan, oplan, vm0, va0 = _setup_case(gc, tile_width=tw)
+    T = 77
+    p0, q0 = montecarlo(gc, T)
+    _compare(plan.solve(p0, q0, vm0, va0), oplan.solve(p0, q0, vm0[:, None], va0[:, None]))
+    outages = np.random.default_rng(4).integers(0, gc.n_branch, T).astype(np.int32)
+    yre, yim, _ = S.contingency_values(gc, outages)
+    _compare(plan.solve(p0, q0, vm0, va0, y=(yre, yim)),
+             oplan.solve(p0, q0, vm0[:, None], va0[:, None], y=(yre, yim)))
+    rng = np.random.default_rng(9)
+    vm = vm0[:, None] * (1 + 0.02 * rng.standard_normal((gc.n_bus, 30)))
+    va = va0[:, None] + 0.05 * rng.standard_normal((gc.n_bus, 30))
+    plan.stage(p0[:, :30], q0[:, :30], vm, va)
+    lu, flags, _ = plan.refactor(reps=1)
+    olu, oflags = oplan.refactor(vm, va)
+    np.testing.assert_array_equal(flags, oflags)
+    np.testing.assert_array_equal(lu, olu)

@@ -124,8 +124,8 @@ class Machine:
             c, slot = int(r[3 + 2 * i]), int(r[4 + 2 * i])
             tape, rows, smem = c & 3, (c >> 2) & 1023, c >> 12
             self.R[smem:smem + rows] = self.tapes[tape][slot:slot + rows]
-            nbytes += rows * 256
-        assert nbytes == r[2]
+            nbytes += rows
+        assert nbytes == r[2]  # expect_tx in rows (the kernel scales by its row bytes)
         self.issued.add(op)
         self.n_issued += 1
         return 3 + 2 * ncopy
