@@ -244,12 +244,13 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 // Shared row address of the low / high 16-bit row index of a packed word
-// (PRMT / SHF, then one shift-add)
-__device__ __forceinline__ unsigned row_lo(unsigned base, int32_t w) {
-    return base + (__byte_perm(unsigned(w), 0u, 0x4410) << 8);
+// (PRMT / SHF, then one shift-add for the power-of-two row sizes); RB = bytes per
+// row = tile width x 8
+__device__ __forceinline__ unsigned row_lo(unsigned base, int32_t w, unsigned RB) {
+    return base + __byte_perm(unsigned(w), 0u, 0x4410) * RB;
 }
-__device__ __forceinline__ unsigned row_hi(unsigned base, int32_t w) {
-    return base + (__byte_perm(unsigned(w), 0u, 0x4432) << 8);
+__device__ __forceinline__ unsigned row_hi(unsigned base, int32_t w, unsigned RB) {
+    return base + __byte_perm(unsigned(w), 0u, 0x4432) * RB;
 }
 // 32-bit shared-window accesses of the walk rows (no generic-address arithmetic)
 __device__ __forceinline__ double lds(unsigned a) {
@@ -313,7 +314,6 @@ struct Prog {
     const int32_t* cur;         // next record
     const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
     int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
-    int RB;                     // bytes per row: tile width x 8
     int W, n_pages, page;
 };
 
@@ -370,7 +370,6 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.cur = P.pg;
     P.tb = reinterpret_cast<const char*>(v.A + size_t(tile) * v.tstride);
     P.tape_rows = v.tape_rows;
-    P.RB = v.tw * 8;
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
     __syncwarp();  // every lane's barrier is initialised before lane 0 arms the page barriers
@@ -400,12 +399,11 @@ __device__ __forceinline__ void prog_next_page(Prog& P, int lane) {
 }
 
 // kRecIssue: lane 0 arms the op's barrier and issues its bulk copies.
-__device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32_t* r, int lane) {
+__device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32_t* r, int lane, unsigned RB) {
     const int ncopy = (r[0] >> 4) & 0xfff;
     fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
     unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
     __syncwarp();
-    const unsigned RB = unsigned(P.RB);
     if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]) * RB);  // rows -> bytes
     // one copy per lane; a copy may complete before lane 0's arrive.expect_tx (the
     // barrier's tx-count dips below zero, its phase cannot complete without the arrive)
@@ -430,14 +428,15 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
 // Shared rows are addressed as 32-bit shared-window offsets: row r of this
 // lane at R0 + r * 256.
-template <bool FS>
+// TW_: the tile width as a compile-time constant (8 / 16 / 24 / 32), 0 = from the view.
+template <bool FS, int TW_>
 __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    const int TW = v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
+    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
     double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const double stol = v.singular_tol;
     const unsigned RB = unsigned(TW) * 8u;  // bytes per shared / tape row
@@ -489,8 +488,8 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
 #pragma unroll 1
             for (int q = 0; q < nrows; q += 4) {
                 const int32_t v0 = dw[q >> 1], v1 = dw[(q >> 1) + 1];
-                const unsigned d0 = row_lo(xs, v0), d1 = row_hi(xs, v0);
-                const unsigned d2 = row_lo(xs, v1), d3 = row_hi(xs, v1);
+                const unsigned d0 = row_lo(xs, v0, RB), d1 = row_hi(xs, v0, RB);
+                const unsigned d2 = row_lo(xs, v1, RB), d3 = row_hi(xs, v1, RB);
                 const int q1 = min(q + 1, last), q2 = min(q + 2, last), q3 = min(q + 3, last);
                 const double a0 = lds(s1 + unsigned(q + 1) * RB), a1 = lds(s1 + unsigned(q1 + 1) * RB);
                 const double a2 = lds(s1 + unsigned(q2 + 1) * RB), a3 = lds(s1 + unsigned(q3 + 1) * RB);
@@ -539,10 +538,10 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 for (; q + 8 <= nrows; q += 8) {  // eight independent rows in flight
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1], w2 = dw[(q >> 1) + 2],
                                   w3 = dw[(q >> 1) + 3];
-                    const unsigned d0 = row_lo(xs, w0), d1 = row_hi(xs, w0);
-                    const unsigned d2 = row_lo(xs, w1), d3 = row_hi(xs, w1);
-                    const unsigned d4 = row_lo(xs, w2), d5 = row_hi(xs, w2);
-                    const unsigned d6 = row_lo(xs, w3), d7 = row_hi(xs, w3);
+                    const unsigned d0 = row_lo(xs, w0, RB), d1 = row_hi(xs, w0, RB);
+                    const unsigned d2 = row_lo(xs, w1, RB), d3 = row_hi(xs, w1, RB);
+                    const unsigned d4 = row_lo(xs, w2, RB), d5 = row_hi(xs, w2, RB);
+                    const unsigned d6 = row_lo(xs, w3, RB), d7 = row_hi(xs, w3, RB);
                     const unsigned sq = src + unsigned(q) * RB;
                     double l[8], a[8];
 #pragma unroll
@@ -571,8 +570,8 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                     // whole groups of 4: padding rows re-read the last L row and
                     // land in the scratch row
                     const int32_t w0 = dw[q >> 1], w1 = dw[(q >> 1) + 1];
-                    const unsigned d0 = row_lo(xs, w0), d1 = row_hi(xs, w0);
-                    const unsigned d2 = row_lo(xs, w1), d3 = row_hi(xs, w1);
+                    const unsigned d0 = row_lo(xs, w0, RB), d1 = row_hi(xs, w0, RB);
+                    const unsigned d2 = row_lo(xs, w1, RB), d3 = row_hi(xs, w1, RB);
                     const unsigned sq = src + unsigned(q) * RB;
                     const int last = nrows - 1;
                     const double l0 = lds(sq), l1 = lds(src + unsigned(min(q + 1, last)) * RB);
@@ -593,7 +592,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             P.cur += 4 + (n4 >> 1);
             PROF_MARK(4)
         } else if (__builtin_expect(type == kRecIssue, 1)) {
-            P.cur += prog_issue(v, P, r, lane);
+            P.cur += prog_issue(v, P, r, lane, RB);
             h = P.cur[0];
             PROF_MARK(7)
             PROF_CNT(11)
@@ -811,13 +810,14 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
 }
 
 // Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
+template <int TW_>
 __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    const int TW = v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
+    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
     double* b_t = v.b + size_t(tile) * v.tstride + le;
     const double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const unsigned RB = unsigned(TW) * 8u;
@@ -839,18 +839,18 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
             int i = 0;
             for (; i + 2 <= n; i += 2) {  // acc -= U(i,k) x_k, k descending (operand loads paired)
                 const int32_t w2 = yw[i >> 1];
-                const double u0 = lds(e), x0 = lds(row_lo(R0, w2)), u1 = lds(e + RB), x1 = lds(row_hi(R0, w2));
+                const double u0 = lds(e), x0 = lds(row_lo(R0, w2, RB)), u1 = lds(e + RB), x1 = lds(row_hi(R0, w2, RB));
                 acc = fma(-u0, x0, acc);
                 acc = fma(-u1, x1, acc);
                 e += 2 * RB;
             }
             if (i < n) {
-                acc = fma(-lds(e), lds(row_lo(R0, yw[i >> 1])), acc);
+                acc = fma(-lds(e), lds(row_lo(R0, yw[i >> 1], RB)), acc);
                 e += RB;
             }
             P.cur += 2 + ((n + 1) >> 1);
         } else if (__builtin_expect(type == kRecIssue, 1)) {
-            const int len = prog_issue(v, P, r, lane);
+            const int len = prog_issue(v, P, r, lane, RB);
             P.cur += len;
             h = P.cur[0];
         } else if (type == kRecStep) {
@@ -1020,19 +1020,30 @@ size_t walk_smem_bytes(const WalkView& w) {
            size_t(w.walkers) * (size_t(kWalkPages) * w.page_words * 4 + size_t(kWalkBars + kWalkPages) * 8);
 }
 
+template <class K>
+void configure_walk(K k) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+template <int TW_>
+void configure_width() {
+    configure_walk(lu_walk_kernel<true, TW_>);
+    configure_walk(lu_walk_kernel<false, TW_>);
+    configure_walk(bs_walk_kernel<TW_>);
+}
+
 void configure_kernels() {
-    const int max_smem = 227 * 1024;
-    cudaFuncSetAttribute(lu_walk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    cudaFuncSetAttribute(lu_walk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    cudaFuncSetAttribute(bs_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    cudaFuncSetAttribute(lu_walk_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(lu_walk_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(bs_walk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configure_width<0>();
+    configure_width<8>();
+    configure_width<16>();
+    configure_width<24>();
+    configure_width<32>();
 }
 
 int walk_ctas_per_sm(size_t smem, int threads) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lu_walk_kernel<true>, threads, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lu_walk_kernel<true, 32>, threads, smem) != cudaSuccess)
         return 0;
     return n;
 }
@@ -1072,17 +1083,36 @@ void launch_jacobian(const DevView& v, bool all, cudaStream_t st) {
         launch_npm_tw<false, kJacFix>(v, grid, st);
 }
 
-void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {
+template <int TW_>
+void launch_lu_tw(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {
     const size_t smem = walk_smem_bytes(w);
-    const unsigned threads = unsigned(kTile * w.walkers);
+    const unsigned threads = unsigned(32 * w.walkers);
     if (fs)
-        lu_walk_kernel<true><<<unsigned(v.n_tiles), threads, smem, st>>>(v, w);
+        lu_walk_kernel<true, TW_><<<unsigned(v.n_tiles), threads, smem, st>>>(v, w);
     else
-        lu_walk_kernel<false><<<unsigned(v.n_tiles), threads, smem, st>>>(v, w);
+        lu_walk_kernel<false, TW_><<<unsigned(v.n_tiles), threads, smem, st>>>(v, w);
+}
+
+void launch_lu_walk(const DevView& v, const WalkView& w, bool fs, cudaStream_t st) {
+    switch (v.tw) {
+        case 8: launch_lu_tw<8>(v, w, fs, st); break;
+        case 16: launch_lu_tw<16>(v, w, fs, st); break;
+        case 24: launch_lu_tw<24>(v, w, fs, st); break;
+        case 32: launch_lu_tw<32>(v, w, fs, st); break;
+        default: launch_lu_tw<0>(v, w, fs, st); break;
+    }
 }
 
 void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st) {
-    bs_walk_kernel<<<unsigned(v.n_tiles), unsigned(kTile * w.walkers), walk_smem_bytes(w), st>>>(v, w);
+    const dim3 grid(unsigned(v.n_tiles)), block(unsigned(32 * w.walkers));
+    const size_t smem = walk_smem_bytes(w);
+    switch (v.tw) {
+        case 8: bs_walk_kernel<8><<<grid, block, smem, st>>>(v, w); break;
+        case 16: bs_walk_kernel<16><<<grid, block, smem, st>>>(v, w); break;
+        case 24: bs_walk_kernel<24><<<grid, block, smem, st>>>(v, w); break;
+        case 32: bs_walk_kernel<32><<<grid, block, smem, st>>>(v, w); break;
+        default: bs_walk_kernel<0><<<grid, block, smem, st>>>(v, w); break;
+    }
 }
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {
