@@ -35,12 +35,6 @@ __device__ __forceinline__ double nan_as_inf_abs(double v) {
     return isnan(a) ? INFINITY : a;
 }
 
-// tile of warp `warp` in super-tile `st`, or -1 when out of range / finished
-__device__ __forceinline__ int my_tile(const DevView& v, int st, int warp) {
-    const int tile = st * kSuper + warp;
-    return (tile < v.n_tiles && v.tile_active[tile] != 0) ? tile : -1;
-}
-
 // ---------------------------------------------------------------------------
 // init: working voltages from the staged inputs, unit phasors, task state
 // grid (ceil(n/32), n_super), block 256: warp = tile, 32 buses per block
@@ -98,16 +92,21 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
 
 // TW_: the tile width as a compile-time constant (8 / 16 / 24 / 32: no register
 // for it under the 5-blocks-per-SM budget), 0 = read from the view.
+// Warps cover 32 consecutive tasks whatever the tile width (the element-major
+// tapes are task-contiguous); the Jacobian / F stores go to each task's lane of
+// its tile's A block.  Lanes past the batch shadow its last task (duplicate
+// stores of equal values).
 template <bool NPM, int JMODE, int TW_>
 __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = my_tile(v, blockIdx.y, warp);
-    if (tile < 0) return;
-    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);
-    const int t = tile * TW + le;
+    const int g = blockIdx.y * kSuper + warp;  // group of 32 tasks
+    if (g * 32 >= v.n_tasks) return;
+    const int t = min(g * 32 + lane, v.n_tasks - 1);
+    if (!__any_sync(kFull, v.active[t] != 0)) return;  // every task of the group has finished
+    const int TW = TW_ ? TW_ : v.tw;
     const size_t bp = v.bpad;
-    double* a_t = v.A + size_t(tile) * v.tstride + le;  // tile-blocked A tape
-    const size_t yt = size_t(min(t, v.n_tasks - 1)) * v.y_inc;  // this task's Ybus value set
+    double* a_t = v.A + size_t(t / TW) * v.tstride + (t % TW);  // tile-blocked A tape
+    const size_t yt = size_t(t) * v.y_inc;  // this task's Ybus value set
     bool act = JMODE != kJacNone && v.active[t] != 0;
     if (JMODE == kJacSpec) {
         const bool skip = act && predict_converged(v, t);
@@ -135,7 +134,7 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
         double P, Q;
         injection(vre, vim, ire, iim, P, Q);
         if (NPM) {
-            const size_t ts = size_t(min(t, v.n_tasks - 1)) * v.s_inc;  // padding lanes read a real task
+            const size_t ts = size_t(t) * v.s_inc;
             const double fp = P - __ldg(v.p0 + size_t(r) * v.s_ld + ts);
             a_t[size_t(__ldg(v.fslot_p + r)) * TW] = fp;  // F beside its A column
             nrm = fmax(nrm, nan_as_inf_abs(fp));
@@ -924,13 +923,12 @@ __global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) 
 // V update for active tasks: va -= dtheta, vm -= d|V|; refresh (cos, sin).
 // block (32-bus chunk, super-tile), warp = tile.
 // ---------------------------------------------------------------------------
+template <int TW_>
 __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = my_tile(v, blockIdx.y, warp);
-    if (tile < 0) return;
-    const int TW = v.tw, le = min(lane, TW - 1);
-    const int t = tile * TW + le;
-    if (!v.active[t]) return;
+    const int t = (blockIdx.y * kSuper + warp) * 32 + lane;  // 32 consecutive tasks per warp
+    if (t >= v.n_tasks || !v.active[t]) return;
+    const int TW = TW_ ? TW_ : v.tw;
     if (v.flag[t]) {  // frozen pivot collapsed: stop, never update V
         if (blockIdx.x == 0) {
             v.status[t] = GBNR_SINGULAR;
@@ -940,7 +938,7 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
         return;
     }
     const size_t bp = v.bpad;
-    const double* b_t = v.b + size_t(tile) * v.tstride + le;  // tile-blocked b tape
+    const double* b_t = v.b + size_t(t / TW) * v.tstride + (t % TW);  // tile-blocked b tape
     const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
     for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
         const int zt = __ldg(v.zcol_t + bus);
@@ -1012,6 +1010,8 @@ __global__ void broadcast_kernel(double* dst, const double* src, int32_t n, int3
 }
 
 unsigned n_super(const DevView& v) { return unsigned((v.n_tiles + kSuper - 1) / kSuper); }
+// blocks of 8 warps x 32 consecutive tasks (NPM, V update)
+unsigned n_groups8(const DevView& v) { return unsigned((v.n_tasks + 32 * kSuper - 1) / (32 * kSuper)); }
 
 }  // namespace
 
@@ -1064,7 +1064,7 @@ void launch_npm_tw(const DevView& v, dim3 grid, cudaStream_t st) {
 }
 
 void launch_npm(const DevView& v, bool jac, cudaStream_t st) {
-    const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v));
+    const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_groups8(v));
     if (jac)
         launch_npm_tw<true, kJacSpec>(v, grid, st);
     else
@@ -1076,7 +1076,7 @@ void launch_npm(const DevView& v, bool jac, cudaStream_t st) {
 void launch_status_count(const DevView& v, cudaStream_t st) { status_count_kernel<<<1, 1024, 0, st>>>(v); }
 
 void launch_jacobian(const DevView& v, bool all, cudaStream_t st) {
-    const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_super(v));
+    const dim3 grid(unsigned((v.n_rows + kRowChunk - 1) / kRowChunk), n_groups8(v));
     if (all)
         launch_npm_tw<false, kJacAll>(v, grid, st);
     else
@@ -1116,7 +1116,14 @@ void launch_bs_walk(const DevView& v, const WalkView& w, cudaStream_t st) {
 }
 
 void launch_vupdate(const DevView& v, cudaStream_t st) {
-    vupdate_kernel<<<dim3(unsigned((v.n + 31) / 32), n_super(v)), 256, 0, st>>>(v);
+    const dim3 grid(unsigned((v.n + 31) / 32), n_groups8(v));
+    switch (v.tw) {
+        case 8: vupdate_kernel<8><<<grid, 256, 0, st>>>(v); break;
+        case 16: vupdate_kernel<16><<<grid, 256, 0, st>>>(v); break;
+        case 24: vupdate_kernel<24><<<grid, 256, 0, st>>>(v); break;
+        case 32: vupdate_kernel<32><<<grid, 256, 0, st>>>(v); break;
+        default: vupdate_kernel<0><<<grid, 256, 0, st>>>(v); break;
+    }
 }
 
 void launch_flows(const DevView& v, int32_t nb, const int32_t* bf, const int32_t* bt, const double* adm,
