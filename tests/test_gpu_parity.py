@@ -351,7 +351,9 @@ def test_dense_grids_plan_and_match_oracle(name, extra, T):
     gc = load_case(util.case_path(name))
     if extra:
         gc = add_random_branches(gc, extra)
-    plan, oplan, vm0, va0 = _setup_case(gc)
+    # full-width tiles: the smallest per-walker pools, so the global forms run (a
+    # narrower automatic width for 64 tasks would give every column shared rows)
+    plan, oplan, vm0, va0 = _setup_case(gc, tile_width=32)
     p0, q0 = montecarlo(gc, T)
     r = plan.solve(p0, q0, vm0, va0, n_tasks=T)
     o = oplan.solve(p0, q0, vm0[:, None], va0[:, None], n_tasks=T)
