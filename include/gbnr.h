@@ -101,10 +101,10 @@ typedef struct gbnr_options {
                               0 = every shard on `device`, e.g. tests on one GPU)    */
     int32_t chunk_tasks;   /* most tasks per device launch; larger slices are solved in
                               chunks (0 = automatic, from the free device memory)    */
-    int32_t tile_width;    /* tasks per tile, even, 2..32 (0 = automatic: the narrowest
-                              of 8/16/24/32 that keeps one resident wave of tiles, so
-                              smaller batches get deeper shared-memory pools).  Results
-                              never depend on it.                                     */
+    int32_t tile_width;    /* tasks per tile, even, 2..32 (0 = automatic: 24 when that
+                              keeps every SM at three tiles where 32 would not fit two,
+                              else 32; narrower tiles give each walk warp more shared
+                              rows).  Results never depend on it.                    */
 } gbnr_options;
 
 void gbnr_default_options(gbnr_options* opt);

@@ -293,18 +293,19 @@ struct gbnr_plan {
         walks.push_back(std::move(tws));
     }
 
-    // Tile width of a batch of T tasks: the narrowest of 8/16/24/32 lanes whose
-    // tiles all fit one resident wave (n_sm x ctas_per_sm CTAs), so that the smem
-    // rows of a walker -- its prefetch depth and its resident dependencies -- grow
-    // as the batch shrinks below a full wave of 32-task tiles (gbnr_options
-    // tile_width / GBNR_TW override).
+    // Tile width of a batch of T tasks.  The LU walk's time is its busiest SM's:
+    // the number of tiles that SM hosts and the shared-memory rows each walker
+    // gets.  32 lanes while every SM hosts at most two full-width tiles (or the
+    // batch needs three anyway); in between, 24 lanes put at most three tiles on
+    // every SM -- the busiest SM hosts no more tiles than with 32 lanes, and every
+    // walker gets a third more rows (profiles/r02h_tile_width.log: LU walk -7% at
+    // 10k tasks).  gbnr_options.tile_width / GBNR_TW override.
     int32_t choose_tw(int32_t T) const {
         int32_t tw = opt.tile_width;
         if (const char* e = std::getenv("GBNR_TW")) tw = std::atoi(e);
         if (tw > 0) return std::min(gbnr::kTile, std::max(2, tw + (tw & 1)));
-        const int64_t slots = int64_t(n_sm) * ctas_per_sm;
-        for (int32_t c : {8, 16, 24})
-            if (int64_t(T) <= slots * c) return c;
+        const int64_t sm = n_sm;
+        if (int64_t(T) > sm * 2 * gbnr::kTile && int64_t(T) <= sm * ctas_per_sm * 24 && ctas_per_sm >= 3) return 24;
         return gbnr::kTile;
     }
 
