@@ -96,8 +96,14 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
 // tapes are task-contiguous); the Jacobian / F stores go to each task's lane of
 // its tile's A block.  Lanes past the batch shadow its last task (duplicate
 // stores of equal values).
+#ifndef GBNR_NPM_BATCH
+#define GBNR_NPM_BATCH 1  // neighbours whose loads are issued together in the current sweep
+#endif
+#ifndef GBNR_NPM_MINB
+#define GBNR_NPM_MINB 5   // resident blocks per SM the register budget is sized for
+#endif
 template <bool NPM, int JMODE, int TW_>
-__global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
+__global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = blockIdx.y * kSuper + warp;  // group of 32 tasks
     if (g * 32 >= v.n_tasks) return;
@@ -123,7 +129,27 @@ __global__ void __launch_bounds__(256, 5) npm_kernel(DevView v) {
         const int r = __ldg(v.rows + ri);
         const int q0 = __ldg(v.yp + r), q1 = __ldg(v.yp + r + 1);
         double ire = 0.0, iim = 0.0;
-        for (int q = q0; q < q1; ++q) {
+        int q = q0;
+#if GBNR_NPM_BATCH > 1
+        constexpr int NB = GBNR_NPM_BATCH;
+        for (; q + NB <= q1; q += NB) {  // NB neighbours' loads in flight, then the CSR-order sums
+            int kk[NB];
+            double gm[NB], gc[NB], gs[NB], gr[NB], gi[NB];
+#pragma unroll
+            for (int u = 0; u < NB; ++u) kk[u] = __ldg(v.yi + q + u);
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                gm[u] = __ldg(v.vm + kk[u] * bp + t);
+                gc[u] = __ldg(v.c + kk[u] * bp + t);
+                gs[u] = __ldg(v.s + kk[u] * bp + t);
+                gr[u] = __ldg(v.yre + size_t(q + u) * v.y_ld + yt);
+                gi[u] = __ldg(v.yim + size_t(q + u) * v.y_ld + yt);
+            }
+#pragma unroll
+            for (int u = 0; u < NB; ++u) acc_current(gr[u], gi[u], gm[u] * gc[u], gm[u] * gs[u], ire, iim);
+        }
+#endif
+        for (; q < q1; ++q) {
             const int k = __ldg(v.yi + q);
             const double vmk = __ldg(v.vm + k * bp + t);
             acc_current(__ldg(v.yre + size_t(q) * v.y_ld + yt), __ldg(v.yim + size_t(q) * v.y_ld + yt), vmk * __ldg(v.c + k * bp + t),
