@@ -97,7 +97,7 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
 // its tile's A block.  Lanes past the batch shadow its last task (duplicate
 // stores of equal values).
 #ifndef GBNR_NPM_BATCH
-#define GBNR_NPM_BATCH 1  // neighbours whose loads are issued together in the current sweep
+#define GBNR_NPM_BATCH 2  // neighbours whose loads are issued together in the current sweep (A/B: profiles/r02j)
 #endif
 #ifndef GBNR_NPM_MINB
 #define GBNR_NPM_MINB 5   // resident blocks per SM the register budget is sized for
@@ -172,6 +172,9 @@ __global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
             }
         }
         if (JMODE != kJacNone && act) {
+#ifdef GBNR_NPM_JUNROLL
+#pragma unroll 2
+#endif
             for (int q = q0; q < q1; ++q) {
                 const int k = __ldg(v.yi + q);
                 const double ck = __ldg(v.c + k * bp + t), sk = __ldg(v.s + k * bp + t), vmk = __ldg(v.vm + k * bp + t);
