@@ -201,38 +201,64 @@ class OraclePlan:
     def _second_chance(self, n_tasks, yre, yim, ny, p0, q0, ns, tol, max_iter, singular_tol,
                        vm, va, it, cv, st, mm):
         """second_chance_refactorize (open question :436): a task
-        whose frozen pivot collapsed (status singular after `it` linear solves) is
-        re-planned alone -- a fresh threshold-pivoting factorization at its current
-        voltages, kept for the rest of its Newton loop -- and continues with the
-        remaining budget max_iter - (it - 1).  Converged -> status 3
-        (fallback_converged); otherwise the re-run's status.  A fresh
-        factorization that is itself singular leaves the task singular.  Every
-        flagged task gets its re-plan (tasks flagged for the fallback
-        are re-run)."""
+        whose frozen pivot collapsed (status singular after `it` linear solves) gets a
+        fresh threshold-pivoting factorization at its current voltages, kept for the
+        rest of its Newton loop, and continues with the remaining budget
+        max_iter - (it - 1).  Converged -> status 3 (fallback_converged, SPEC.md:384);
+        otherwise the re-run's status.  As the product's plan.cu second_chance: one
+        fresh plan from the flagged task with the largest mismatch at its failure
+        (first of the largest) re-runs every flagged task, grouped by budget; the
+        tasks its pivots do not carry (flagged again) each get their own fresh plan.
+        A task whose own fresh factorization is singular stays singular."""
         ip, ix, _, _, pv, pq = self._keep
-        for t in np.nonzero(st == 2)[0]:
-            budget = max_iter - (int(it[t]) - 1)
-            if budget < 1:
-                continue
-            yr = yre[:, t] if ny > 1 else (yre[:, 0] if yre.ndim == 2 else yre)
-            yi = yim[:, t] if ny > 1 else (yim[:, 0] if yim.ndim == 2 else yim)
-            pp = p0[:, t] if ns > 1 else (p0[:, 0] if p0.ndim == 2 else p0)
-            qq = q0[:, t] if ns > 1 else (q0[:, 0] if q0.ndim == 2 else q0)
-            v_m, v_a = vm[:, t].copy(), va[:, t].copy()
+        col = lambda a, sets, t: (a[:, t] if sets > 1 else (a[:, 0] if a.ndim == 2 else a))  # noqa: E731
+        flagged = [int(t) for t in np.nonzero(st == 2)[0] if max_iter - (int(it[t]) - 1) >= 1]
+        if not flagged:
+            return
+        fail = {t: (vm[:, t].copy(), va[:, t].copy(), int(it[t])) for t in flagged}
+        w = max(flagged, key=lambda t: (float(mm[t]), -t))  # first of the largest
+
+        def fresh(t):
             try:
-                sub = OraclePlan(self.o, self.n_bus, ip, ix, yr, yi, self.ref, pv, pq, v_m, v_a,
-                                 self.pivot_tol)
+                return OraclePlan(self.o, self.n_bus, ip, ix, col(yre, ny, t), col(yim, ny, t), self.ref, pv, pq,
+                                  fail[t][0], fail[t][1], self.pivot_tol)
             except OracleError as e:
                 if e.code != 4:  # only a numerically singular fresh factorization leaves it failed
                     raise
-                continue
-            r = sub.solve(pp[:, None], qq[:, None], v_m[:, None], v_a[:, None], n_tasks=1, tol=tol,
-                          max_iter=budget, singular_tol=singular_tol, n_threads=1, second_chance=False)
-            s2 = int(r["status"][0])
-            st[t] = 3 if s2 == 0 else s2
-            cv[t] = 1 if s2 == 0 else 0
-            it[t] = int(it[t]) - 1 + int(r["iterations"][0])
-            vm[:, t], va[:, t], mm[t] = r["vm"][:, 0], r["va"][:, 0], r["max_mismatch"][0]
+                return None
+
+        def rerun(sub, grp, b, self_t):
+            """grp through sub's pivots; returns the tasks not carried (flagged again)."""
+            pp = np.stack([col(p0, ns, t) for t in grp], axis=1)
+            qq = np.stack([col(q0, ns, t) for t in grp], axis=1)
+            vmg = np.stack([fail[t][0] for t in grp], axis=1)
+            vag = np.stack([fail[t][1] for t in grp], axis=1)
+            y = None if ny == 1 else (np.ascontiguousarray(yre[:, grp]), np.ascontiguousarray(yim[:, grp]))
+            r = sub.solve(pp, qq, vmg, vag, n_tasks=len(grp), y=y, tol=tol, max_iter=b,
+                          singular_tol=singular_tol, n_threads=1, second_chance=False)
+            left = []
+            for j, t in enumerate(grp):
+                s2 = int(r["status"][j])
+                if s2 == 2 and t != self_t:
+                    left.append(t)
+                    continue
+                st[t] = 3 if s2 == 0 else s2
+                cv[t] = 1 if s2 == 0 else 0
+                it[t] = fail[t][2] - 1 + int(r["iterations"][j])
+                vm[:, t], va[:, t], mm[t] = r["vm"][:, j], r["va"][:, j], r["max_mismatch"][j]
+            return left
+
+        # one fresh plan from the worst flagged task for all of them, in one batch per budget
+        sub = fresh(w)
+        rest = [t for t in flagged if t != w] if sub is None else []
+        if sub is not None:
+            for b in sorted({max_iter - (fail[t][2] - 1) for t in flagged}):
+                rest += rerun(sub, [t for t in flagged if max_iter - (fail[t][2] - 1) == b], b, w)
+        # the tasks its pivots did not carry: each its own fresh plan
+        for t in sorted(rest):
+            own = fresh(t)
+            if own is not None:
+                rerun(own, [t], max_iter - (fail[t][2] - 1), t)
 
     def refactor(self, vm, va, singular_tol=1e-14, n_threads=None):
         vm = _f64(vm); va = _f64(va)

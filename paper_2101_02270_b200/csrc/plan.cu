@@ -12,6 +12,7 @@
 #include <cstring>
 #include <array>
 #include <atomic>
+#include <chrono>
 #include <exception>
 #include <functional>
 #include <memory>
@@ -256,12 +257,35 @@ struct gbnr_plan {
         tws->tw = tw;
         gbnr::WalkConfig wc = wcfg;
         wc.row_bytes = tw * 8;
+        // the three programs are independent: planned on three host threads
         auto build = [&] {
-            tws->wf = gbnr::build_forward_walk(sym, lay, true, wc);
-            if (!sub_plan) tws->wl = gbnr::build_forward_walk(sym, lay, false, wc);
-            gbnr::WalkConfig wcb = wc;
-            if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
-            tws->wb = gbnr::build_backward_walk(sym, lay, wcb);
+            std::exception_ptr e1, e2;
+            std::thread tl([&] {
+                try {
+                    if (!sub_plan) tws->wl = gbnr::build_forward_walk(sym, lay, false, wc);
+                } catch (...) {
+                    e1 = std::current_exception();
+                }
+            });
+            std::thread tb([&] {
+                try {
+                    gbnr::WalkConfig wcb = wc;
+                    if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
+                    tws->wb = gbnr::build_backward_walk(sym, lay, wcb);
+                } catch (...) {
+                    e2 = std::current_exception();
+                }
+            });
+            std::exception_ptr e0;
+            try {
+                tws->wf = gbnr::build_forward_walk(sym, lay, true, wc);
+            } catch (...) {
+                e0 = std::current_exception();
+            }
+            tl.join();
+            tb.join();
+            for (auto& e : {e0, e1, e2})
+                if (e) std::rethrow_exception(e);
         };
         build();
         if (on_device) {
@@ -677,49 +701,91 @@ struct gbnr_plan {
     }
 
     // ---- second chance -------------------------------
-    // Every flagged task is re-planned alone: its own threshold-pivoting
-    // factorization at its current voltages (kept for the rest of its Newton loop),
-    // then it continues on this GPU with the remaining budget max_iter - (it - 1).
-    // The re-plans (host symbolic analysis + walk plans) and their one-task solves
-    // run concurrently, one host thread and stream per re-plan.
+    // Every flagged task gets a fresh threshold-pivoting factorization at its
+    // current voltages and continues on this GPU with its remaining budget
+    // max_iter - (it - 1).  A re-plan is a host symbolic analysis plus walk plans
+    // (about 0.3 s at synth9241), so: first one fresh plan from the flagged task
+    // with the largest mismatch at its failure (its own voltages and Ybus values;
+    // first of the largest) solves every flagged task in one batch -- flags that
+    // share a cause are done after one re-plan; the tasks its pivots do not carry
+    // (they collapse again) then each get their own fresh plan, concurrently.
+    // Status 3 on convergence, else the re-run's status; a task whose own fresh
+    // factorization is singular stays singular (oracle/pyoracle.py
+    // OraclePlan._second_chance restates the same rule).
     struct Chance {
         int32_t t = 0, it = 0;
         std::vector<double> vm, va, yr, yi, pp, qq;  // the task's state at the failure
-        bool ran = false;
+        double mm_fail = 0.0;
+        bool done = false, ran = false;
         int32_t status = GBNR_SINGULAR, iters = 0;
         double mm = 0.0;
+        std::vector<double> vm_out, va_out;
     };
 
-    void run_chance(Chance& c) {
+    // options of a second-chance plan: one chance, one device
+    gbnr_options chance_options() const {
         gbnr_options o = opt;
-        o.second_chance = 0;  // one chance
+        o.second_chance = 0;
         o.profile = 0;
         o.n_devices = 1;
         o.chunk_tasks = 0;
-        o.max_iter = opt.max_iter - (c.it - 1);
-        gbnr_plan* sub = nullptr;
-        const int rc = create_plan(sym.n, sym.yp.data(), sym.yi.data(), c.yr.data(), c.yi.data(), sym.ref,
-                                   in_pv.data(), int32_t(in_pv.size()), in_pq.data(), int32_t(in_pq.size()),
-                                   c.vm.data(), c.va.data(), &o, &sub, true);
-        if (rc == GBNR_ESINGULAR) return;  // still singular: the task stays failed
-        if (rc != GBNR_OK) throw Error(rc, std::string("second chance: ") + gbnr_last_error());
-        std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(sub, gbnr_plan_destroy);
-        sub->stage_ybus(nullptr, nullptr, 1, 1);
-        sub->stage(1, c.pp.data(), c.qq.data(), 1, c.vm.data(), c.va.data(), 1);
-        sub->run(false);
-        int32_t s2 = 0, i2 = 0;
-        sub->fetch(c.vm.data(), c.va.data(), &i2, nullptr, &s2, &c.mm);
-        c.status = s2 == GBNR_CONVERGED ? GBNR_FALLBACK_CONVERGED : s2;
-        c.iters = c.it - 1 + i2;
-        c.ran = true;
+        return o;
+    }
+
+    // Solve the chances `grp` (budget b) through the fresh plan `sp` in one batch; a
+    // task that does not collapse again -- or the plan's own representative `self`,
+    // whatever becomes of it -- takes the re-run's results.
+    void run_chances(gbnr_plan& sp, std::vector<Chance>& work, const std::vector<int32_t>& grp, int32_t b,
+                     bool per_y, int32_t self) {
+        const int32_t n = sym.n, nY = sym.nnzY, m = int32_t(grp.size());
+        std::vector<double> P(size_t(n) * m), Q(P.size()), VM(P.size()), VA(P.size());
+        std::vector<double> YR(per_y ? size_t(nY) * m : 0), YI(YR.size());
+        for (int32_t j = 0; j < m; ++j) {
+            const Chance& c = work[grp[j]];
+            for (int32_t q = 0; q < n; ++q) {
+                P[size_t(q) * m + j] = c.pp[q];
+                Q[size_t(q) * m + j] = c.qq[q];
+                VM[size_t(q) * m + j] = c.vm[q];
+                VA[size_t(q) * m + j] = c.va[q];
+            }
+            if (per_y)
+                for (int32_t q = 0; q < nY; ++q) {
+                    YR[size_t(q) * m + j] = c.yr[q];
+                    YI[size_t(q) * m + j] = c.yi[q];
+                }
+        }
+        std::vector<double> ovm(P.size()), ova(P.size()), omm(m);
+        std::vector<int32_t> oit(m), ost(m);
+        sp.opt.max_iter = b;
+        sp.v.max_iter = b;
+        const SolveIn in{m, per_y ? YR.data() : nullptr, per_y ? YI.data() : nullptr, per_y ? m : 1,
+                         P.data(), Q.data(), m, VM.data(), VA.data(), m};
+        const SolveOut out{ovm.data(), ova.data(), oit.data(), nullptr, ost.data(), omm.data()};
+        sp.solve_general(in, out, false);
+        for (int32_t j = 0; j < m; ++j) {
+            Chance& c = work[grp[j]];
+            if (ost[j] == GBNR_SINGULAR && grp[j] != self) continue;  // not carried: its own plan next
+            c.done = c.ran = true;
+            c.status = ost[j] == GBNR_CONVERGED ? GBNR_FALLBACK_CONVERGED : ost[j];
+            c.iters = c.it - 1 + oit[j];
+            c.mm = omm[j];
+            c.vm_out.resize(n);
+            c.va_out.resize(n);
+            for (int32_t q = 0; q < n; ++q) {
+                c.vm_out[q] = ovm[size_t(q) * m + j];
+                c.va_out[q] = ova[size_t(q) * m + j];
+            }
+        }
     }
 
     void second_chance() {
         CK(cudaSetDevice(opt.device));
         const int32_t nt = v.n_tasks, n = sym.n, nY = sym.nnzY;
         std::vector<int32_t> st(nt), it(nt);
+        std::vector<double> mmf(nt);
         CK(cudaMemcpyAsync(st.data(), v.status, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
         CK(cudaMemcpyAsync(it.data(), v.iters, size_t(nt) * 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(mmf.data(), v.maxmis, size_t(nt) * 8, cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         std::vector<Chance> work;
         const size_t bp = size_t(v.bpad);
@@ -732,6 +798,7 @@ struct gbnr_plan {
             Chance c;
             c.t = t;
             c.it = it[t];
+            c.mm_fail = mmf[t];
             column(c.vm, v.vm + t, bp, n);
             column(c.va, v.va + t, bp, n);
             column(c.yr, v.yre + size_t(t) * v.y_inc, size_t(v.y_ld), nY);
@@ -742,30 +809,80 @@ struct gbnr_plan {
         }
         CK(cudaStreamSynchronize(stream));
         if (work.empty()) return;
-        // workers: host threads, bounded by the cores and by the device memory a
-        // one-task plan needs next to this batch
-        size_t free_b = 0, total_b = 0;
-        CK(cudaMemGetInfo(&free_b, &total_b));
-        const size_t per_plan = bytes_per_task(false) * gbnr::kTile + (size_t(64) << 20);
-        const size_t by_mem = free_b > (size_t(1) << 30) ? (free_b - (size_t(1) << 30)) / per_plan : 1;
-        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        const size_t W = std::max<size_t>(1, std::min({work.size(), size_t(std::min(hw, 16u)), by_mem}));
-        std::atomic<size_t> next{0};
-        std::vector<std::exception_ptr> errs(W);
-        auto worker = [&](size_t w) {
-            try {
-                for (size_t i; (i = next.fetch_add(1)) < work.size();) run_chance(work[i]);
-            } catch (...) {
-                errs[w] = std::current_exception();
-                next = work.size();
+        const bool per_y = v.y_inc != 0;
+        // round 1: the representative's fresh plan for every flagged task, in one batch
+        // per remaining budget
+        int32_t w = 0;  // largest mismatch at failure, first of the largest
+        for (int32_t i = 1; i < int32_t(work.size()); ++i)
+            if (work[i].mm_fail > work[w].mm_fail) w = i;
+        gbnr_plan* sub = nullptr;
+        const gbnr_options co = chance_options();
+        {
+            const Chance& rep = work[w];
+            const int rc = create_plan(n, sym.yp.data(), sym.yi.data(), rep.yr.data(), rep.yi.data(), sym.ref,
+                                       in_pv.data(), int32_t(in_pv.size()), in_pq.data(), int32_t(in_pq.size()),
+                                       rep.vm.data(), rep.va.data(), &co, &sub, true);
+            if (rc == GBNR_ESINGULAR) {
+                work[w].done = true;  // no fresh factorization: the representative stays failed
+                sub = nullptr;
+            } else if (rc != GBNR_OK) {
+                throw Error(rc, std::string("second chance: ") + gbnr_last_error());
             }
-        };
-        std::vector<std::thread> pool;
-        for (size_t w = 1; w < W; ++w) pool.emplace_back(worker, w);
-        worker(0);
-        for (auto& th : pool) th.join();
-        for (auto& e : errs)
-            if (e) std::rethrow_exception(e);
+        }
+        if (sub) {
+            std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> guard(sub, gbnr_plan_destroy);
+            std::vector<int32_t> budgets;
+            for (const Chance& c : work) budgets.push_back(opt.max_iter - (c.it - 1));
+            std::sort(budgets.begin(), budgets.end());
+            budgets.erase(std::unique(budgets.begin(), budgets.end()), budgets.end());
+            for (int32_t b : budgets) {
+                std::vector<int32_t> grp;
+                for (int32_t i = 0; i < int32_t(work.size()); ++i)
+                    if (opt.max_iter - (work[i].it - 1) == b) grp.push_back(i);
+                run_chances(*sub, work, grp, b, per_y, w);
+            }
+            work[w].done = true;
+        }
+        // the tasks the representative's pivots did not carry: each its own fresh
+        // plan, concurrently (host threads, one plan and stream each)
+        std::vector<int32_t> rest;
+        for (int32_t i = 0; i < int32_t(work.size()); ++i)
+            if (!work[i].done) rest.push_back(i);
+        if (!rest.empty()) {
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            const size_t per_plan = bytes_per_task(false) * gbnr::kTile + (size_t(64) << 20);
+            const size_t by_mem = free_b > (size_t(1) << 30) ? (free_b - (size_t(1) << 30)) / per_plan : 1;
+            const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+            const size_t W = std::max<size_t>(1, std::min({rest.size(), size_t(std::min(hw, 16u)), by_mem}));
+            std::atomic<size_t> next{0};
+            std::vector<std::exception_ptr> errs(W);
+            auto worker = [&](size_t wk) {
+                try {
+                    for (size_t j; (j = next.fetch_add(1)) < rest.size();) {
+                        Chance& c = work[rest[j]];
+                        gbnr_plan* own = nullptr;
+                        const int rc = create_plan(n, sym.yp.data(), sym.yi.data(), c.yr.data(), c.yi.data(),
+                                                   sym.ref, in_pv.data(), int32_t(in_pv.size()), in_pq.data(),
+                                                   int32_t(in_pq.size()), c.vm.data(), c.va.data(),
+                                                   &co, &own, true);
+                        if (rc == GBNR_ESINGULAR) continue;  // the task stays failed
+                        if (rc != GBNR_OK) throw Error(rc, std::string("second chance: ") + gbnr_last_error());
+                        std::unique_ptr<gbnr_plan, void (*)(gbnr_plan*)> g(own, gbnr_plan_destroy);
+                        run_chances(*own, work, {rest[j]}, opt.max_iter - (c.it - 1), per_y, rest[j]);
+                    }
+                } catch (...) {
+                    errs[wk] = std::current_exception();
+                    next = rest.size();
+                }
+            };
+            std::vector<std::thread> pool;
+            for (size_t wk = 1; wk < W; ++wk) pool.emplace_back(worker, wk);
+            worker(0);
+            for (auto& th : pool) th.join();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
+        }
         // results -> this batch's device state (statuses, iterations, mismatch, V)
         CK(cudaSetDevice(opt.device));
         for (const Chance& c : work) {
@@ -774,8 +891,8 @@ struct gbnr_plan {
             CK(cudaMemcpy(v.status + t, &c.status, 4, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(v.iters + t, &c.iters, 4, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(v.maxmis + t, &c.mm, 8, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy2D(v.vm + t, bp * 8, c.vm.data(), 8, 8, size_t(n), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy2D(v.va + t, bp * 8, c.va.data(), 8, 8, size_t(n), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy2D(v.vm + t, bp * 8, c.vm_out.data(), 8, 8, size_t(n), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy2D(v.va + t, bp * 8, c.va_out.data(), 8, 8, size_t(n), cudaMemcpyHostToDevice));
         }
         gbnr::launch_status_count(v, stream);
         CK(cudaStreamSynchronize(stream));
@@ -1290,11 +1407,13 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         if (p->opt.tile_width < 0 || p->opt.tile_width > gbnr::kTile || (p->opt.tile_width & 1))
             throw Error(GBNR_ECONFIG, "tile_width must be 0 (automatic) or even in 2..32");
         p->sub_plan = sub;
+        const auto t0 = std::chrono::steady_clock::now();
         p->sym.analyze(n_bus, indptr, indices, y_re, y_im, ref, pv, n_pv, pq, n_pq, vm0, va0,
                        p->opt.pivot_tol);
         p->in_pv.assign(pv, pv + n_pv);
         p->in_pq.assign(pq, pq + n_pq);
         p->lay = gbnr::build_lu_layout(p->sym);
+        const auto t1 = std::chrono::steady_clock::now();
         gbnr::WalkConfig wc;
         if (p->opt.ring_rows) wc.ring_rows = p->opt.ring_rows;
         if (p->opt.stage_rows) wc.stage_rows = p->opt.stage_rows;
@@ -1322,6 +1441,10 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         if (const char* e = std::getenv("GBNR_CTAS")) p->ctas_per_sm = std::max(1, std::atoi(e));
         if (p->opt.device < 0) {
             p->cur = p->walks_for(gbnr::kTile);  // host-only plan: the full-width programs (inspection, tests)
+            if (std::getenv("GBNR_PLAN_TIMING"))
+                std::fprintf(stderr, "[plan] analysis %.1f ms, walks %.1f ms\n",
+                             std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
         } else {
             int ndev = 0;
             CK(cudaGetDeviceCount(&ndev));
