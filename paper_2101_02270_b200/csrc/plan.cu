@@ -57,13 +57,16 @@ int guarded(F&& f) {
     }
 }
 
+// Device memory is stream-ordered (cudaMallocAsync / cudaFreeAsync on the plan's
+// stream): a plan freeing its buffers never synchronizes the device, so the
+// concurrent second-chance plans of one solve do not serialize each other.
 template <class T>
-T* dev_upload(std::vector<void*>& owned, const std::vector<T>& h) {
+T* dev_upload(std::vector<void*>& owned, const std::vector<T>& h, cudaStream_t st) {
     T* d = nullptr;
     const size_t bytes = std::max<size_t>(h.size(), 1) * sizeof(T);
-    CK(cudaMalloc(&d, bytes));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st));
     owned.push_back(d);
-    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!h.empty()) CK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     return d;
 }
 
@@ -133,19 +136,33 @@ struct gbnr_plan {
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_used;  // (phase, first event index)
 
+    template <class T>
+    T* dev_upload_s(const std::vector<T>& h) {
+        return dev_upload(owned, h, stream);
+    }
+    void* dmalloc(size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), stream));
+        return p;
+    }
+    void dfree(void* p) {
+        if (p) cudaFreeAsync(p, stream);
+    }
+
     ~gbnr_plan() {
         if (!on_device) return;
         cudaSetDevice(opt.device);
         if (stream) cudaStreamSynchronize(stream);
-        for (void* p : batch) cudaFree(p);
-        for (void* p : owned) cudaFree(p);
+        for (void* p : batch) dfree(p);
+        for (void* p : owned) dfree(p);
         if (h_count) cudaFreeHost(h_count);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-        for (void* q : pipe) cudaFree(q);
-        if (y_task_re) cudaFree(y_task_re);
-        if (y_task_im) cudaFree(y_task_im);
+        for (void* q : pipe) dfree(q);
+        dfree(y_task_re);
+        dfree(y_task_im);
+        if (stream) cudaStreamSynchronize(stream);
         for (int i = 0; i < 2; ++i) {
             for (cudaEvent_t e : {ev_in[i], ev_free_in[i], ev_res[i], ev_out[i]})
                 if (e) cudaEventDestroy(e);
@@ -176,18 +193,18 @@ struct gbnr_plan {
         CK(cudaEventCreate(&ev1));
         gbnr::configure_kernels();
         const gbnr::Symbolic& s = sym;
-        CK(cudaMalloc(&d_scratch, size_t(s.n) * sizeof(double)));
+        d_scratch = static_cast<double*>(dmalloc(size_t(s.n) * sizeof(double)));
         owned.push_back(d_scratch);
         v.n = s.n;
         v.nJ = s.nJ;
         v.nnzY = s.nnzY;
         v.n_rows = static_cast<int32_t>(s.rows.size());
         v.nnzLU = static_cast<int32_t>(s.nnzLU);
-        v.yp = dev_upload(owned, s.yp);
-        v.yi = dev_upload(owned, s.yi);
-        v.rows = dev_upload(owned, s.rows);
-        v.brow_p = dev_upload(owned, s.brow_p);
-        v.brow_q = dev_upload(owned, s.brow_q);
+        v.yp = dev_upload_s(s.yp);
+        v.yi = dev_upload_s(s.yi);
+        v.rows = dev_upload_s(s.rows);
+        v.brow_p = dev_upload_s(s.brow_p);
+        v.brow_q = dev_upload_s(s.brow_q);
         {
             // A-tape slots (walk.hpp LuLayout): CCS entry z of column j at z + j,
             // F_m right after column m
@@ -199,9 +216,9 @@ struct gbnr_plan {
             auto fslot = [&](int32_t m) { return m >= 0 ? gbnr::a_slot(s.cp[m + 1], m) : -1; };
             for (size_t r = 0; r < fp.size(); ++r) fp[r] = fslot(s.brow_p[r]);
             for (size_t r = 0; r < fq.size(); ++r) fq[r] = fslot(s.brow_q[r]);
-            v.lk = dev_upload(owned, lk);
-            v.fslot_p = dev_upload(owned, fp);
-            v.fslot_q = dev_upload(owned, fq);
+            v.lk = dev_upload_s(lk);
+            v.fslot_p = dev_upload_s(fp);
+            v.fslot_q = dev_upload_s(fq);
             v.tape_rows = lay.rows;
         }
         {
@@ -210,20 +227,21 @@ struct gbnr_plan {
             std::vector<int32_t> zt(s.zcol_t), zv(s.zcol_v);
             for (int32_t& z : zt) z = z >= 0 ? s.nJ - 1 - z : -1;
             for (int32_t& z : zv) z = z >= 0 ? s.nJ - 1 - z : -1;
-            v.zcol_t = dev_upload(owned, zt);
-            v.zcol_v = dev_upload(owned, zv);
+            v.zcol_t = dev_upload_s(zt);
+            v.zcol_v = dev_upload_s(zv);
         }
         int32_t* itd = nullptr;
-        CK(cudaMalloc(&itd, sizeof(int32_t)));
+        itd = static_cast<int32_t*>(dmalloc(sizeof(int32_t)));
         owned.push_back(itd);
         v.it_dev = itd;
         if (const char* d = std::getenv("GBNR_DBG")) v.dbg = std::atoi(d);
 #ifdef GBNR_PROF
         if (v.dbg & 8) {
-            CK(cudaMalloc(&v.prof, 4 * 8 * 16 * sizeof(unsigned long long)));
+            v.prof = static_cast<unsigned long long*>(dmalloc(4 * 8 * 16 * sizeof(unsigned long long)));
             owned.push_back(v.prof);
         }
 #endif
+        CK(cudaStreamSynchronize(stream));
         v.tol = opt.tol;
         v.singular_tol = opt.singular_tol;
         v.max_iter = opt.max_iter;
@@ -232,7 +250,7 @@ struct gbnr_plan {
 
     gbnr::WalkView upload_walk(const gbnr::WalkSet& w, int32_t tw) {
         gbnr::WalkView x{};
-        x.stream = dev_upload(owned, w.stream);
+        x.stream = dev_upload_s(w.stream);
         x.walkers = w.walkers;
         x.page_words = w.page_words;
         x.rows = w.rows;
@@ -298,6 +316,7 @@ struct gbnr_plan {
             tws->vf = upload_walk(tws->wf, tw);
             if (!sub_plan) tws->vl = upload_walk(tws->wl, tw);
             tws->vb = upload_walk(tws->wb, tw);
+            CK(cudaStreamSynchronize(stream));
         }
         walks.push_back(std::move(tws));
         return walks.back().get();
@@ -314,6 +333,7 @@ struct gbnr_plan {
         tws->vf = upload_walk(tws->wf, src.tw);
         if (!sub_plan) tws->vl = upload_walk(tws->wl, src.tw);
         tws->vb = upload_walk(tws->wb, src.tw);
+        CK(cudaStreamSynchronize(stream));
         walks.push_back(std::move(tws));
     }
 
@@ -342,8 +362,8 @@ struct gbnr_plan {
     void set_ybus(const double* re, const double* im) {
         y_host_re.assign(re, re + sym.nnzY);
         y_host_im.assign(im, im + sym.nnzY);
-        v.yre = y_shared_re = dev_upload(owned, y_host_re);
-        v.yim = y_shared_im = dev_upload(owned, y_host_im);
+        v.yre = y_shared_re = dev_upload_s(y_host_re);
+        v.yim = y_shared_im = dev_upload_s(y_host_im);
         v.y_ld = 1;
         v.y_inc = 0;
     }
@@ -390,12 +410,13 @@ struct gbnr_plan {
     void ensure_ytask(size_t bytes) {
         if (bytes <= y_task_cap) return;
         CK(cudaStreamSynchronize(stream));
-        if (y_task_re) cudaFree(y_task_re);
-        if (y_task_im) cudaFree(y_task_im);
+        dfree(y_task_re);
+        dfree(y_task_im);
         y_task_re = y_task_im = nullptr;
         y_task_cap = 0;
-        CK(cudaMalloc(&y_task_re, bytes));
-        CK(cudaMalloc(&y_task_im, bytes));
+        y_task_re = static_cast<double*>(dmalloc(bytes));
+        y_task_im = static_cast<double*>(dmalloc(bytes));
+        CK(cudaStreamSynchronize(stream));
         y_task_cap = bytes;
     }
 
@@ -431,14 +452,13 @@ struct gbnr_plan {
     void ensure_capacity(size_t lanes, int32_t scratch_rows) {
         if (lanes <= cap_lanes && scratch_rows <= cap_scratch) return;
         CK(cudaStreamSynchronize(stream));
-        for (void* p : batch) cudaFree(p);
+        for (void* p : batch) dfree(p);
         batch.clear();
         lanes = std::max(lanes, cap_lanes);
         scratch_rows = std::max(scratch_rows, cap_scratch);
         batch_bytes = 0;
         auto alloc = [&](size_t bytes) {
-            void* p = nullptr;
-            CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+            void* p = dmalloc(bytes);
             batch.push_back(p);
             batch_bytes += bytes;
             return p;
@@ -478,6 +498,7 @@ struct gbnr_plan {
         v.active_count = static_cast<int32_t*>(alloc(128 * sizeof(int32_t)));
         cap_lanes = lanes;
         cap_scratch = scratch_rows;
+        CK(cudaStreamSynchronize(stream));  // stream-ordered allocations ready for every stream
     }
 
     // Tile geometry of a batch of n_tasks tasks at tile width tw (its walks current).
@@ -1058,14 +1079,13 @@ struct gbnr_plan {
     void ensure_pipe(size_t lanes) {
         if (lanes <= pipe_lanes) return;
         CK(cudaDeviceSynchronize());
-        for (void* q : pipe) cudaFree(q);
+        for (void* q : pipe) dfree(q);
         pipe.clear();
         const size_t nb = size_t(sym.n) * lanes * sizeof(double);
         const size_t tb = lanes;
         pipe_bytes = 0;
         auto alloc = [&](size_t bytes) {
-            void* q = nullptr;
-            CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+            void* q = dmalloc(bytes);
             pipe.push_back(q);
             pipe_bytes += bytes;
             return q;
@@ -1086,6 +1106,7 @@ struct gbnr_plan {
             out_st[i] = static_cast<int32_t*>(alloc(tb * sizeof(int32_t)));
         }
         pipe_lanes = lanes;
+        CK(cudaStreamSynchronize(stream));  // the copy streams use these buffers next
     }
 
     // Pipelined sequence of batches (all of n_tasks tasks, injections per task,
@@ -1205,8 +1226,7 @@ struct gbnr_plan {
         const size_t T = size_t(v.n_tasks), out_bytes = size_t(nb) * T * 8;
         std::vector<void*> tmp;
         auto up = [&](const void* h, size_t bytes) {
-            void* d = nullptr;
-            CK(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
+            void* d = dmalloc(bytes);
             tmp.push_back(d);
             if (h) CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
             return d;
@@ -1225,10 +1245,10 @@ struct gbnr_plan {
                 if (h[i]) CK(cudaMemcpyAsync(h[i], o[i], out_bytes, cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
         } catch (...) {
-            for (void* q : tmp) cudaFree(q);
+            for (void* q : tmp) dfree(q);
             throw;
         }
-        for (void* q : tmp) cudaFree(q);
+        for (void* q : tmp) dfree(q);
     }
 
     // walker time breakdown of the launches since the last reset (GBNR_PROF builds)
