@@ -95,6 +95,30 @@ def reduce_sum(r: Rank, x: float) -> float:
     return float(t.item())
 
 
+def gather_columns(r: Rank, arrays, total: int):
+    """The final host gather: every rank's result arrays, columns
+    [task0, task0 + count) of its shard (2-D [rows][count] or 1-D [count]), are
+    assembled on rank 0 into arrays over all `total` tasks; other ranks get None.
+    Runs once after the solve, outside any timed region."""
+    import numpy as np
+    if r.world == 1:
+        return list(arrays)
+    import torch.distributed as td
+    task0, count = shard(total, r.world, r.rank)
+    parts = [None] * r.world if r.is_root else None
+    td.gather_object((task0, [np.asarray(a) for a in arrays]), parts, dst=0)
+    if not r.is_root:
+        return None
+    out = []
+    for i, a in enumerate(arrays):
+        a = np.asarray(a)
+        full = np.empty(a.shape[:-1] + (total,), a.dtype)
+        for t0, arrs in parts:
+            full[..., t0:t0 + arrs[i].shape[-1]] = arrs[i]
+        out.append(full)
+    return out
+
+
 def finalize(r: Rank) -> None:
     if r.world > 1:
         import torch.distributed as td

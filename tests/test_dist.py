@@ -62,11 +62,15 @@ def _worker(rank, world, port, total, q):
     r = plan.solve(p0, q0, vm0[:, None], va0[:, None], n_threads=1)
     conv = dist.reduce_sum(rk, int(r["converged"].sum()))
     tmax = dist.reduce_max(rk, float(rk.rank + 1))
+    g = dist.gather_columns(rk, [r["vm"], r["va"], r["iterations"]], total)
+    if rk.is_root:
+        np.save(os.path.join(os.environ["GBNR_TEST_OUT"], "gathered.npy"), np.concatenate([g[0], g[1]]))
     q.put((rk.rank, t0, r["iterations"].tolist(), conv, tmax))
     dist.finalize(rk)
 
 
-def test_gloo_world2_sharded_solve_equals_single():
+def test_gloo_world2_sharded_solve_equals_single(tmp_path, monkeypatch):
+    monkeypatch.setenv("GBNR_TEST_OUT", str(tmp_path))
     total, world = 101, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -89,3 +93,5 @@ def test_gloo_world2_sharded_solve_equals_single():
     assert its == full["iterations"].tolist()
     assert all(r[3] == int(full["converged"].sum()) for r in res)
     assert all(r[4] == float(world) for r in res)
+    # the final gather on rank 0 reassembles the whole batch's voltages
+    np.testing.assert_array_equal(np.load(tmp_path / "gathered.npy"), np.concatenate([full["vm"], full["va"]]))
