@@ -86,7 +86,7 @@ struct WalkConfig {
     int32_t page_words = 128;     // program-stream page (grown to the longest record)
     int32_t pages = 2;            // program-stream pages resident per walker
     double balance = 1.5;         // split subtrees heavier than total / (walkers * balance)
-    double stage_frac = 0.3;      // staging share of a walker's rows (split plan; the
+    double stage_frac = 0.45;     // staging share of a walker's rows (split plan; the
                                   // subtree partition sizes columns against it too)
     double stage_frac_up = 0.3;   // staging share above level 0 (< 0: stage_frac)
     double global_frac = 0.0;     // > 0: also stage in global memory every block larger than
