@@ -838,8 +838,9 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
 }
 
 // Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
+// up to kBsWarps walkers, three CTAs per SM
 template <int TW_>
-__global__ void __launch_bounds__(256, 3) bs_walk_kernel(DevView v, WalkView w) {
+__global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
@@ -1068,6 +1069,12 @@ void configure_kernels() {
     configure_width<16>();
     configure_width<24>();
     configure_width<32>();
+}
+
+int bs_ctas_per_sm(size_t smem, int threads) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, bs_walk_kernel<32>, threads, smem) != cudaSuccess) return 0;
+    return n;
 }
 
 int walk_ctas_per_sm(size_t smem, int threads) {

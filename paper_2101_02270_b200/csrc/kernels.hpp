@@ -71,12 +71,17 @@ struct WalkView {
     const int32_t* stream;  // program words (walk.hpp kRec*), walker-major pages
     int32_t walkers, page_words, rows;
     int32_t tw;             // tile width the program's row budget was planned for
-    int32_t wpage0[9];      // first page of each walker's program
+    int32_t wpage0[17];     // first page of each walker's program (<= 16 walkers)
 };
+
+// Most backward-walk warps per CTA (its kernel's launch bound).  12 warps fit three
+// CTAs per SM at 56 registers but ran no faster than 8 at 78 (profiles/r02q_bs_walkers.log).
+constexpr int kBsWarps = 8;
 
 size_t walk_smem_bytes(const WalkView& w);
 void configure_kernels();
 int walk_ctas_per_sm(size_t smem, int threads);  // resident LU-walk CTAs per SM
+int bs_ctas_per_sm(size_t smem, int threads);    // resident backward-walk CTAs per SM
 void launch_init(const DevView& v, cudaStream_t st);
 // NPM + convergence + iteration bump; with jac, also the next Jacobian of every
 // active task not predicted to converge at this check

@@ -255,7 +255,7 @@ struct gbnr_plan {
         x.page_words = w.page_words;
         x.rows = w.rows;
         x.tw = tw;
-        if (w.walkers < 1 || w.walkers > 8) throw Error(GBNR_ECONFIG, "1..8 walkers per tile");
+        if (w.walkers < 1 || w.walkers > 16) throw Error(GBNR_ECONFIG, "1..16 walkers per tile");
         for (int32_t i = 0; i <= w.walkers; ++i) x.wpage0[i] = w.wpage0[i];
         if (w.barriers != 32 || w.pages != 2) throw Error(GBNR_ECONFIG, "walk kernels use 32 barriers, 2 pages");
         if (w.row_bytes != tw * 8 || gbnr::walk_smem_bytes(x) != w.smem_bytes())
@@ -263,6 +263,13 @@ struct gbnr_plan {
         if (gbnr::walk_smem_bytes(x) > 227 * 1024)
             throw Error(GBNR_ECONFIG, "walk needs more shared memory than a B200 CTA has");
         return x;
+    }
+
+    // Walkers of the backward walk (at most kBsWarps; GBNR_BS_WALKERS overrides).
+    int32_t bs_walkers() const {
+        int32_t k = std::min(gbnr::kBsWarps, std::max(opt.walkers, 1) == 8 ? gbnr::kBsWarps : opt.walkers);
+        if (const char* e = std::getenv("GBNR_BS_WALKERS")) k = std::atoi(e);
+        return std::max(1, std::min(k, gbnr::kBsWarps));
     }
 
     // The walks of tile width tw, planned (and on a device plan uploaded) on first
@@ -288,6 +295,7 @@ struct gbnr_plan {
             std::thread tb([&] {
                 try {
                     gbnr::WalkConfig wcb = wc;
+                    wcb.walkers = bs_walkers();
                     if (const char* e = std::getenv("GBNR_BS_STAGE_FRAC")) wcb.stage_frac = std::atof(e);
                     tws->wb = gbnr::build_backward_walk(sym, lay, wcb);
                 } catch (...) {
@@ -308,7 +316,8 @@ struct gbnr_plan {
         build();
         if (on_device) {
             CK(cudaSetDevice(opt.device));
-            while (gbnr::walk_ctas_per_sm(tws->wf.smem_bytes(), 32 * tws->wf.walkers) < ctas_per_sm &&
+            while ((gbnr::walk_ctas_per_sm(tws->wf.smem_bytes(), 32 * tws->wf.walkers) < ctas_per_sm ||
+                    gbnr::bs_ctas_per_sm(tws->wb.smem_bytes(), 32 * tws->wb.walkers) < ctas_per_sm) &&
                    wc.smem_budget > 65536) {
                 wc.smem_budget -= 1024;
                 build();

@@ -1070,7 +1070,7 @@ struct Schedule {
 // Walkers per level halve until one walks the remaining top alone.
 Schedule choose_schedule(const Symbolic& s, const WalkConfig& cfg, Geometry& g, bool backward) {
     Schedule sc;
-    sc.K = std::max(1, std::min(cfg.walkers, 8));
+    sc.K = std::max(1, std::min(cfg.walkers, 16));
     for (;;) {
         g = geometry(s, cfg, sc.K);
         sc.lvl_walkers.clear();
