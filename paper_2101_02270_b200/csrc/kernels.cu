@@ -343,7 +343,6 @@ struct Prog {
     const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
     int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
     int W, n_pages, page;
-    unsigned slot0, slot_stride;  // team job slots (shared window)
 };
 
 // Debug timeline (GBNR_DBG & 4): kernel start (-1), phase barrier (0), end (1).
@@ -387,12 +386,8 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
                                            int lane) {
     extern __shared__ __align__(128) unsigned char walk_smem[];
     P.R = reinterpret_cast<double*>(walk_smem);
-    const size_t per_warp = size_t(kWalkPages) * w.page_words * 4 + (kWalkBars + kWalkPages + kTeamSlotWords) * 8;
-    unsigned char* mine = walk_smem + size_t(w.rows) * size_t(w.tw) * 8 + size_t(warp) * per_warp;
-    // team job slots: warp L's at slot0 + L * slot_stride (after its page barriers)
-    P.slot0 = smem_u32(walk_smem + size_t(w.rows) * size_t(w.tw) * 8 + size_t(kWalkPages) * w.page_words * 4 +
-                       (kWalkBars + kWalkPages) * 8);
-    P.slot_stride = unsigned(per_warp);
+    unsigned char* mine = walk_smem + size_t(w.rows) * size_t(w.tw) * 8 +
+                          size_t(warp) * (size_t(kWalkPages) * w.page_words * 4 + (kWalkBars + kWalkPages) * 8);
     P.pg = reinterpret_cast<int32_t*>(mine);
     P.bar = reinterpret_cast<unsigned long long*>(mine + size_t(kWalkPages) * w.page_words * 4);
     P.pbar = P.bar + kWalkBars;
@@ -458,109 +453,6 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
     mbar_wait(P.bar + (op & (kWalkBars - 1)), unsigned((op / kWalkBars) & 1));
 }
 
-// ---- teams (walk.hpp kRecTeam) ---------------------------------------------
-// In a phase with fewer walkers than warps, a walker's idle warps help it with
-// long dependency updates: the walker posts a job (the dependency's rows, its x
-// block, its destination words) in its slot, the team meets at the walker's named
-// barrier, every member updates its share of the 4-row groups of x, and the team
-// meets again before the walker goes on.  Each x element still sees the same
-// operations in the same order (the rows of one update are independent), so the
-// bits do not change.  Job words: kind (0 = end of phase, 1 = DEP, 2 = DEP2), rows,
-// s1, s2, xs (lane-0 shared addresses), destination words, kpos1, kpos2.
-__device__ __forceinline__ int32_t lds32(unsigned a) {
-    int32_t r;
-    asm volatile("ld.shared.s32 %0, [%1];\n" : "=r"(r) : "r"(a) : "memory");
-    return r;
-}
-__device__ __forceinline__ void sts32(unsigned a, int32_t x) {
-    asm volatile("st.shared.s32 [%0], %1;\n" ::"r"(a), "r"(x) : "memory");
-}
-// named barrier 1 + leader (constant ids, so ptxas reserves 9 of the SM's barriers
-// per CTA, not all 16)
-template <int ID>
-__device__ __forceinline__ void bar_id(int threads) {
-    asm volatile("bar.sync %0, %1;\n" ::"n"(ID), "r"(threads) : "memory");
-}
-__device__ __forceinline__ void team_bar(int id, int threads) {
-    switch (id) {
-        case 1: bar_id<1>(threads); break;
-        case 2: bar_id<2>(threads); break;
-        case 3: bar_id<3>(threads); break;
-        case 4: bar_id<4>(threads); break;
-        case 5: bar_id<5>(threads); break;
-        case 6: bar_id<6>(threads); break;
-        case 7: bar_id<7>(threads); break;
-        default: bar_id<8>(threads); break;
-    }
-}
-__device__ __forceinline__ void team_post(unsigned slot, int kind, int nrows, unsigned s1, unsigned s2, unsigned xs,
-                                          unsigned dw, int kpos1, int kpos2) {
-    sts32(slot, kind);
-    sts32(slot + 4, nrows);
-    sts32(slot + 8, int32_t(s1));
-    sts32(slot + 12, int32_t(s2));
-    sts32(slot + 16, int32_t(xs));
-    sts32(slot + 20, int32_t(dw));
-    sts32(slot + 24, kpos1);
-    sts32(slot + 28, kpos2);
-}
-// 4-row groups g0, g0 + gs, ... of a dependency update (the destination words are
-// padded to whole groups with the block's spare row)
-__device__ __forceinline__ void team_groups(int kind, unsigned s1, unsigned s2, unsigned xs, unsigned dw, int nrows,
-                                            double m1, double m2, int g0, int gs, unsigned RB) {
-    const int last = nrows - 1;
-#pragma unroll 1
-    for (int q = g0 * 4; q < nrows; q += gs * 4) {
-        const int32_t v0 = lds32(dw + unsigned(q >> 1) * 4u), v1 = lds32(dw + unsigned((q >> 1) + 1) * 4u);
-        const unsigned d0 = row_lo(xs, v0, RB), d1 = row_hi(xs, v0, RB);
-        const unsigned d2 = row_lo(xs, v1, RB), d3 = row_hi(xs, v1, RB);
-        const int q1 = min(q + 1, last), q2 = min(q + 2, last), q3 = min(q + 3, last);
-        if (kind == 2) {
-            const double a0 = lds(s1 + unsigned(q + 1) * RB), a1 = lds(s1 + unsigned(q1 + 1) * RB);
-            const double a2 = lds(s1 + unsigned(q2 + 1) * RB), a3 = lds(s1 + unsigned(q3 + 1) * RB);
-            const double b0 = lds(s2 + unsigned(q) * RB), b1 = lds(s2 + unsigned(q1) * RB);
-            const double b2 = lds(s2 + unsigned(q2) * RB), b3 = lds(s2 + unsigned(q3) * RB);
-            double x0 = lds(d0), x1 = lds(d1), x2 = lds(d2), x3 = lds(d3);
-            x0 = fma(-m2, b0, fma(-m1, a0, x0));
-            x1 = fma(-m2, b1, fma(-m1, a1, x1));
-            x2 = fma(-m2, b2, fma(-m1, a2, x2));
-            x3 = fma(-m2, b3, fma(-m1, a3, x3));
-            sts(d0, x0);
-            sts(d1, x1);
-            sts(d2, x2);
-            sts(d3, x3);
-        } else {
-            const double l0 = lds(s1 + unsigned(q) * RB), l1 = lds(s1 + unsigned(q1) * RB);
-            const double l2 = lds(s1 + unsigned(q2) * RB), l3 = lds(s1 + unsigned(q3) * RB);
-            double x0 = lds(d0), x1 = lds(d1), x2 = lds(d2), x3 = lds(d3);
-            x0 = fma(-m1, l0, x0);
-            x1 = fma(-m1, l1, x1);
-            x2 = fma(-m1, l2, x2);
-            x3 = fma(-m1, l3, x3);
-            sts(d0, x0);
-            sts(d1, x1);
-            sts(d2, x2);
-            sts(d3, x3);
-        }
-    }
-}
-// a helper warp: serve the leader's jobs until it ends the phase
-__device__ __noinline__ void team_help(const Prog& P, int leader, int tsize, int idx, unsigned le8, unsigned RB) {
-    const unsigned slot = P.slot0 + unsigned(leader) * P.slot_stride;
-    for (;;) {
-        team_bar(1 + leader, 32 * tsize);
-        const int kind = lds32(slot);
-        if (kind == 0) break;
-        const int nrows = lds32(slot + 4);
-        const unsigned s1 = unsigned(lds32(slot + 8)) + le8, s2 = unsigned(lds32(slot + 12)) + le8;
-        const unsigned xs = unsigned(lds32(slot + 16)) + le8, dw = unsigned(lds32(slot + 20));
-        const double m1 = lds(xs + unsigned(lds32(slot + 24)) * RB);
-        const double m2 = kind == 2 ? lds(xs + unsigned(lds32(slot + 28)) * RB) : 0.0;
-        team_groups(kind, s1, s2, xs, dw, nrows, m1, m2, idx, tsize, RB);
-        team_bar(1 + leader, 32 * tsize);
-    }
-}
-
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
 // Shared rows are addressed as 32-bit shared-window offsets: row r of this
 // lane at R0 + r * 256.
@@ -576,9 +468,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
     double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const double stol = v.singular_tol;
     const unsigned RB = unsigned(TW) * 8u;  // bytes per shared / tape row
-    const unsigned le8 = unsigned(le) * 8u;
-    const unsigned R0 = smem_u32(P.R) + le8;
-    int team = 1;  // warps in this walker's team in the current phase (kRecTeam)
+    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
     bool flagged = false;
     unsigned xs = R0;  // this step's block
     int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
@@ -623,19 +513,8 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             sts(p2, m2);
             const int32_t* dw = r + 6;
             const int last = nrows - 1;
-            int qend = nrows;
-            if (team > 1 && nrows >= v.team_min) {  // the team shares the row groups
-                if (lane == 0)
-                    team_post(P.slot0 + unsigned(warp) * P.slot_stride, 2, nrows, s1 - le8, s2 - le8, xs - le8,
-                              smem_u32(dw), w1 & 0xffff, int(unsigned(w1) >> 16));
-                __syncwarp();
-                team_bar(1 + warp, 32 * team);
-                team_groups(2, s1, s2, xs, smem_u32(dw), nrows, m1, m2, 0, team, RB);
-                team_bar(1 + warp, 32 * team);
-                qend = 0;
-            }
 #pragma unroll 1
-            for (int q = 0; q < qend; q += 4) {
+            for (int q = 0; q < nrows; q += 4) {
                 const int32_t v0 = dw[q >> 1], v1 = dw[(q >> 1) + 1];
                 const unsigned d0 = row_lo(xs, v0, RB), d1 = row_hi(xs, v0, RB);
                 const unsigned d2 = row_lo(xs, v1, RB), d3 = row_hi(xs, v1, RB);
@@ -679,16 +558,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
                 fl = lds(src + unsigned(fspos) * RB);
                 fy = lds(R0 + unsigned(ysrc) * RB);
             }
-            if (nrows > 0 && team > 1 && nrows >= v.team_min) {  // the team shares the row groups
-                const double mult = lds(xs + unsigned(kpos_fs & 0xffff) * RB);
-                if (lane == 0)
-                    team_post(P.slot0 + unsigned(warp) * P.slot_stride, 1, nrows, src - le8, 0u, xs - le8,
-                              smem_u32(r + 4), kpos_fs & 0xffff, 0);
-                __syncwarp();
-                team_bar(1 + warp, 32 * team);
-                team_groups(1, src, 0u, xs, smem_u32(r + 4), nrows, mult, 0.0, 0, team, RB);
-                team_bar(1 + warp, 32 * team);
-            } else if (nrows > 0) {
+            if (nrows > 0) {
                 const double mult = lds(xs + unsigned(kpos_fs & 0xffff) * RB);
                 const int32_t* dw = r + 4;
                 int q = 0;
@@ -946,23 +816,9 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1;
-        } else if (type == kRecTeam) {
-            const int tsize = (h >> 9) & 15;
-            P.cur += 1;
-            h = P.cur[0];
-            if ((P.cur[-1] >> 4) & 1)  // a helper: serve the leader until its phase ends
-                team_help(P, (P.cur[-1] >> 5) & 15, tsize, (P.cur[-1] >> 13) & 15, le8, RB);
-            else
-                team = tsize;
         } else if (type == kRecSync) {
             walk_trace(v, tile, warp, lane, 0);
             PROF_MARK(8)
-            if (team > 1) {  // release the helpers
-                if (lane == 0) sts32(P.slot0 + unsigned(warp) * P.slot_stride, 0);
-                __syncwarp();
-                team_bar(1 + warp, 32 * team);
-                team = 1;
-            }
             __syncthreads();  // phase boundary: every walker's columns are written and fenced
             PROF_MARK(3)
             PROF_FLUSH
@@ -975,11 +831,6 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             walk_trace(v, tile, warp, lane, 1);
             PROF_MARK(8)
             PROF_FLUSH
-            if (team > 1) {  // release the helpers
-                if (lane == 0) sts32(P.slot0 + unsigned(warp) * P.slot_stride, 0);
-                __syncwarp();
-                team_bar(1 + warp, 32 * team);
-            }
             break;
         }
     }
@@ -1196,8 +1047,7 @@ unsigned n_groups8(const DevView& v) { return unsigned((v.n_tasks + 32 * kSuper 
 
 size_t walk_smem_bytes(const WalkView& w) {
     return size_t(w.rows) * size_t(w.tw) * 8 +
-           size_t(w.walkers) *
-               (size_t(kWalkPages) * w.page_words * 4 + size_t(kWalkBars + kWalkPages + kTeamSlotWords) * 8);
+           size_t(w.walkers) * (size_t(kWalkPages) * w.page_words * 4 + size_t(kWalkBars + kWalkPages) * 8);
 }
 
 template <class K>

@@ -59,7 +59,6 @@ struct DevView {
     int32_t max_iter;
     int32_t jpolicy;                // gbnr_options.jacobian
     int32_t dbg;                    // experiment switches (GBNR_DBG), 0 in production
-    int32_t team_min;               // rows from which a walker's team shares a dependency update
     unsigned long long* prof;       // walker time breakdown (GBNR_PROF builds), else null
     // per-tile, per-walker global scratch of the forward walk's global steps (columns
     // too large for shared memory): walker w of tile t at (t * 8 + w) * scratch_rows rows

@@ -235,8 +235,6 @@ struct gbnr_plan {
         owned.push_back(itd);
         v.it_dev = itd;
         if (const char* d = std::getenv("GBNR_DBG")) v.dbg = std::atoi(d);
-        v.team_min = 24;  // rows; GBNR_TEAM_MIN overrides (a large value disables the teams)
-        if (const char* e = std::getenv("GBNR_TEAM_MIN")) v.team_min = std::atoi(e);
 #ifdef GBNR_PROF
         if (v.dbg & 8) {
             v.prof = static_cast<unsigned long long*>(dmalloc(4 * 8 * 16 * sizeof(unsigned long long)));

@@ -906,8 +906,7 @@ Geometry geometry(const Symbolic& s, const WalkConfig& cfg, int32_t walkers) {
     }
     // longer records than a page of kMaxPageWords go global (their forms split)
     const int32_t W = std::min(std::max(cfg.page_words, 4 * ((longest + 1 + 3) / 4)), kMaxPageWords);
-    const int64_t fixed =
-        int64_t(walkers) * (int64_t(cfg.pages) * W * 4 + int64_t(cfg.barriers + cfg.pages + kTeamSlotWords) * 8);
+    const int64_t fixed = int64_t(walkers) * (int64_t(cfg.pages) * W * 4 + int64_t(cfg.barriers + cfg.pages) * 8);
     const int64_t rows = (int64_t(cfg.smem_budget) - fixed) / cfg.row_bytes;
     return Geometry{W, int32_t(std::max<int64_t>(rows, 0))};
 }
@@ -997,27 +996,6 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
         int32_t active = 0;
         for (const auto& l : phases[ph].lists) active += !l.empty();
         const int32_t share = active > 0 ? g.rows / active : g.rows;
-        // teams (forward walk): the idle warps of this phase dealt round-robin to the
-        // walkers; kRecTeam announces each warp's role at the start of its phase
-        if (forward && active > 0 && active < walkers && cfg.teams) {
-            std::vector<int32_t> leaders, size(walkers, 1);
-            for (int32_t w = 0; w < walkers; ++w)
-                if (!phases[ph].lists[w].empty()) leaders.push_back(w);
-            std::vector<int32_t> lead_of(walkers, -1), idx(walkers, 0);
-            int32_t h = 0;
-            for (int32_t w = 0; w < walkers; ++w) {
-                if (!phases[ph].lists[w].empty()) continue;
-                const int32_t l = leaders[size_t(h++) % leaders.size()];
-                lead_of[w] = l;
-                idx[w] = size[l]++;
-            }
-            for (int32_t w = 0; w < walkers; ++w) {
-                if (lead_of[w] >= 0)
-                    em[w].emit({kRecTeam | (1 << 4) | (lead_of[w] << 5) | (size[lead_of[w]] << 9) | (idx[w] << 13)});
-                else if (size[w] > 1)
-                    em[w].emit({kRecTeam | (w << 5) | (size[w] << 9)});
-            }
-        }
         int32_t slot = 0;
         for (int32_t w = 0; w < walkers; ++w) {
             const std::vector<int32_t>& list = phases[ph].lists[w];

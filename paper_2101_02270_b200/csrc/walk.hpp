@@ -94,7 +94,6 @@ struct WalkConfig {
                                   // of it (tests; columns that cannot be planned in shared
                                   // memory go global regardless)
     std::vector<int32_t> levels;  // walkers per level (empty: walkers, walkers/2, ..., 1)
-    bool teams = true;            // idle warps of a phase help its walkers (kRecTeam)
     bool unified = true;          // blocks and fetches share one pool (plan_unified;
                                   // the split ring / staging plan where it is infeasible)
 };
@@ -135,15 +134,8 @@ enum : int32_t {
     kRecEndU = 13,
     // bwd: 14 | n << 4, b-tape rows of x_k [n] (global row block, x_k from the b tape)
     kRecDepNG = 14,
-    // fwd, phases with fewer walkers than warps: the idle warps join a walker's team
-    // and take a share of the rows of its long dependency updates (kernel-side row
-    // threshold).  15 | role << 4 | leader << 5 | team << 9 | index << 13; role 0 =
-    // the walker itself (team = its team size), 1 = a helper (leader, team size, its
-    // index in the team).  A helper serves jobs until the leader's phase ends.
-    kRecTeam = 15,
 };
 constexpr int32_t kMaxPageWords = 256;  // longer records are split (global forms)
-constexpr int32_t kTeamSlotWords = 4;   // 8-byte words per walker: its team job slot
 
 // One verified single-walker program (one walker in one phase).
 struct Walk {
@@ -170,7 +162,7 @@ struct WalkSet {
     int32_t scratch_rows = 0;       // per-tile global scratch rows (forward global steps)
     size_t smem_bytes() const {
         return size_t(rows) * size_t(row_bytes) +
-               size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages + kTeamSlotWords) * 8);
+               size_t(walkers) * (size_t(pages) * page_words * 4 + size_t(barriers + pages) * 8);
     }
 };
 

@@ -83,7 +83,7 @@ def sequential(ex, A, b):
 
 
 REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC, REC_DEP2, REC_DEPN = 1, 2, 3, 4, 5, 6, 7, 8, 9
-REC_STEPG, REC_DEPG, REC_ENDG, REC_ENDU, REC_DEPNG, REC_TEAM = 10, 11, 12, 13, 14, 15
+REC_STEPG, REC_DEPG, REC_ENDG, REC_ENDU, REC_DEPNG = 10, 11, 12, 13, 14
 
 
 class Machine:
@@ -151,8 +151,6 @@ def run_phases(w, tapes, step_fn):
                     m.off += m.issue(r)
                 elif t == REC_PAGE:
                     m.next_page()
-                elif t == REC_TEAM:  # team roles only split row work: a no-op for the replay
-                    m.off += 1
                 elif t == REC_SYNC:
                     m.off += 1
                     break
