@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--tasks", type=int, default=10000, help="tasks per GPU (weak scaling)")
     ap.add_argument("--total-tasks", type=int, default=0, help="strong scaling: total tasks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget")
-    ap.add_argument("--e2e-steps", type=int, default=10,
-                    help="batches in the pipelined e2e call (10 x 10k = the 100k-scenario job of configs[4])")
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="batches in the pipelined e2e call (0 = --steps, at least 10: every step one "
+                         "10k batch in, its voltages out)")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -298,7 +299,7 @@ def main():
     ins = [(pin(p0), pin(q0)), (pin(pb), pin(qb))]
     outs = [S.TaskResults(pin(np.empty((n, T))), pin(np.empty((n, T))), np.empty(T, np.int32),
                           np.empty(T, np.uint8), np.empty(T, np.int32), np.empty(T)) for _ in range(2)]
-    K = max(a.e2e_steps, 1)
+    K = max(a.e2e_steps, 1) if a.e2e_steps > 0 else max(a.steps, 10)
     P = C.c_void_p * K
     arr = lambda xs: P(*[x.ctypes.data for x in xs])  # noqa: E731
     sel = [i % 2 for i in range(K)]
