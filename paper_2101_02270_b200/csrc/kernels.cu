@@ -369,7 +369,7 @@ __device__ __forceinline__ void walk_trace(const DevView& v, int tile, int warp,
 #define PROF_FLUSH                                                                          \
     if (v.prof && lane == 0) {                                                              \
         for (int i_ = 0; i_ < 12; ++i_)                                                     \
-            atomicAdd(v.prof + (size_t(pf_ph) * 8 + warp) * 16 + i_, (unsigned long long)pf[i_]); \
+            if (warp < 8) atomicAdd(v.prof + (size_t(pf_ph) * 8 + warp) * 16 + i_, (unsigned long long)pf[i_]); \
         for (int i_ = 0; i_ < 12; ++i_) pf[i_] = 0;                                         \
     }
 #else
@@ -458,7 +458,7 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 // lane at R0 + r * 256.
 // TW_: the tile width as a compile-time constant (8 / 16 / 24 / 32), 0 = from the view.
 template <bool FS, int TW_>
-__global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) {
+__global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, WalkView w) {
     const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(256, 3) lu_walk_kernel(DevView v, WalkView w) 
             brow = r[4];
             h = r[5];
             P.cur += 5;
-            xg = v.scratch + (size_t(tile) * 8 + warp) * size_t(v.scratch_rows) * TW + le;
+            xg = v.scratch + (size_t(tile) * kLuWarps + warp) * size_t(v.scratch_rows) * TW + le;
             const double* at = v.A + size_t(tile) * v.tstride + le + size_t(a0) * TW;
             int z = 0;
 #pragma unroll 1

@@ -77,6 +77,10 @@ struct WalkView {
 // Most backward-walk warps per CTA (its kernel's launch bound).  12 warps fit three
 // CTAs per SM at 56 registers but ran no faster than 8 at 78 (profiles/r02q_bs_walkers.log).
 constexpr int kBsWarps = 8;
+#ifndef GBNR_LU_WARPS
+#define GBNR_LU_WARPS 8
+#endif
+constexpr int kLuWarps = GBNR_LU_WARPS;  // most forward-walk warps per CTA (its kernel's launch bound)
 
 size_t walk_smem_bytes(const WalkView& w);
 void configure_kernels();

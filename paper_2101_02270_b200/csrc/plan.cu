@@ -503,7 +503,8 @@ struct gbnr_plan {
         v.tile_active = static_cast<int32_t*>(alloc(lanes * sizeof(int32_t)));  // >= tiles at any width
         // global scratch of the forward walks' global steps (columns too large for
         // a walker's shared-memory pool), 8 walkers per tile
-        v.scratch = scratch_rows > 0 ? static_cast<double*>(alloc(lanes * 8 * size_t(scratch_rows) * 8)) : nullptr;
+        v.scratch = scratch_rows > 0 ? static_cast<double*>(alloc(lanes * gbnr::kLuWarps * size_t(scratch_rows) * 8))
+                                     : nullptr;
         v.active_count = static_cast<int32_t*>(alloc(128 * sizeof(int32_t)));
         cap_lanes = lanes;
         cap_scratch = scratch_rows;
@@ -1427,7 +1428,7 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         if (!(p->opt.tol > 0.0) || p->opt.max_iter < 1 || p->opt.max_iter > 30)
             throw Error(GBNR_ECONFIG, "need tol > 0 and 1 <= max_iter <= 30");
         if (p->opt.ring_rows < 0 || p->opt.stage_rows < 0 || p->opt.prefetch < 0 || p->opt.headroom < 0 ||
-            p->opt.walkers < 0 || p->opt.walkers > 8)
+            p->opt.walkers < 0 || p->opt.walkers > gbnr::kLuWarps)
             throw Error(GBNR_ECONFIG, "negative walk parameter");
         if (p->opt.jacobian < 0 || p->opt.jacobian > 2) throw Error(GBNR_ECONFIG, "jacobian policy must be 0, 1 or 2");
         if (p->opt.second_chance < 0) throw Error(GBNR_ECONFIG, "second_chance must be >= 0");
