@@ -903,6 +903,51 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
         } else if (type == kRecPage) {
             prog_next_page(P, lane);
             h = P.cur[0];
+        } else if (type == kRecPair) {
+            // two independent rows A, B: their dependency chains interleave (each
+            // accumulator sees its own row's operations in the unpaired order)
+            const int nA = (h >> 4) & 0xfff, nw = (h >> 16) & 0xff;
+            const int32_t wa = r[1], wb = r[2], bra = r[3], brb = r[4], ops = r[5], nB = r[6];
+            const int32_t* ya = r + 7 + nw;
+            const int32_t* yb = ya + ((nA + 1) >> 1);
+            h = yb[(nB + 1) >> 1];
+            if ((ops & 0xffff) != 0) prog_wait(P, (ops & 0xffff) - 1);
+            if ((unsigned(ops) >> 16) != 0) prog_wait(P, int(unsigned(ops) >> 16) - 1);
+            for (int i = 0; i < nw; ++i) prog_wait(P, r[7 + i] - 1);
+            const unsigned ba = R0 + unsigned(wa & 0xffff) * RB, bb = R0 + unsigned(wb & 0xffff) * RB;
+            const unsigned nea = unsigned(wa) >> 16, neb = unsigned(wb) >> 16;
+            double acca = lds(ba + nea * RB), accb = lds(bb + neb * RB);
+            unsigned ea = ba, eb = bb;
+            const int m = min(nA, nB);
+            int i = 0;
+#pragma unroll 1
+            for (; i < m; ++i) {
+                const int32_t pa = ya[i >> 1], pb = yb[i >> 1];
+                const double xa = lds((i & 1) ? row_hi(R0, pa, RB) : row_lo(R0, pa, RB));
+                const double xb = lds((i & 1) ? row_hi(R0, pb, RB) : row_lo(R0, pb, RB));
+                const double ua = lds(ea), ub = lds(eb);
+                acca = fma(-ua, xa, acca);
+                accb = fma(-ub, xb, accb);
+                ea += RB;
+                eb += RB;
+            }
+            for (int j = i; j < nA; ++j) {
+                const int32_t pa = ya[j >> 1];
+                acca = fma(-lds(ea), lds((j & 1) ? row_hi(R0, pa, RB) : row_lo(R0, pa, RB)), acca);
+                ea += RB;
+            }
+            for (int j = i; j < nB; ++j) {
+                const int32_t pb = yb[j >> 1];
+                accb = fma(-lds(eb), lds((j & 1) ? row_hi(R0, pb, RB) : row_lo(R0, pb, RB)), accb);
+                eb += RB;
+            }
+            const double xa = acca / lds(ba + (nea + 1) * RB), xb = accb / lds(bb + (neb + 1) * RB);
+            sts(ba + nea * RB, xa);
+            sts(bb + neb * RB, xb);
+            b_t[size_t(bra) * TW] = xa;
+            b_t[size_t(brb) * TW] = xb;
+            fence_proxy_async_global();
+            P.cur = yb + ((nB + 1) >> 1);
         } else if (type == kRecStepG) {
             // a row too long for the pool: its block read in place from the LU tape
             ne = r[1];

@@ -1454,6 +1454,7 @@ static int create_plan(int32_t n_bus, const int32_t* indptr, const int32_t* indi
         if (const char* e = std::getenv("GBNR_STAGE_FRAC_UP")) wc.stage_frac_up = std::atof(e);
         if (const char* e = std::getenv("GBNR_PAGE_WORDS")) wc.page_words = std::atoi(e);
         if (const char* e = std::getenv("GBNR_UNIFIED")) wc.unified = std::atoi(e) != 0;  // 0: split plans
+        if (const char* e = std::getenv("GBNR_PAIRS")) wc.pairs = std::atoi(e) != 0;      // 0: no row pairs
         if (const char* e = std::getenv("GBNR_SMEM_BUDGET")) wc.smem_budget = std::atoi(e);
         if (const char* e = std::getenv("GBNR_BALANCE")) wc.balance = std::atof(e);
         // tests: also move blocks larger than this share of a walker's pool to global memory

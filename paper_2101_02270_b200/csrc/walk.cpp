@@ -207,6 +207,7 @@ Walk plan(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         for (size_t d = 0; d < si.deps.size(); ++d) {
             DepIn& di = si.deps[d];
             WDep dr = di.rec;
+            dr.prod = di.producer;
             dr.op = -1;
             if (di.global) {
                 dr.src = dr.ysrc = -1;
@@ -485,6 +486,7 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
             for (const DepIn& di : si.deps) {
                 if (!di.global) throw Error(3, "walk: a global step with a staged dependency");
                 WDep dr = di.rec;
+            dr.prod = di.producer;
                 dr.op = -1;
                 dr.src = dr.ysrc = -1;
                 dr.global = 1;
@@ -551,6 +553,7 @@ Walk plan_unified(std::vector<StepIn>& steps, const PlanCfg& cfg) {
         for (size_t d = 0; d < si.deps.size(); ++d) {
             DepIn& di = si.deps[d];
             WDep dr = di.rec;
+            dr.prod = di.producer;
             dr.op = -1;
             const int32_t pr = di.producer;
             if (di.global) {
@@ -725,7 +728,7 @@ bool pairable(const Walk& w, const WDep& e, const WDep& f, int64_t ev_e, int32_t
 // (DEP, ISSUE*) per dependency, END, ISSUE* -- each ISSUE right after the
 // consumer event it waits for.  Op numbers continue at op_base (barrier parity
 // runs on across phases).
-void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
+void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base, bool pairs) {
     size_t next = 0;
     auto issue_upto = [&](int64_t ev) {
         while (next < w.op.size() && w.op[next].after <= ev) {
@@ -784,7 +787,50 @@ void encode(Emitter& em, const Walk& w, bool forward, int32_t op_base) {
     };
     issue_upto(-1);
     int64_t ev = 0;
-    for (const WStep& s : w.step) {
+    // backward: two consecutive rows travel as one kRecPair when the second does not
+    // depend on the first, every op either waits for is already issued, and the
+    // record fits a page (their copy issues follow the pair)
+    auto pair_record = [&](const WStep& a, const WStep& b, int32_t t) -> std::vector<int32_t> {
+        if (forward || a.global || b.global || !pairs) return {};
+        const int32_t nA = a.ndep, nB = b.ndep;
+        if (nA >= 4096 || nB >= 65536) return {};
+        std::vector<int32_t> waits;
+        auto ready = [&](int32_t op) { return op < 0 || (size_t(op) < next && opn(op) + 1 < 65536); };
+        if (!ready(a.op) || !ready(b.op)) return {};
+        for (const WStep* st : {&a, &b})
+            for (int32_t d = 0; d < st->ndep; ++d) {
+                const WDep& e = w.dep[st->dep0 + d];
+                if (st == &b && e.prod == t) return {};  // B needs A's x
+                if (e.global || e.ysrc >= 65536 || !ready(e.op)) return {};
+                if (e.op >= 0 && std::find(waits.begin(), waits.end(), opn(e.op) + 1) == waits.end())
+                    waits.push_back(opn(e.op) + 1);
+            }
+        const int32_t len = 7 + int32_t(waits.size()) + (nA + 1) / 2 + (nB + 1) / 2;
+        if (len > W - 1 || waits.size() >= 256) return {};
+        std::vector<int32_t> rec{kRecPair | (nA << 4) | (int32_t(waits.size()) << 16), a.ring | (a.len_dp << 16),
+                                 b.ring | (b.len_dp << 16), a.brow, b.brow, (opn(a.op) + 1) | ((opn(b.op) + 1) << 16),
+                                 nB};
+        rec.insert(rec.end(), waits.begin(), waits.end());
+        for (const WStep* st : {&a, &b})
+            for (int32_t i = 0; i < st->ndep; i += 2) {
+                const int32_t lo = w.dep[st->dep0 + i].ysrc;
+                const int32_t hi = i + 1 < st->ndep ? w.dep[st->dep0 + i + 1].ysrc : 0;
+                rec.push_back(lo | (hi << 16));
+            }
+        return rec;
+    };
+    for (int32_t t = 0; t < int32_t(w.step.size()); ++t) {
+        const WStep& s = w.step[t];
+        if (t + 1 < int32_t(w.step.size())) {
+            std::vector<int32_t> rec = pair_record(s, w.step[t + 1], t);
+            if (!rec.empty()) {
+                em.emit(rec);
+                const int32_t evs = s.ndep + 1 + w.step[t + 1].ndep + 1;
+                for (int32_t i = 0; i < evs; ++i) issue_upto(ev++);
+                ++t;
+                continue;
+            }
+        }
         if (forward) {
             const int32_t len = s.len_dp & 0xffff, dp = s.len_dp >> 16;
             if (s.global) {
@@ -1013,7 +1059,7 @@ WalkSet assemble(const WalkConfig& cfg, int32_t walkers, const Geometry& g, cons
                 part = plan_walker(pr, pc, cfg, g.W, forward);
                 part.dst = std::move(pr.dst);
                 part.ut = std::move(pr.ut);
-                encode(em[w], part, forward, op_base[w]);
+                encode(em[w], part, forward, op_base[w], cfg.pairs);
                 op_base[w] += static_cast<int32_t>(part.op.size());
                 ++slot;
             }

@@ -58,6 +58,7 @@ struct WDep {
     int32_t global;   // source read from global memory (too large to stage)
     int32_t gslot;    // global source: LU-tape slot of L(:,k) (fwd) / b-tape row of x_k (bwd)
     int32_t gnl;      // global source (fwd): rows of L(:,k) (y_k follows them)
+    int32_t prod = -1;  // producing step of this walker's program (-1: earlier phase / walker)
 };
 // One TMA bulk copy: nrows rows of tape `tape` from slot/row `slot` (a row is one
 // value per task of a tile: tile width x 8 bytes).
@@ -94,6 +95,7 @@ struct WalkConfig {
                                   // of it (tests; columns that cannot be planned in shared
                                   // memory go global regardless)
     std::vector<int32_t> levels;  // walkers per level (empty: walkers, walkers/2, ..., 1)
+    bool pairs = true;            // backward: independent consecutive rows in one kRecPair
     bool unified = true;          // blocks and fetches share one pool (plan_unified;
                                   // the split ring / staging plan where it is infeasible)
 };
@@ -134,6 +136,11 @@ enum : int32_t {
     kRecEndU = 13,
     // bwd: 14 | n << 4, b-tape rows of x_k [n] (global row block, x_k from the b tape)
     kRecDepNG = 14,
+    // bwd: two consecutive independent rows A, B in one record (their dependency
+    // chains interleave; every op they wait for is issued before it):
+    // 15 | nA << 4 | nw << 16, ringA | neA << 16, ringB | neB << 16, browA, browB,
+    // (opA + 1) | (opB + 1) << 16, nB, (dep op + 1) x nw, ysrc u16 pairs of A, of B
+    kRecPair = 15,
 };
 constexpr int32_t kMaxPageWords = 256;  // longer records are split (global forms)
 

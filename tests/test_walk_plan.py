@@ -83,7 +83,7 @@ def sequential(ex, A, b):
 
 
 REC_ISSUE, REC_STEP, REC_DEP, REC_END, REC_PAGE, REC_DONE, REC_SYNC, REC_DEP2, REC_DEPN = 1, 2, 3, 4, 5, 6, 7, 8, 9
-REC_STEPG, REC_DEPG, REC_ENDG, REC_ENDU, REC_DEPNG = 10, 11, 12, 13, 14
+REC_STEPG, REC_DEPG, REC_ENDG, REC_ENDU, REC_DEPNG, REC_PAIR = 10, 11, 12, 13, 14, 15
 
 
 class Machine:
@@ -285,6 +285,27 @@ def replay_backward(w, LU, b_tape):
             S.update(ring=None, ne=ne, brow=int(r[3]), gslot=slot, e=0)
             S["acc"] = LU[slot + ne].copy()
             return 4
+        if t == REC_PAIR:  # two independent rows in one record (their order is free)
+            nA, nw = (h >> 4) & 0xFFF, (h >> 16) & 0xFF
+            wa, wb, bra, brb, ops, nB = (int(x) for x in r[1:7])
+            for op in ((ops & 0xFFFF) - 1, (ops >> 16) - 1, *[int(x) - 1 for x in r[7:7 + nw]]):
+                if op >= 0:
+                    M.wait(op)
+            ya = 7 + nw
+            yb = ya + (nA + 1) // 2
+            xs = []
+            for (w_, n_, y0) in ((wa, nA, ya), (wb, nB, yb)):
+                ring, ne = w_ & 0xFFFF, w_ >> 16
+                acc = R[ring + ne].copy()
+                for i in range(n_):
+                    wq = int(r[y0 + i // 2])
+                    ysrc = (wq >> 16) & 0xFFFF if i & 1 else wq & 0xFFFF
+                    acc = acc - R[ring + i] * R[ysrc]
+                xs.append((ring, ne, acc / R[ring + ne + 1]))
+            for (ring, ne, x), br in zip(xs, (bra, brb)):
+                R[ring + ne] = x
+                b_tape[br] = x
+            return yb + (nB + 1) // 2
         if t == REC_DEPNG:
             n = (h >> 4) & 0xFFFFF
             for i in range(n):
