@@ -1369,8 +1369,50 @@ WalkSet build_backward_walk(const Symbolic& s, const LuLayout& lay, const WalkCo
         for (int32_t z = s.cp[k]; z < s.dpos[k]; ++z) urow[s.ri[z]].push_back(k);
     Geometry g;
     const Schedule sc = choose_schedule(s, cfg, g, true);
-    const std::vector<Phase> phases = make_phases(sc.level, sc.bin, sc.K, sc.levels, false);
+    std::vector<Phase> phases = make_phases(sc.level, sc.bin, sc.K, sc.levels, false);
     std::vector<int32_t> local(nJ, -1);
+    if (cfg.pairs) {
+        // zip: after each row, pull forward the first of the next 32 rows that needs
+        // neither that row nor any other row not yet walked, so consecutive rows are
+        // independent as often as possible (encode pairs them into kRecPair records).
+        // Any such order is a topological order of the row DAG.
+        std::vector<char> out(nJ, 0);
+        for (Phase& ph : phases)
+            for (std::vector<int32_t>& list : ph.lists) {
+                for (size_t t = 0; t < list.size(); ++t) local[list[t]] = int32_t(t);
+                auto ready = [&](int32_t r, int32_t without) {
+                    for (int32_t k : urow[r])
+                        if (local[k] >= 0 && (!out[k] || k == without)) return false;
+                    return true;
+                };
+                std::vector<int32_t> zipped;
+                zipped.reserve(list.size());
+                std::vector<char> taken(list.size(), 0);
+                size_t head = 0;
+                while (zipped.size() < list.size()) {
+                    while (taken[head]) ++head;
+                    const int32_t a = list[head];
+                    taken[head] = 1;
+                    zipped.push_back(a);
+                    out[a] = 1;
+                    for (size_t j = head + 1, seen = 0; j < list.size() && seen < 32; ++j) {
+                        if (taken[j]) continue;
+                        ++seen;
+                        if (ready(list[j], a)) {
+                            taken[j] = 1;
+                            zipped.push_back(list[j]);
+                            out[list[j]] = 1;
+                            break;
+                        }
+                    }
+                }
+                for (int32_t c : list) {
+                    local[c] = -1;
+                    out[c] = 0;
+                }
+                list.swap(zipped);
+            }
+    }
     auto make_program = [&](const std::vector<int32_t>& list) {
         for (size_t t = 0; t < list.size(); ++t) local[list[t]] = int32_t(t);
         Program pr;
