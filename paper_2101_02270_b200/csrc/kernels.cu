@@ -99,6 +99,16 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
 #ifndef GBNR_NPM_BATCH
 #define GBNR_NPM_BATCH 2  // neighbours whose loads are issued together in the current sweep (A/B: profiles/r02j)
 #endif
+// The sweep's A-tape stores (F and J, read back only by the next LU walk) and
+// injection loads stream past L2 (evict-first), so the gathered voltages of the
+// task group being swept stay L2-resident
+#ifndef GBNR_NPM_PLAIN
+#define NPM_ST(p, x) __stcs((p), (x))
+#define NPM_LDS(p) __ldcs(p)
+#else
+#define NPM_ST(p, x) (*(p) = (x))
+#define NPM_LDS(p) __ldg(p)
+#endif
 #ifndef GBNR_NPM_MINB
 #define GBNR_NPM_MINB 5   // resident blocks per SM the register budget is sized for
 #endif
@@ -161,13 +171,13 @@ __global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
         injection(vre, vim, ire, iim, P, Q);
         if (NPM) {
             const size_t ts = size_t(t) * v.s_inc;
-            const double fp = P - __ldg(v.p0 + size_t(r) * v.s_ld + ts);
-            a_t[size_t(__ldg(v.fslot_p + r)) * TW] = fp;  // F beside its A column
+            const double fp = P - NPM_LDS(v.p0 + size_t(r) * v.s_ld + ts);
+            NPM_ST(a_t + size_t(__ldg(v.fslot_p + r)) * TW, fp);  // F beside its A column
             nrm = fmax(nrm, nan_as_inf_abs(fp));
             const int fq_slot = __ldg(v.fslot_q + r);
             if (fq_slot >= 0) {
-                const double fq = Q - __ldg(v.q0 + size_t(r) * v.s_ld + ts);
-                a_t[size_t(fq_slot) * TW] = fq;
+                const double fq = Q - NPM_LDS(v.q0 + size_t(r) * v.s_ld + ts);
+                NPM_ST(a_t + size_t(fq_slot) * TW, fq);
                 nrm = fmax(nrm, nan_as_inf_abs(fq));
             }
         }
@@ -182,10 +192,10 @@ __global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
                 jac_z(__ldg(v.yre + size_t(q) * v.y_ld + yt), __ldg(v.yim + size_t(q) * v.y_ld + yt), vre, vim, ck, sk, zre, zim);
                 jac_entries(k == r, zre, zim, vmk, ck, sk, ire, iim, P, Q, j);
                 const int4 l = __ldg(reinterpret_cast<const int4*>(v.lk) + q);
-                if (l.x >= 0) a_t[size_t(l.x) * TW] = j[0];
-                if (l.y >= 0) a_t[size_t(l.y) * TW] = j[1];
-                if (l.z >= 0) a_t[size_t(l.z) * TW] = j[2];
-                if (l.w >= 0) a_t[size_t(l.w) * TW] = j[3];
+                if (l.x >= 0) NPM_ST(a_t + size_t(l.x) * TW, j[0]);
+                if (l.y >= 0) NPM_ST(a_t + size_t(l.y) * TW, j[1]);
+                if (l.z >= 0) NPM_ST(a_t + size_t(l.z) * TW, j[2]);
+                if (l.w >= 0) NPM_ST(a_t + size_t(l.w) * TW, j[3]);
             }
         }
     }
@@ -440,6 +450,17 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
         const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
         const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
         const char* src = P.tb + size_t(unsigned((c & 3) * P.tape_rows + slot)) * RB;
+#ifdef GBNR_TMA_HINT
+        if ((c & 3) == GBNR_TMA_HINT) {  // a tape read once per walk: evict first from L2
+            asm volatile(
+                "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+                " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}\n" ::"r"(
+                    rbase + smem * RB),
+                "l"(src), "r"(rows * RB), "r"(ubar)
+                : "memory");
+            continue;
+        }
+#endif
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 rbase + smem * RB),
