@@ -353,6 +353,7 @@ struct Prog {
     const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
     int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
     int W, n_pages, page;
+    int once_tape;              // tape whose copies the walk reads exactly once: L2 evict-first
 };
 
 // Debug timeline (GBNR_DBG & 4): kernel start (-1), phase barrier (0), end (1).
@@ -408,6 +409,7 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.cur = P.pg;
     P.tb = reinterpret_cast<const char*>(v.A + size_t(tile) * v.tstride);
     P.tape_rows = v.tape_rows;
+    P.once_tape = w.once_tape;
     mbar_init(P.bar + lane, 1);
     if (lane < kWalkPages) mbar_init(P.pbar + lane, 1);
     __syncwarp();  // every lane's barrier is initialised before lane 0 arms the page barriers
@@ -450,8 +452,7 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
         const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
         const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
         const char* src = P.tb + size_t(unsigned((c & 3) * P.tape_rows + slot)) * RB;
-#ifdef GBNR_TMA_HINT
-        if ((c & 3) == GBNR_TMA_HINT) {  // a tape read once per walk: evict first from L2
+        if ((c & 3) == P.once_tape) {  // the walk reads this tape once: evict first from L2
             asm volatile(
                 "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
                 " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}\n" ::"r"(
@@ -460,7 +461,6 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
                 : "memory");
             continue;
         }
-#endif
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 rbase + smem * RB),

@@ -71,6 +71,7 @@ struct WalkView {
     const int32_t* stream;  // program words (walk.hpp kRec*), walker-major pages
     int32_t walkers, page_words, rows;
     int32_t tw;             // tile width the program's row budget was planned for
+    int32_t once_tape;      // tape whose copies this walk reads exactly once (-1: none): L2 evict-first
     int32_t wpage0[17];     // first page of each walker's program (<= 16 walkers)
 };
 

@@ -325,10 +325,22 @@ struct gbnr_plan {
             tws->vf = upload_walk(tws->wf, tw);
             if (!sub_plan) tws->vl = upload_walk(tws->wl, tw);
             tws->vb = upload_walk(tws->wb, tw);
+            set_once_tapes(*tws);
             CK(cudaStreamSynchronize(stream));
         }
         walks.push_back(std::move(tws));
         return walks.back().get();
+    }
+
+    // L2 policy of the walk copies: the forward walks read each A-tape block once,
+    // so those copies are evict-first (room for the LU columns they re-fetch and
+    // the U rows the backward walk reads next).  Within the box noise so far
+    // (profiles/r02z_l2_hints.log); GBNR_ONCE_TAPE_LU / _BS override (-1: none).
+    static void set_once_tapes(TileWalks& t) {
+        t.vf.once_tape = t.vl.once_tape = gbnr::kTapeA;
+        t.vb.once_tape = -1;
+        if (const char* e = std::getenv("GBNR_ONCE_TAPE_BS")) t.vb.once_tape = std::atoi(e);
+        if (const char* e = std::getenv("GBNR_ONCE_TAPE_LU")) t.vf.once_tape = t.vl.once_tape = std::atoi(e);
     }
 
     // A copy of another device plan's walks (same programs), uploaded here.
@@ -342,6 +354,7 @@ struct gbnr_plan {
         tws->vf = upload_walk(tws->wf, src.tw);
         if (!sub_plan) tws->vl = upload_walk(tws->wl, src.tw);
         tws->vb = upload_walk(tws->wb, src.tw);
+        set_once_tapes(*tws);
         CK(cudaStreamSynchronize(stream));
         walks.push_back(std::move(tws));
     }
