@@ -306,27 +306,14 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
-// a barrier by its 32-bit shared-window address (computed once per walker: the
-// generic -> shared conversion needs the CTA window, an S2R, at every use)
-__device__ __forceinline__ bool mbar_try_s(unsigned b, unsigned parity) {
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
     unsigned ok;
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(b), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity)
         : "memory");
     return ok != 0;
-}
-__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
-    return mbar_try_s(smem_u32(b), parity);
-}
-// Bounded wait: a plan bug must fail loudly (trap -> CUDA error), never hang the GPU.
-__device__ __forceinline__ void mbar_wait_s(unsigned b, unsigned parity) {
-    if (mbar_try_s(b, parity)) return;
-    const long long t0 = clock64();
-    while (!mbar_try_s(b, parity)) {
-        if (clock64() - t0 > (1ll << 33)) __trap();
-    }
 }
 // Bounded wait: a plan bug must fail loudly (trap -> CUDA error), never hang the GPU.
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
@@ -366,7 +353,6 @@ struct Prog {
     const char* tb;             // this tile's tape block: A, LU, b rows (256 B each)
     int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
     int W, n_pages, page;
-    unsigned bar_s, R_s;        // shared-window addresses of the op barriers and the rows
     int once_tape;              // tape whose copies the walk reads exactly once: L2 evict-first
 };
 
@@ -416,8 +402,6 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.pg = reinterpret_cast<int32_t*>(mine);
     P.bar = reinterpret_cast<unsigned long long*>(mine + size_t(kWalkPages) * w.page_words * 4);
     P.pbar = P.bar + kWalkBars;
-    P.bar_s = smem_u32(P.bar);
-    P.R_s = smem_u32(P.R);
     P.W = w.page_words;
     P.gs = w.stream + size_t(w.wpage0[warp]) * P.W;
     P.n_pages = w.wpage0[warp + 1] - w.wpage0[warp];
@@ -463,7 +447,7 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
     if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]) * RB);  // rows -> bytes
     // one copy per lane; a copy may complete before lane 0's arrive.expect_tx (the
     // barrier's tx-count dips below zero, its phase cannot complete without the arrive)
-    const unsigned rbase = P.R_s, ubar = P.bar_s + unsigned(r[1] & (kWalkBars - 1)) * 8u;
+    const unsigned rbase = smem_u32(P.R), ubar = smem_u32(bar);
     for (int i = lane; i < ncopy; i += 32) {
         const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
         const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
@@ -487,7 +471,7 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
 }
 
 __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
-    mbar_wait_s(P.bar_s + unsigned(op & (kWalkBars - 1)) * 8u, unsigned((op / kWalkBars) & 1));
+    mbar_wait(P.bar + (op & (kWalkBars - 1)), unsigned((op / kWalkBars) & 1));
 }
 
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
