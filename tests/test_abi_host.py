@@ -46,7 +46,7 @@ def test_version_and_defaults():
     o = S.default_options()
     assert o.tol == 1e-8 and o.max_iter == 10 and o.pivot_tol == 1e-3 and o.singular_tol == 1e-14
     assert o.second_chance == 1 and o.jacobian == 0 and o.walkers == 8 and o.headroom == 1
-    assert o.n_devices == 1 and o.device_step == 1 and o.chunk_tasks == 0
+    assert o.n_devices == 1 and o.device_step == 1 and o.chunk_tasks == 0 and o.tile_width == 0
 
 
 def host_plan(name, **kw):
@@ -92,7 +92,8 @@ def test_no_cpu_fallback():
 def test_config_and_structural_errors():
     gc = load_case(util.case_path("case14"))
     for bad in (dict(max_iter=0), dict(max_iter=31), dict(jacobian=3), dict(second_chance=-1),
-                dict(walkers=9), dict(prefetch=-1), dict(n_devices=-1), dict(chunk_tasks=-2)):
+                dict(walkers=9), dict(prefetch=-1), dict(n_devices=-1), dict(chunk_tasks=-2),
+                dict(tile_width=3), dict(tile_width=34)):
         with pytest.raises(S.GbnrError) as e:
             S.NrPlan.from_case(gc, device=-1, **bad)
         assert e.value.code == 3, bad
