@@ -485,22 +485,11 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);
-    // Lanes >= tw shadow lane tw - 1: they run the same instructions but touch no
-    // shared memory (their loads read 0) and store nothing, so no shared location is
-    // ever accessed by two threads.  Shared rows are byte offsets from the walk's
-    // shared base (32-bit LDS / STS addressing).
-    const bool on = TW_ == kTile || lane < TW;
-    char* const S = reinterpret_cast<char*>(P.R);
-    auto lds = [S, on](unsigned o) -> double { return on ? *reinterpret_cast<const double*>(S + o) : 0.0; };
-    auto sts = [S, on](unsigned o, double x) {
-        if (on) *reinterpret_cast<double*>(S + o) = x;
-    };
+    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
     double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const double stol = v.singular_tol;
     const unsigned RB = unsigned(TW) * 8u;  // bytes per shared / tape row
-    const unsigned R0 = unsigned(le) * 8u;
-    bool xg_shared = true;  // the step's block (xg) is in shared memory, not the global scratch
+    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
     bool flagged = false;
     unsigned xs = R0;  // this step's block
     int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
@@ -671,7 +660,6 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
             PROF_CNT(3)
             xs = R0 + unsigned(ring) * RB;
             xg = P.R + size_t(ring) * TW + le;
-            xg_shared = true;
             acc_y = FS ? lds(xs + unsigned(len) * RB) : 0.0;
         } else if (type == kRecEnd) {
             h = r[1 + dp];
@@ -690,15 +678,15 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
                 const double l0 = x0 * inv, l1 = x1 * inv;
                 sts(xs + unsigned(z) * RB, l0);
                 sts(xs + unsigned(z + 1) * RB, l1);
-                if (on) lcol[size_t(z) * TW] = l0;
-                if (on) lcol[size_t(z + 1) * TW] = l1;
+                lcol[size_t(z) * TW] = l0;
+                lcol[size_t(z + 1) * TW] = l1;
             }
             if (z < len) {
                 const double x0 = lds(xs + unsigned(z) * RB);
                 c0 = fmax(c0, fabs(x0));
                 const double l0 = x0 * inv;
                 sts(xs + unsigned(z) * RB, l0);
-                if (on) lcol[size_t(z) * TW] = l0;
+                lcol[size_t(z) * TW] = l0;
             }
             z = 0;
             for (; z + 4 <= dp; z += 4) {  // U part -> its row-major slots
@@ -709,10 +697,10 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
                 c1 = fmax(c1, fabs(u1));
                 c0 = fmax(c0, fabs(u2));
                 c1 = fmax(c1, fabs(u3));
-                if (on) lu_t[size_t(s0) * TW] = u0;
-                if (on) lu_t[size_t(s1) * TW] = u1;
-                if (on) lu_t[size_t(s2) * TW] = u2;
-                if (on) lu_t[size_t(s3) * TW] = u3;
+                lu_t[size_t(s0) * TW] = u0;
+                lu_t[size_t(s1) * TW] = u1;
+                lu_t[size_t(s2) * TW] = u2;
+                lu_t[size_t(s3) * TW] = u3;
             }
             for (; z < dp; ++z) {
                 const double u0 = lds(xs + unsigned(z) * RB);
@@ -721,11 +709,11 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
             }
             const double cmax = fmax(c0, c1);
             flagged |= isfinite(cmax) && (piv == 0.0 || fabs(piv) < stol * cmax);
-            if (on) lu_t[size_t(brow + 1) * TW] = piv;  // U(m,m) closing the backward block
+            lu_t[size_t(brow + 1) * TW] = piv;  // U(m,m) closing the backward block
             if (FS) {  // y_m after the L rows (forward re-fetches) and in the backward block
                 sts(xs + unsigned(len) * RB, acc_y);
-                if (on) lcol[size_t(len) * TW] = acc_y;
-                if (on) lu_t[size_t(brow) * TW] = acc_y;
+                lcol[size_t(len) * TW] = acc_y;
+                lu_t[size_t(brow) * TW] = acc_y;
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1 + dp;
@@ -743,7 +731,7 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
             if (op >= 0) prog_wait(P, op);
             const double* src = lu_t + size_t(slot) * TW;
             const int fspos = int(unsigned(kpos_fs) >> 16);
-            if (nrows > 0 && (on || !xg_shared)) {
+            if (nrows > 0) {
                 const double mult = xg[size_t(kpos_fs & 0xffff) * TW];
                 const int32_t* dw = r + 5;
                 int q = 0;
@@ -762,8 +750,7 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
 #pragma unroll
                     for (int u = 0; u < 8; ++u) a[u] = xg[size_t(d[u]) * TW];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (on || !xg_shared) xg[size_t(d[u]) * TW] = fma(-mult, l[u], a[u]);
+                    for (int u = 0; u < 8; ++u) xg[size_t(d[u]) * TW] = fma(-mult, l[u], a[u]);
                 }
                 for (; q < nrows; ++q) {
                     const int32_t wq = dw[q >> 1];
@@ -783,7 +770,6 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
             h = r[5];
             P.cur += 5;
             xg = v.scratch + (size_t(tile) * kLuWarps + warp) * size_t(v.scratch_rows) * TW + le;
-            xg_shared = false;
             const double* at = v.A + size_t(tile) * v.tstride + le + size_t(a0) * TW;
             int z = 0;
 #pragma unroll 1
@@ -835,19 +821,19 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     c0 = fmax(c0, fabs(x[k]));
-                    if (on) lcol[size_t(z + k) * TW] = x[k] * inv;
+                    lcol[size_t(z + k) * TW] = x[k] * inv;
                 }
             }
             for (; z < len; ++z) {
                 const double x0 = xg[size_t(z) * TW];
                 c0 = fmax(c0, fabs(x0));
-                if (on) lcol[size_t(z) * TW] = x0 * inv;
+                lcol[size_t(z) * TW] = x0 * inv;
             }
             flagged |= isfinite(c0) && (piv == 0.0 || fabs(piv) < stol * c0);
-            if (on) lu_t[size_t(brow + 1) * TW] = piv;
+            lu_t[size_t(brow + 1) * TW] = piv;
             if (FS) {
-                if (on) lcol[size_t(len) * TW] = acc_y;
-                if (on) lu_t[size_t(brow) * TW] = acc_y;
+                lcol[size_t(len) * TW] = acc_y;
+                lu_t[size_t(brow) * TW] = acc_y;
             }
             fence_proxy_async_global();  // later TMA re-fetches of this column see it
             P.cur += 1;
@@ -869,7 +855,7 @@ __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, Wa
             break;
         }
     }
-    if (on && flagged && v.active[tile * TW + le]) v.flag[tile * TW + le] = 1;
+    if (flagged && v.active[tile * TW + le]) v.flag[tile * TW + le] = 1;
 }
 
 // Backward walk: x_i = (y_i - sum_k U(i,k) x_k) / U(i,i), k descending.
@@ -881,18 +867,11 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
-    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);
-    // lanes >= tw shadow lane tw - 1 without touching shared memory or storing (as in the forward walk)
-    const bool on = TW_ == kTile || lane < TW;
-    char* const S = reinterpret_cast<char*>(P.R);
-    auto lds = [S, on](unsigned o) -> double { return on ? *reinterpret_cast<const double*>(S + o) : 0.0; };
-    auto sts = [S, on](unsigned o, double x) {
-        if (on) *reinterpret_cast<double*>(S + o) = x;
-    };
+    const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
     double* b_t = v.b + size_t(tile) * v.tstride + le;
     const double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const unsigned RB = unsigned(TW) * 8u;
-    const unsigned R0 = unsigned(le) * 8u;
+    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
     unsigned blk = R0, e = R0;  // this step's block; its next U entry
     const double *blk_g = lu_t, *e_g = lu_t;  // a global step's row block in the LU tape
     int ne = 0, brow = 0;
@@ -939,7 +918,7 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
             h = r[1];
             const double xi = acc / lds(blk + unsigned(ne + 1) * RB);
             sts(blk + unsigned(ne) * RB, xi);
-            if (on) b_t[size_t(brow) * TW] = xi;
+            b_t[size_t(brow) * TW] = xi;
             fence_proxy_async_global();
             P.cur += 1;
         } else if (type == kRecPage) {
@@ -986,8 +965,8 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
             const double xa = acca / lds(ba + (nea + 1) * RB), xb = accb / lds(bb + (neb + 1) * RB);
             sts(ba + nea * RB, xa);
             sts(bb + neb * RB, xb);
-            if (on) b_t[size_t(bra) * TW] = xa;
-            if (on) b_t[size_t(brb) * TW] = xb;
+            b_t[size_t(bra) * TW] = xa;
+            b_t[size_t(brb) * TW] = xb;
             fence_proxy_async_global();
             P.cur = yb + ((nB + 1) >> 1);
         } else if (type == kRecStepG) {
@@ -1021,7 +1000,7 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
             P.cur += 1 + n;
         } else if (type == kRecEndG) {
             h = r[1];
-            if (on) b_t[size_t(brow) * TW] = acc / blk_g[size_t(ne + 1) * TW];
+            b_t[size_t(brow) * TW] = acc / blk_g[size_t(ne + 1) * TW];
             fence_proxy_async_global();
             P.cur += 1;
         } else if (type == kRecSync) {
