@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
         v.s[o] = s;
         v.c[o] = c;
     }
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && lane < v.tw) {
         v.status[t] = real ? GBNR_DIVERGED : -1;
         v.iters[t] = 0;
         v.active[t] = real ? 1 : 0;
@@ -66,9 +66,11 @@ __global__ void __launch_bounds__(256) init_kernel(DevView v) {
         v.mis_prev[t] = INFINITY;
         v.jskip[t] = 0;
         v.norm_bits[t] = 0ull;
+        if (t == 0) *v.it_dev = 0;
+    }
+    if (blockIdx.x == 0) {
         const int cnt = __popc(__ballot_sync(kFull, real && lane < v.tw));
         if (lane == 0) v.tile_active[tile] = cnt;
-        if (t == 0) *v.it_dev = 0;
     }
 }
 
@@ -211,8 +213,9 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
     const int t = tile * v.tw + min(lane, v.tw - 1);
     const int it = *v.it_dev;
     const double m = __longlong_as_double(static_cast<long long>(v.norm_bits[t]));
-    v.norm_bits[t] = 0ull;
-    bool act = v.tile_active[tile] != 0 && v.active[t] != 0;
+    // shadow lanes only read: the real lane owns every write of task t
+    bool act = in && v.tile_active[tile] != 0 && v.active[t] != 0;
+    if (in) v.norm_bits[t] = 0ull;
     if (act) {
         if (it == 0) v.mis0[t] = m;
         v.mis_prev[t] = v.maxmis[t];
@@ -229,8 +232,8 @@ __global__ void __launch_bounds__(256) conv_kernel(DevView v) {
             act = false;
         }
     }
-    const int cnt = __popc(__ballot_sync(kFull, act && in));
-    const int nj = __popc(__ballot_sync(kFull, act && in && v.jskip[t] != 0));
+    const int cnt = __popc(__ballot_sync(kFull, act));
+    const int nj = __popc(__ballot_sync(kFull, act && v.jskip[t] != 0));
     if (lane == 0) {
         v.tile_active[tile] = cnt;
         if (cnt) {
@@ -1059,8 +1062,8 @@ __global__ void __launch_bounds__(256) flows_kernel(DevView v, int32_t nb, const
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.y * kSuper + warp;
     if (tile >= v.n_tiles) return;
-    const int t = tile * v.tw + min(lane, v.tw - 1);
-    if (t >= v.n_tasks) return;
+    const int t = tile * v.tw + lane;
+    if (lane >= v.tw || t >= v.n_tasks) return;
     const size_t bp = v.bpad, T = size_t(v.n_tasks);
     const int out = outage ? outage[t] : -1;
     const int k1 = min(nb, int(blockIdx.x + 1) * 32);
