@@ -1022,6 +1022,9 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
 // V update for active tasks: va -= dtheta, vm -= d|V|; refresh (cos, sin).
 // block (32-bus chunk, super-tile), warp = tile.
 // ---------------------------------------------------------------------------
+#ifndef GBNR_VUP_BATCH
+#define GBNR_VUP_BATCH 8  // buses per load batch (A/B: profiles/r02ff)
+#endif
 template <int TW_>
 __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1038,19 +1041,43 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     }
     const size_t bp = v.bpad;
     const double* b_t = v.b + size_t(t / TW) * v.tstride + (t % TW);  // tile-blocked b tape
-    const int b1 = min(v.n, int(blockIdx.x + 1) * 32);
-    for (int bus = blockIdx.x * 32; bus < b1; ++bus) {
-        const int zt = __ldg(v.zcol_t + bus);
-        if (zt < 0) continue;
-        const size_t o = size_t(bus) * bp + t;
-        const double va = v.va[o] - b_t[size_t(zt) * TW];
-        v.va[o] = va;
-        const int zv = __ldg(v.zcol_v + bus);
-        if (zv >= 0) v.vm[o] = v.vm[o] - b_t[size_t(zv) * TW];
-        double s, c;
-        gb_sincos(va, &s, &c);
-        v.s[o] = s;
-        v.c[o] = c;
+    const int b0 = blockIdx.x * 32, b1 = min(v.n, b0 + 32);
+    // VB buses' loads in flight per warp before their updates (the loop is
+    // latency-bound at one bus per round trip otherwise)
+    constexpr int VB = GBNR_VUP_BATCH;
+    for (int bus = b0; bus < b1; bus += VB) {
+        int zt[VB], zv[VB];
+        double va[VB], vm[VB], dt[VB], dv[VB];
+#pragma unroll
+        for (int u = 0; u < VB; ++u) {
+            const bool in = bus + u < b1;
+            zt[u] = in ? __ldg(v.zcol_t + bus + u) : -1;
+            zv[u] = in ? __ldg(v.zcol_v + bus + u) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < VB; ++u) {
+            const size_t o = size_t(bus + u) * bp + t;
+            if (zt[u] >= 0) {
+                va[u] = v.va[o];
+                dt[u] = b_t[size_t(zt[u]) * TW];
+            }
+            if (zt[u] >= 0 && zv[u] >= 0) {
+                vm[u] = v.vm[o];
+                dv[u] = b_t[size_t(zv[u]) * TW];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < VB; ++u) {
+            if (zt[u] < 0) continue;
+            const size_t o = size_t(bus + u) * bp + t;
+            const double a = va[u] - dt[u];
+            v.va[o] = a;
+            if (zv[u] >= 0) v.vm[o] = vm[u] - dv[u];
+            double s, c;
+            gb_sincos(a, &s, &c);
+            v.s[o] = s;
+            v.c[o] = c;
+        }
     }
 }
 

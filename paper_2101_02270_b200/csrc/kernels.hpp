@@ -12,7 +12,10 @@ namespace gbnr {
 
 constexpr int kTile = 32;      // most tasks per tile = lanes of a warp (DevView::tw: the batch's tile width)
 constexpr int kSuper = 8;      // tiles per super-tile = warps per block (2 KB access runs)
-constexpr int kRowChunk = 4;  // Ybus rows per warp in the NPM / Jacobian kernels
+#ifndef GBNR_ROW_CHUNK
+#define GBNR_ROW_CHUNK 4
+#endif
+constexpr int kRowChunk = GBNR_ROW_CHUNK;  // Ybus rows per warp in the NPM / Jacobian kernels
 
 // Everything a kernel needs, by value (device pointers + sizes).  All per-task
 // tapes are element-major: value(elem, task) at elem * bpad + task.
