@@ -114,6 +114,9 @@ __device__ __forceinline__ bool predict_converged(const DevView& v, int t) {
 #ifndef GBNR_NPM_MINB
 #define GBNR_NPM_MINB 5   // resident blocks per SM the register budget is sized for
 #endif
+#ifndef GBNR_JSKIP_LANE
+#define GBNR_JSKIP_LANE 0
+#endif
 template <bool NPM, int JMODE, int TW_>
 __global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -127,7 +130,15 @@ __global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
     const size_t yt = size_t(t) * v.y_inc;  // this task's Ybus value set
     bool act = JMODE != kJacNone && v.active[t] != 0;
     if (JMODE == kJacSpec) {
+        // skipped per warp: only when every active task of the 32 is predicted to
+        // converge.  A lane skipping alone would leave holes in the warp's J stores,
+        // and the partial sectors cost their L2 fills from HBM (+1.5 GB, +1.8 ms in
+        // the sweep where some tasks converge; profiles/r02jj)
+#if GBNR_JSKIP_LANE
         const bool skip = act && predict_converged(v, t);
+#else
+        const bool skip = act && __all_sync(kFull, !act || predict_converged(v, t));
+#endif
         act = act && !skip;
         if (blockIdx.x == 0) v.jskip[t] = skip;
     } else if (JMODE == kJacFix) {
