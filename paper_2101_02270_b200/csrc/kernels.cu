@@ -137,13 +137,20 @@ __global__ void __launch_bounds__(256, GBNR_NPM_MINB) npm_kernel(DevView v) {
 #if GBNR_JSKIP_LANE
         const bool skip = act && predict_converged(v, t);
 #else
-        const bool skip = act && __all_sync(kFull, !act || predict_converged(v, t));
+        const bool all_pred = __all_sync(kFull, !act || predict_converged(v, t));  // every lane votes
+        const bool skip = act && all_pred;
 #endif
         act = act && !skip;
         if (blockIdx.x == 0) v.jskip[t] = skip;
     } else if (JMODE == kJacFix) {
         act = act && v.jskip[t] != 0;
     }
+#if !GBNR_JSKIP_LANE
+    // a warp that builds J stores it in every lane, for finished and skipped tasks
+    // too (their A rows are dead, or rebuilt bit-identically by the fix launch), so
+    // its stores fill whole sectors
+    if (JMODE != kJacNone) act = __any_sync(kFull, act);
+#endif
     if (JMODE != kJacNone && blockIdx.x == 0) v.flag[t] = 0;  // pivot flags of the coming refactorization
     if (!NPM && !__any_sync(kFull, act)) return;
     double nrm = 0.0;
@@ -1040,16 +1047,22 @@ template <int TW_>
 __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = (blockIdx.y * kSuper + warp) * 32 + lane;  // 32 consecutive tasks per warp
-    if (t >= v.n_tasks || !v.active[t]) return;
-    const int TW = TW_ ? TW_ : v.tw;
-    if (v.flag[t]) {  // frozen pivot collapsed: stop, never update V
+    const bool in = t < v.n_tasks;
+    bool upd = in && v.active[t];
+    if (upd && v.flag[t]) {  // frozen pivot collapsed: stop, never update V
         if (blockIdx.x == 0) {
             v.status[t] = GBNR_SINGULAR;
             v.iters[t] = *v.it_dev;
             v.active[t] = 0;
         }
-        return;
+        upd = false;
     }
+    // Lanes of finished tasks in a warp that updates rewrite their unchanged values
+    // (x - 0.0 == x; cos / sin recomputed from the angle, as every writer of the
+    // tapes does), so the warp's stores fill whole sectors instead of leaving
+    // holes that L2 fills from HBM
+    if (!__any_sync(kFull, upd) || !in) return;
+    const int TW = TW_ ? TW_ : v.tw;
     const size_t bp = v.bpad;
     const double* b_t = v.b + size_t(t / TW) * v.tstride + (t % TW);  // tile-blocked b tape
     const int b0 = blockIdx.x * 32, b1 = min(v.n, b0 + 32);
@@ -1070,11 +1083,11 @@ __global__ void __launch_bounds__(256) vupdate_kernel(DevView v) {
             const size_t o = size_t(bus + u) * bp + t;
             if (zt[u] >= 0) {
                 va[u] = v.va[o];
-                dt[u] = b_t[size_t(zt[u]) * TW];
+                dt[u] = upd ? b_t[size_t(zt[u]) * TW] : 0.0;
             }
             if (zt[u] >= 0 && zv[u] >= 0) {
                 vm[u] = v.vm[o];
-                dv[u] = b_t[size_t(zv[u]) * TW];
+                dv[u] = upd ? b_t[size_t(zv[u]) * TW] : 0.0;
             }
         }
 #pragma unroll
