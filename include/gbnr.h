@@ -81,8 +81,9 @@ typedef struct gbnr_options {
     int32_t headroom;      /* ring residency margin in steps (0 = 1)               */
     int32_t walkers;       /* warps per tile walking disjoint subtrees (0 = 8, <= 8) */
     int32_t jacobian;      /* when the next Jacobian is built: 0 = inside the mismatch
-                              sweep unless the task is predicted to converge at that
-                              check (a wrong guess adds a Jacobian-only launch);
+                              sweep unless every active task of its 32-task warp is
+                              predicted to converge at that check (a wrong guess adds
+                              a Jacobian-only launch);
                               1 = always inside the sweep; 2 = always after the check
                               (the reference's order).  Results are identical.        */
     int32_t second_chance; /* 1 (default): every task whose frozen pivot collapsed is
