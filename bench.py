@@ -252,6 +252,9 @@ def main():
         task0, T = rk.rank * a.tasks, a.tasks
         scaling = "weak"
     torch.cuda.init()
+    # load the library and its modules once (a case14 plan), so init_ms is the plan
+    # build of the benchmark case itself, not the process's first CUDA use
+    S.NrPlan.from_case(load_case(os.path.join(ROOT, "cases", "case14.m")), device=dev).close()
     i0 = time.perf_counter()
     plan = S.NrPlan.from_case(gc, device=dev, profile=1)  # one-time init
     init_ms = (time.perf_counter() - i0) * 1e3
@@ -372,6 +375,8 @@ def main():
                                 f"{st['nnzLU'] * 8 * T / 1e9:.1f} GB per GPU)",
                           "wall_s_timed": wall},
                "init_ms": init_ms,
+               "init_note": "one-time plan create of the case (symbolic analysis, walk programs, upload), "
+                            "excluded from value; library loaded beforehand",
                "clocks": clk.summary(),
                "e2e": {"value": e2e_conv / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "steps": K, "jobs_timed": 3, "statistic": "median",
