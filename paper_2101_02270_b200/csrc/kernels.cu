@@ -302,6 +302,26 @@ __global__ void status_count_kernel(DevView v) {
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
+// A value the compiler must keep (or spill) instead of re-deriving it: the walk
+// loops run at the 80-register cap, where ptxas otherwise rematerialises the
+// tile's tape pointers and shared addresses from SR_CTAID / SR_TID / SR_CgaCtaId
+// reads at every record dispatch.
+#ifndef GBNR_OPAQUE
+#define GBNR_OPAQUE 1
+#endif
+__device__ __forceinline__ unsigned opaque_u32(unsigned x) {
+#if GBNR_OPAQUE
+    asm volatile("mov.b32 %0, %0;\n" : "+r"(x));
+#endif
+    return x;
+}
+template <class T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+#if GBNR_OPAQUE
+    asm volatile("mov.b64 %0, %0;\n" : "+l"(p));
+#endif
+    return p;
+}
 // Shared row address of the low / high 16-bit row index of a packed word
 // (PRMT / SHF, then one shift-add for the power-of-two row sizes); RB = bytes per
 // row = tile width x 8
@@ -335,6 +355,22 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
     return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_s(unsigned a, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_s(unsigned a, unsigned parity) {
+    if (mbar_try_s(a, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_s(a, parity)) {
+        if (clock64() - t0 > (1ll << 33)) __trap();
+    }
 }
 // Bounded wait: a plan bug must fail loudly (trap -> CUDA error), never hang the GPU.
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
@@ -375,6 +411,7 @@ struct Prog {
     int32_t tape_rows;          // rows per tape: tape t starts at row t * tape_rows
     int W, n_pages, page;
     int once_tape;              // tape whose copies the walk reads exactly once: L2 evict-first
+    unsigned Rs, bars;          // shared-window addresses of R and bar (kept, not re-derived)
 };
 
 // Debug timeline (GBNR_DBG & 4): kernel start (-1), phase barrier (0), end (1).
@@ -423,6 +460,8 @@ __device__ __forceinline__ void prog_begin(const DevView& v, const WalkView& w, 
     P.pg = reinterpret_cast<int32_t*>(mine);
     P.bar = reinterpret_cast<unsigned long long*>(mine + size_t(kWalkPages) * w.page_words * 4);
     P.pbar = P.bar + kWalkBars;
+    P.Rs = opaque_u32(smem_u32(P.R));
+    P.bars = opaque_u32(smem_u32(P.bar));
     P.W = w.page_words;
     P.gs = w.stream + size_t(w.wpage0[warp]) * P.W;
     P.n_pages = w.wpage0[warp + 1] - w.wpage0[warp];
@@ -463,12 +502,14 @@ __device__ __forceinline__ void prog_next_page(Prog& P, int lane) {
 __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32_t* r, int lane, unsigned RB) {
     const int ncopy = (r[0] >> 4) & 0xfff;
     fence_proxy_async_smem();  // this lane's smem accesses before the async overwrite
-    unsigned long long* bar = P.bar + (r[1] & (kWalkBars - 1));
+    const unsigned ubar = P.bars + unsigned(r[1] & (kWalkBars - 1)) * 8u;
     __syncwarp();
-    if (lane == 0) mbar_expect_tx(bar, unsigned(r[2]) * RB);  // rows -> bytes
+    if (lane == 0)  // rows -> bytes
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(ubar), "r"(unsigned(r[2]) * RB)
+                     : "memory");
     // one copy per lane; a copy may complete before lane 0's arrive.expect_tx (the
     // barrier's tx-count dips below zero, its phase cannot complete without the arrive)
-    const unsigned rbase = smem_u32(P.R), ubar = smem_u32(bar);
+    const unsigned rbase = P.Rs;
     for (int i = lane; i < ncopy; i += 32) {
         const int32_t c = r[3 + 2 * i], slot = r[4 + 2 * i];
         const unsigned rows = (unsigned(c) >> 2) & 1023u, smem = unsigned(c) >> 12;
@@ -492,7 +533,7 @@ __device__ __forceinline__ int prog_issue(const DevView& v, Prog& P, const int32
 }
 
 __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
-    mbar_wait(P.bar + (op & (kWalkBars - 1)), unsigned((op / kWalkBars) & 1));
+    mbar_wait_s(P.bars + unsigned(op & (kWalkBars - 1)) * 8u, unsigned((op / kWalkBars) & 1));
 }
 
 // Forward walk: Alg. 2 column by column (+ forward substitution when FS).
@@ -501,16 +542,17 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 // TW_: the tile width as a compile-time constant (8 / 16 / 24 / 32), 0 = from the view.
 template <bool FS, int TW_>
 __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, WalkView w) {
-    const int tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned tid = opaque_u32(threadIdx.x);
+    const int tile = int(opaque_u32(blockIdx.x)), lane = int(tid & 31u), warp = int(tid >> 5);
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
     prog_begin(v, w, P, tile, warp, lane);
     const int TW = TW_ ? TW_ : v.tw, le = min(lane, TW - 1);  // lanes >= tw shadow lane tw - 1
-    double* lu_t = v.LU + size_t(tile) * v.tstride + le;
+    double* lu_t = opaque_ptr(v.LU + size_t(tile) * v.tstride + le);
     const double stol = v.singular_tol;
     const unsigned RB = unsigned(TW) * 8u;  // bytes per shared / tape row
-    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
+    const unsigned R0 = P.Rs + unsigned(le) * 8u;
     bool flagged = false;
     unsigned xs = R0;  // this step's block
     int len = 0, dp = 0, lslot = 0, brow = 0;  // brow: slot of y_m in the backward block
@@ -892,7 +934,7 @@ __global__ void __launch_bounds__(32 * kBsWarps, 3) bs_walk_kernel(DevView v, Wa
     double* b_t = v.b + size_t(tile) * v.tstride + le;
     const double* lu_t = v.LU + size_t(tile) * v.tstride + le;
     const unsigned RB = unsigned(TW) * 8u;
-    const unsigned R0 = smem_u32(P.R) + unsigned(le) * 8u;
+    const unsigned R0 = P.Rs + unsigned(le) * 8u;
     unsigned blk = R0, e = R0;  // this step's block; its next U entry
     const double *blk_g = lu_t, *e_g = lu_t;  // a global step's row block in the LU tape
     int ne = 0, brow = 0;
