@@ -309,6 +309,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 #ifndef GBNR_OPAQUE
 #define GBNR_OPAQUE 1
 #endif
+#ifndef GBNR_LANE_SHFL
+#define GBNR_LANE_SHFL 1  // the LU walk's lane id through a shuffle (profiles/r02pp_lane_shfl.log)
+#endif
 __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 #if GBNR_OPAQUE
     asm volatile("mov.b32 %0, %0;\n" : "+r"(x));
@@ -543,7 +546,12 @@ __device__ __forceinline__ void prog_wait(const Prog& P, int op) {
 template <bool FS, int TW_>
 __global__ void __launch_bounds__(32 * kLuWarps, 3) lu_walk_kernel(DevView v, WalkView w) {
     const unsigned tid = opaque_u32(threadIdx.x);
-    const int tile = int(opaque_u32(blockIdx.x)), lane = int(tid & 31u), warp = int(tid >> 5);
+    const int tile = int(opaque_u32(blockIdx.x)), warp = int(tid >> 5);
+#if GBNR_LANE_SHFL
+    const int lane = __shfl_sync(kFull, int(tid & 31u), int(tid & 31u));  // a register ptxas cannot re-derive
+#else
+    const int lane = int(tid & 31u);
+#endif
     if (tile >= v.n_tiles || v.tile_active[tile] == 0) return;
     Prog P;
     walk_trace(v, tile, warp, lane, -1);
